@@ -1,0 +1,112 @@
+"""fp64 CPU oracle for HadaCore's batched normalized Walsh-Hadamard transform.
+
+TEST INFRASTRUCTURE ONLY -- only ``tests/``, ``__graft_entry__.smoke()`` and
+``bench.py`` (its ``cpu_baseline`` leg and ``--impl reference``) may import this
+package.  The product path (``paper_2412_08832_b200``) never imports it, and this
+package never imports the product path: the two share no code, header, table or
+constant generator.  Only the seeded input generators (``synthetic/``, which
+holds none of the method's arithmetic) serve both.
+
+The arithmetic lives in plain C (``fwht_oracle.c``, fp64, compiled here with gcc)
+and follows /root/reference/PAPER.md:
+
+* ``fwht``        -- the FWHT listing, P:50-64 [Sec. 2.2], scale applied once at
+                     the end (reading R3).
+* ``dense_entry`` -- the definition y_l = scale * sum_j (-1)^popcount(j&l) x_j,
+                     P:41 [Sec. 2.1] + Sylvester's construction P:45 [Sec. 2.2].
+* ``dense``       -- the definition for a whole (small) matrix.
+
+Parity status: pinned (see tests/test_oracle.py and DESIGN.md "Oracle pins").
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "fwht_oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+_lib = None
+
+
+def build(force: bool = False) -> str:
+    """Compile the C oracle in-tree (gcc -O2, no fast-math: IEEE fp64)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = _LIB + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", "-O2", "-fPIC", "-shared", "-pthread", "-std=c11",
+                               "-fno-fast-math", "-o", tmp, _SRC, "-lm"])
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+def _load():
+    global _lib
+    if _lib is None:
+        lib = ctypes.CDLL(build())
+        dp = ctypes.POINTER(ctypes.c_double)
+        lib.oracle_fwht_f64.argtypes = [dp, dp, ctypes.c_int64, ctypes.c_int64, ctypes.c_double, ctypes.c_int]
+        lib.oracle_fwht_f64.restype = ctypes.c_int
+        lib.oracle_dense_f64.argtypes = [dp, dp, ctypes.c_int64, ctypes.c_int64, ctypes.c_double]
+        lib.oracle_dense_f64.restype = ctypes.c_int
+        lib.oracle_dense_entry_f64.argtypes = [dp, ctypes.c_int64, ctypes.c_int64, ctypes.c_double]
+        lib.oracle_dense_entry_f64.restype = ctypes.c_double
+        _lib = lib
+    return _lib
+
+
+def _ptr(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+
+
+def _as_f64_2d(x) -> np.ndarray:
+    a = np.ascontiguousarray(np.asarray(x, dtype=np.float64))
+    if a.ndim == 1:
+        a = a[None, :]
+    if a.ndim != 2:
+        raise ValueError("oracle expects a 2-D (m, n) matrix")
+    return a
+
+
+def default_threads() -> int:
+    return len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+
+
+def fwht(x, scale: float | None = None, threads: int | None = None) -> np.ndarray:
+    """y[i,:] = scale * H_n x[i,:] in fp64 via the P:50-64 listing (scale once at end).
+
+    ``scale`` defaults to 1/sqrt(n) (the normalized transform).
+    """
+    a = _as_f64_2d(x)
+    m, n = a.shape
+    if scale is None:
+        scale = 1.0 / np.sqrt(n)
+    out = np.empty_like(a)
+    rc = _load().oracle_fwht_f64(_ptr(a), _ptr(out), m, n, float(scale),
+                                 int(threads or default_threads()))
+    if rc != 0:
+        raise ValueError(f"oracle_fwht_f64 rejected m={m} n={n}")
+    return out
+
+
+def dense(x, scale: float | None = None) -> np.ndarray:
+    """The definition (O(m n^2)): y_l = scale * sum_j (-1)^popcount(j&l) x_j."""
+    a = _as_f64_2d(x)
+    m, n = a.shape
+    if scale is None:
+        scale = 1.0 / np.sqrt(n)
+    out = np.empty_like(a)
+    if _load().oracle_dense_f64(_ptr(a), _ptr(out), m, n, float(scale)) != 0:
+        raise ValueError(f"oracle_dense_f64 rejected m={m} n={n}")
+    return out
+
+
+def dense_entry(row, l: int, scale: float | None = None) -> float:
+    """One output of the definition for one row: scale * sum_j (-1)^popcount(j&l) row_j."""
+    a = np.ascontiguousarray(np.asarray(row, dtype=np.float64).reshape(-1))
+    n = a.shape[0]
+    if scale is None:
+        scale = 1.0 / np.sqrt(n)
+    return float(_load().oracle_dense_entry_f64(_ptr(a), n, int(l), float(scale)))
