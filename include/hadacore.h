@@ -1,0 +1,111 @@
+/*
+ * hadacore.h -- C ABI of the B200-native batched normalized Walsh-Hadamard transform
+ * (the hot path of HadaCore, arXiv 2412.08832).
+ *
+ * Citations: "P:NN" = /root/reference/PAPER.md line NN [section].
+ *
+ * The operation (P:41 [Sec. 2.1]; P:87 [Sec. 2.4] "right-Hadamard transform"):
+ *     out[i, :] = scale * H_n * in[i, :]        for every row i in [0, m)
+ * where H_n is the n x n Walsh-Hadamard matrix in natural (Sylvester) order,
+ * (H_n)[j][l] = (-1)^popcount(j & l), built by H(2k) = [[H, H], [H, -H]] (P:45
+ * [Sec. 2.2]).  H_n is symmetric, so this equals the right multiply in * H_n.
+ * `scale` is the WHOLE multiplier on the +-1 matrix: pass 1/sqrt(n) for the
+ * normalized (orthonormal) transform of P:41 ("+-1/sqrt(d) ... when normalized").
+ * n is a power of two in [2^7, 2^15] (the paper's range, P:97, P:128 [Sec. 3.2]).
+ *
+ * Layout: `in` and `out` are row-major m x n matrices of 16-bit floats (IEEE
+ * binary16 or bfloat16), contiguous, row pitch = n elements, in DEVICE memory of
+ * the current CUDA device, 16-byte aligned.  in == out (in-place, P:264-274
+ * [App. B]) is allowed and gives bit-identical results to out-of-place.
+ *
+ * Ownership: the caller owns both buffers; the library allocates nothing for
+ * hadacore_fwht, keeps no reference after the call returns, and has no global
+ * mutable state except a per-process cache of device attributes.  Buffers must
+ * stay alive until the work queued on `stream` has completed.
+ *
+ * Errors: arguments are validated synchronously, before anything is queued; on a
+ * validation error nothing is launched.  The launch is asynchronous on `stream`
+ * (no host synchronisation; safe inside CUDA-graph capture).  A launch failure
+ * returns HADACORE_ERR_CUDA and leaves the CUDA error for cudaGetLastError().
+ * Faults during execution surface at the caller's next synchronisation.
+ * No C++ exception crosses this ABI.  There is no CPU fallback: without a usable
+ * sm_100 device the call returns HADACORE_ERR_CUDA.
+ *
+ * Numerics: the internal precision is fp16 (for fp16 data) or fp32 accumulate
+ * rounded to bf16 between factor stages (for bf16 data), the final factor stage is
+ * accumulated in fp32, multiplied by `scale` (times an exact power of two) in fp32
+ * and rounded to nearest even.  Rows are independent: a
+ * non-finite value in one row never affects another row.
+ */
+#ifndef HADACORE_H_
+#define HADACORE_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Opaque to keep this header free of CUDA headers: a cudaStream_t is passed as
+ * this pointer type (cudaStream_t is itself a pointer; 0/NULL = legacy default). */
+typedef struct CUstream_st* hadacore_stream_t;
+
+typedef enum {
+  HADACORE_F16 = 0,  /* IEEE 754 binary16 */
+  HADACORE_BF16 = 1  /* bfloat16 */
+} hadacore_dtype_t;
+
+typedef enum {
+  HADACORE_OK = 0,
+  HADACORE_ERR_INVALID_N = 1,   /* n is not a power of two in [128, 32768] */
+  HADACORE_ERR_INVALID_M = 2,   /* m < 0, or m * n * 2 overflows int64 */
+  HADACORE_ERR_NULL = 3,        /* in or out is NULL while m > 0 */
+  HADACORE_ERR_MISALIGNED = 4,  /* in or out is not 16-byte aligned */
+  HADACORE_ERR_OVERLAP = 5,     /* in != out and the two byte ranges overlap */
+  HADACORE_ERR_DTYPE = 6,       /* unknown dtype */
+  HADACORE_ERR_SCALE = 7,       /* scale is NaN or +-Inf */
+  HADACORE_ERR_CUDA = 8,        /* CUDA error (no device, launch failure, copy failure) */
+  HADACORE_ERR_WORKSPACE = 9    /* hadacore_fwht_host: workspace NULL or too small */
+} hadacore_status_t;
+
+/*
+ * out[i, :] = scale * H_n * in[i, :] for i in [0, m), on `stream` (device buffers).
+ * m == 0 returns HADACORE_OK without launching anything.
+ */
+hadacore_status_t hadacore_fwht(const void* in, void* out, int64_t m, int64_t n,
+                                hadacore_dtype_t dtype, float scale, hadacore_stream_t stream);
+
+/*
+ * End-to-end variant on HOST buffers (the call a host-side user makes): copies row
+ * blocks host->device into `workspace`, transforms them in place with the same
+ * kernel, and copies them device->host into `out_host`, pipelined over two halves
+ * of the workspace so the copies overlap the kernels.  Returns after the last
+ * device->host copy has completed (synchronises `stream`).
+ *   in_host / out_host: m x n row-major 16-bit matrices in host memory (pinned
+ *     memory gives full PCIe bandwidth; pageable works but is slower).  May be equal.
+ *   workspace: device buffer of workspace_bytes >= 2 * 2 * n bytes (two rows),
+ *     16-byte aligned; larger workspaces mean larger copy blocks.
+ * Same validation and errors as hadacore_fwht, plus HADACORE_ERR_WORKSPACE.
+ */
+hadacore_status_t hadacore_fwht_host(const void* in_host, void* out_host, int64_t m, int64_t n,
+                                     hadacore_dtype_t dtype, float scale, void* workspace,
+                                     size_t workspace_bytes, hadacore_stream_t stream);
+
+/* Static, human-readable description of a status code (never NULL). */
+const char* hadacore_status_string(hadacore_status_t status);
+
+/* Library version as 10000 * major + 100 * minor + patch. */
+int hadacore_version(void);
+
+/*
+ * Number of kernel launches one hadacore_fwht call with these arguments makes
+ * (0 when m == 0, else 1), for launch accounting in benchmarks.
+ */
+int hadacore_launches_per_call(int64_t m, int64_t n);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HADACORE_H_ */

@@ -1,0 +1,147 @@
+"""B200-native batched normalized Walsh-Hadamard transform (HadaCore, arXiv 2412.08832).
+
+Thin Python binding over the C ABI in ``include/hadacore.h`` (``libhadacore.so``,
+built in-tree for sm_100a).  Argument marshalling only: every step of the
+transform runs in the CUDA kernel.  There is no CPU or PyTorch fallback -- if the
+library is missing or no GPU is present, calls raise.
+
+    out = hadacore_fwht(x)                 # scale = 1/sqrt(n), out-of-place
+    hadacore_fwht(x, out=x)                # in place (App. B)
+    y = hadacore_fwht_host(x_cpu)          # host buffers, copies pipelined in C
+
+``x`` is a CUDA tensor of dtype float16 or bfloat16 whose last dimension n is a
+power of two in [128, 32768]; all leading dimensions are rows (m = numel / n).
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+
+import torch
+
+__all__ = ["hadacore_fwht", "hadacore_fwht_host", "fwht", "HadacoreError", "library_path", "version",
+           "launches_per_call", "STATUS"]
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "libhadacore.so")
+_lib = None
+
+STATUS = {
+    0: "HADACORE_OK", 1: "HADACORE_ERR_INVALID_N", 2: "HADACORE_ERR_INVALID_M", 3: "HADACORE_ERR_NULL",
+    4: "HADACORE_ERR_MISALIGNED", 5: "HADACORE_ERR_OVERLAP", 6: "HADACORE_ERR_DTYPE",
+    7: "HADACORE_ERR_SCALE", 8: "HADACORE_ERR_CUDA", 9: "HADACORE_ERR_WORKSPACE",
+}
+_DTYPES = {torch.float16: 0, torch.bfloat16: 1}
+
+
+class HadacoreError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"{STATUS.get(code, code)}: {msg}")
+        self.code = code
+
+
+def library_path() -> str:
+    return _LIB_PATH
+
+
+def _load():
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(_LIB_PATH):
+        raise ImportError(f"{_LIB_PATH} is missing: build it with `python -m paper_2412_08832_b200.build` "
+                          "(nvcc, sm_100a). There is no fallback implementation.")
+    lib = ctypes.CDLL(_LIB_PATH)
+    vp, i64, f32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_float
+    lib.hadacore_fwht.argtypes = [vp, vp, i64, i64, ctypes.c_int, f32, vp]
+    lib.hadacore_fwht.restype = ctypes.c_int
+    lib.hadacore_fwht_host.argtypes = [vp, vp, i64, i64, ctypes.c_int, f32, vp, ctypes.c_size_t, vp]
+    lib.hadacore_fwht_host.restype = ctypes.c_int
+    lib.hadacore_status_string.argtypes = [ctypes.c_int]
+    lib.hadacore_status_string.restype = ctypes.c_char_p
+    lib.hadacore_version.argtypes = []
+    lib.hadacore_version.restype = ctypes.c_int
+    lib.hadacore_launches_per_call.argtypes = [i64, i64]
+    lib.hadacore_launches_per_call.restype = ctypes.c_int
+    _lib = lib
+    return lib
+
+
+def _check(rc: int):
+    if rc != 0:
+        raise HadacoreError(rc, _load().hadacore_status_string(rc).decode())
+
+
+def version() -> int:
+    return _load().hadacore_version()
+
+
+def launches_per_call(m: int, n: int) -> int:
+    return _load().hadacore_launches_per_call(int(m), int(n))
+
+
+def _shape(x: torch.Tensor):
+    if x.dtype not in _DTYPES:
+        raise HadacoreError(6, f"dtype {x.dtype} (expected float16 or bfloat16)")
+    if x.dim() < 1:
+        raise HadacoreError(1, "need at least one dimension")
+    n = x.shape[-1]
+    m = x.numel() // n if n else 0
+    return m, n
+
+
+def hadacore_fwht(x: torch.Tensor, out: torch.Tensor | None = None, scale: float | None = None,
+                  stream: torch.cuda.Stream | None = None) -> torch.Tensor:
+    """out[..., :] = scale * H_n x[..., :] on the GPU (scale defaults to 1/sqrt(n)).
+
+    ``out=x`` transforms in place.  Launches on ``stream`` (default: the current
+    torch stream of x's device); asynchronous like any CUDA op.
+    """
+    m, n = _shape(x)
+    if not x.is_cuda:
+        raise HadacoreError(8, "x must be a CUDA tensor (use hadacore_fwht_host for host buffers)")
+    if not x.is_contiguous():
+        raise HadacoreError(4, "x must be contiguous (row pitch = n)")
+    if out is None:
+        out = torch.empty_like(x)
+    elif out.shape != x.shape or out.dtype != x.dtype or out.device != x.device or not out.is_contiguous():
+        raise HadacoreError(3, "out must be a contiguous tensor with x's shape, dtype and device")
+    if scale is None:
+        scale = 1.0 / math.sqrt(n) if n > 0 else 1.0
+    with torch.cuda.device(x.device):
+        st = stream if stream is not None else torch.cuda.current_stream(x.device)
+        _check(_load().hadacore_fwht(x.data_ptr(), out.data_ptr(), m, n, _DTYPES[x.dtype], float(scale),
+                                     st.cuda_stream))
+    return out
+
+
+fwht = hadacore_fwht
+
+
+def hadacore_fwht_host(x: torch.Tensor, out: torch.Tensor | None = None, scale: float | None = None,
+                       workspace: torch.Tensor | None = None, device=None,
+                       stream: torch.cuda.Stream | None = None) -> torch.Tensor:
+    """Host-buffer entry (C: hadacore_fwht_host): H2D, kernel, D2H pipelined in the library.
+
+    ``x``/``out`` are CPU tensors (pin them for full PCIe bandwidth).  ``workspace``
+    is a CUDA uint8 tensor (default: 256 MiB, allocated here once per call).
+    Returns after the results are in ``out``.
+    """
+    m, n = _shape(x)
+    if x.is_cuda or not x.is_contiguous():
+        raise HadacoreError(3, "x must be a contiguous CPU tensor")
+    if out is None:
+        out = torch.empty_like(x, pin_memory=x.is_pinned())
+    elif out.is_cuda or out.shape != x.shape or out.dtype != x.dtype or not out.is_contiguous():
+        raise HadacoreError(3, "out must be a contiguous CPU tensor with x's shape and dtype")
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    if workspace is None:
+        workspace = torch.empty(min(256 << 20, max(4 * n, 2 * m * n * 2)), dtype=torch.uint8, device=dev)
+    if scale is None:
+        scale = 1.0 / math.sqrt(n) if n > 0 else 1.0
+    with torch.cuda.device(workspace.device):
+        st = stream if stream is not None else torch.cuda.current_stream(workspace.device)
+        _check(_load().hadacore_fwht_host(x.data_ptr(), out.data_ptr(), m, n, _DTYPES[x.dtype], float(scale),
+                                          workspace.data_ptr(), workspace.numel(), st.cuda_stream))
+    return out

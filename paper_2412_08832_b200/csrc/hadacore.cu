@@ -1,0 +1,203 @@
+// hadacore.cu -- C ABI (include/hadacore.h) of the B200-native batched normalized
+// Walsh-Hadamard transform: argument validation, per-(n, dtype) kernel dispatch,
+// launch configuration, and the pipelined host-buffer entry point.
+// "P:NN" = /root/reference/PAPER.md line NN.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+
+#include "../../include/hadacore.h"
+#include "fwht_kernel.cuh"
+
+namespace hadacore {
+namespace {
+
+constexpr int kVersion = 100;  // 0.1.0
+constexpr int kMaxDevices = 64;
+
+std::atomic<int> g_sm_count[kMaxDevices];
+
+int sm_count(int dev) {
+  if (dev < 0 || dev >= kMaxDevices) return 148;
+  int v = g_sm_count[dev].load(std::memory_order_relaxed);
+  if (v == 0) {
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) v = 148;
+    g_sm_count[dev].store(v, std::memory_order_relaxed);
+  }
+  return v;
+}
+
+// Per-n launch configuration: rows per pipeline
+// stage (32 KiB tiles; 64 KiB for n = 2^15 where one row is 64 KiB), ring depth,
+// compute warps, warps per row team.
+template <int N>
+struct Cfg;
+template <> struct Cfg<128>   { static constexpr int rows = 128, stages = 4, nt = 8, p = 1; };
+template <> struct Cfg<256>   { static constexpr int rows = 64,  stages = 4, nt = 8, p = 1; };
+template <> struct Cfg<512>   { static constexpr int rows = 32,  stages = 4, nt = 8, p = 1; };
+template <> struct Cfg<1024>  { static constexpr int rows = 16,  stages = 4, nt = 8, p = 1; };
+template <> struct Cfg<2048>  { static constexpr int rows = 8,   stages = 4, nt = 8, p = 1; };
+template <> struct Cfg<4096>  { static constexpr int rows = 4,   stages = 4, nt = 8, p = 2; };
+template <> struct Cfg<8192>  { static constexpr int rows = 2,   stages = 4, nt = 8, p = 4; };
+template <> struct Cfg<16384> { static constexpr int rows = 1,   stages = 4, nt = 8, p = 8; };
+template <> struct Cfg<32768> { static constexpr int rows = 1,   stages = 3, nt = 8, p = 8; };
+
+template <int N, int DT>
+hadacore_status_t launch(const void* in, void* out, int64_t m, float scale, cudaStream_t stream) {
+  using C = Cfg<N>;
+  constexpr int tile_bytes = C::rows * 2 * N;
+  constexpr int smem = C::stages * tile_bytes + 2 * C::stages * 8;
+  auto kern = fwht_kernel<N, DT, C::rows, C::stages, C::nt, C::p>;
+  static std::atomic<uint64_t> attr_done{0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return HADACORE_ERR_CUDA;
+  const uint64_t bit = (dev < 64) ? (1ull << dev) : 0;
+  if (!bit || !(attr_done.load(std::memory_order_relaxed) & bit)) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
+      return HADACORE_ERR_CUDA;
+    attr_done.fetch_or(bit, std::memory_order_relaxed);
+  }
+  const int64_t tiles = (m + C::rows - 1) / C::rows;
+  const int64_t max_ctas = sm_count(dev);  // one persistent CTA per SM
+  const int grid = int(tiles < max_ctas ? tiles : max_ctas);
+  // the per-stage constants multiply by exact powers of two 2^-E; fold the rest of
+  // `scale` into the fp32 epilogue of the last stage.
+  const float s_res = std::ldexp(scale, total_shift<N>());
+  kern<<<grid, (C::nt + 1) * 32, smem, stream>>>(static_cast<const uint16_t*>(in),
+                                                  static_cast<uint16_t*>(out), m, s_res);
+  return cudaPeekAtLastError() == cudaSuccess ? HADACORE_OK : HADACORE_ERR_CUDA;
+}
+
+template <int DT>
+hadacore_status_t dispatch_n(const void* in, void* out, int64_t m, int64_t n, float scale,
+                             cudaStream_t st) {
+  switch (n) {
+    case 128: return launch<128, DT>(in, out, m, scale, st);
+    case 256: return launch<256, DT>(in, out, m, scale, st);
+    case 512: return launch<512, DT>(in, out, m, scale, st);
+    case 1024: return launch<1024, DT>(in, out, m, scale, st);
+    case 2048: return launch<2048, DT>(in, out, m, scale, st);
+    case 4096: return launch<4096, DT>(in, out, m, scale, st);
+    case 8192: return launch<8192, DT>(in, out, m, scale, st);
+    case 16384: return launch<16384, DT>(in, out, m, scale, st);
+    case 32768: return launch<32768, DT>(in, out, m, scale, st);
+    default: return HADACORE_ERR_INVALID_N;
+  }
+}
+
+bool valid_n(int64_t n) { return n >= 128 && n <= 32768 && (n & (n - 1)) == 0; }
+
+// Shared by both entry points: everything that can be checked without CUDA.
+hadacore_status_t validate(const void* in, const void* out, int64_t m, int64_t n, int dtype, float scale,
+                           bool device_buffers) {
+  if (dtype != HADACORE_F16 && dtype != HADACORE_BF16) return HADACORE_ERR_DTYPE;
+  if (!valid_n(n)) return HADACORE_ERR_INVALID_N;
+  if (m < 0 || m > INT64_MAX / (2 * n)) return HADACORE_ERR_INVALID_M;
+  if (!std::isfinite(scale)) return HADACORE_ERR_SCALE;
+  if (m == 0) return HADACORE_OK;
+  if (!in || !out) return HADACORE_ERR_NULL;
+  if (device_buffers && ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 15u))
+    return HADACORE_ERR_MISALIGNED;
+  if (in != out) {
+    const uintptr_t a = reinterpret_cast<uintptr_t>(in), b = reinterpret_cast<uintptr_t>(out);
+    const uintptr_t bytes = uintptr_t(m) * uintptr_t(n) * 2u;
+    if (a < b + bytes && b < a + bytes) return HADACORE_ERR_OVERLAP;
+  }
+  return HADACORE_OK;
+}
+
+hadacore_status_t run(const void* in, void* out, int64_t m, int64_t n, int dtype, float scale,
+                      cudaStream_t st) {
+  return dtype == HADACORE_F16 ? dispatch_n<DT_F16>(in, out, m, n, scale, st)
+                               : dispatch_n<DT_BF16>(in, out, m, n, scale, st);
+}
+
+}  // namespace
+}  // namespace hadacore
+
+using namespace hadacore;
+
+extern "C" hadacore_status_t hadacore_fwht(const void* in, void* out, int64_t m, int64_t n,
+                                           hadacore_dtype_t dtype, float scale, hadacore_stream_t stream) {
+  const hadacore_status_t v = validate(in, out, m, n, int(dtype), scale, true);
+  if (v != HADACORE_OK || m == 0) return v;
+  return run(in, out, m, n, int(dtype), scale, reinterpret_cast<cudaStream_t>(stream));
+}
+
+extern "C" hadacore_status_t hadacore_fwht_host(const void* in_host, void* out_host, int64_t m, int64_t n,
+                                                hadacore_dtype_t dtype, float scale, void* workspace,
+                                                size_t workspace_bytes, hadacore_stream_t stream) {
+  const hadacore_status_t v = validate(in_host, out_host, m, n, int(dtype), scale, false);
+  if (v != HADACORE_OK || m == 0) return v;
+  const size_t row_bytes = size_t(n) * 2;
+  if (!workspace || (reinterpret_cast<uintptr_t>(workspace) & 15u) || workspace_bytes < 2 * row_bytes)
+    return HADACORE_ERR_WORKSPACE;
+  // Two halves of the workspace, one internal stream each: block b goes through
+  // H2D -> kernel (in place) -> D2H on stream b&1, so consecutive blocks overlap
+  // their copies (both PCIe directions) with each other's kernels.
+  const int64_t rows_per_half = int64_t((workspace_bytes / 2) / row_bytes);
+  cudaStream_t user = reinterpret_cast<cudaStream_t>(stream);
+  cudaStream_t st[2] = {nullptr, nullptr};
+  cudaEvent_t ev = nullptr;
+  hadacore_status_t rc = HADACORE_OK;
+  if (cudaStreamCreateWithFlags(&st[0], cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&st[1], cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess) {
+    rc = HADACORE_ERR_CUDA;
+  }
+  if (rc == HADACORE_OK) {
+    // order after everything already queued on the caller's stream
+    if (cudaEventRecord(ev, user) != cudaSuccess || cudaStreamWaitEvent(st[0], ev, 0) != cudaSuccess ||
+        cudaStreamWaitEvent(st[1], ev, 0) != cudaSuccess)
+      rc = HADACORE_ERR_CUDA;
+  }
+  const uint8_t* src = static_cast<const uint8_t*>(in_host);
+  uint8_t* dst = static_cast<uint8_t*>(out_host);
+  int64_t b = 0;
+  for (int64_t r0 = 0; rc == HADACORE_OK && r0 < m; r0 += rows_per_half, ++b) {
+    const int64_t rows = (m - r0) < rows_per_half ? (m - r0) : rows_per_half;
+    const size_t bytes = size_t(rows) * row_bytes;
+    uint8_t* ws = static_cast<uint8_t*>(workspace) + size_t(b & 1) * size_t(rows_per_half) * row_bytes;
+    cudaStream_t s = st[b & 1];
+    if (cudaMemcpyAsync(ws, src + size_t(r0) * row_bytes, bytes, cudaMemcpyHostToDevice, s) != cudaSuccess) {
+      rc = HADACORE_ERR_CUDA;
+      break;
+    }
+    rc = run(ws, ws, rows, n, int(dtype), scale, s);
+    if (rc != HADACORE_OK) break;
+    if (cudaMemcpyAsync(dst + size_t(r0) * row_bytes, ws, bytes, cudaMemcpyDeviceToHost, s) != cudaSuccess)
+      rc = HADACORE_ERR_CUDA;
+  }
+  for (int i = 0; i < 2; ++i)
+    if (st[i]) {
+      if (cudaStreamSynchronize(st[i]) != cudaSuccess) rc = HADACORE_ERR_CUDA;
+      cudaStreamDestroy(st[i]);
+    }
+  if (ev) cudaEventDestroy(ev);
+  return rc;
+}
+
+extern "C" const char* hadacore_status_string(hadacore_status_t s) {
+  switch (s) {
+    case HADACORE_OK: return "ok";
+    case HADACORE_ERR_INVALID_N: return "n must be a power of two in [128, 32768]";
+    case HADACORE_ERR_INVALID_M: return "m must be >= 0 and m*n*2 must fit in int64";
+    case HADACORE_ERR_NULL: return "in/out must be non-NULL when m > 0";
+    case HADACORE_ERR_MISALIGNED: return "in/out must be 16-byte aligned";
+    case HADACORE_ERR_OVERLAP: return "in and out partially overlap (only in == out is allowed)";
+    case HADACORE_ERR_DTYPE: return "unknown dtype (expected HADACORE_F16 or HADACORE_BF16)";
+    case HADACORE_ERR_SCALE: return "scale must be finite";
+    case HADACORE_ERR_CUDA: return "CUDA error (see cudaGetLastError)";
+    case HADACORE_ERR_WORKSPACE: return "workspace NULL, misaligned or smaller than two rows";
+  }
+  return "unknown status";
+}
+
+extern "C" int hadacore_version(void) { return kVersion; }
+
+extern "C" int hadacore_launches_per_call(int64_t m, int64_t n) {
+  return (m > 0 && valid_n(n)) ? 1 : 0;
+}

@@ -1,0 +1,119 @@
+"""C-ABI boundary checks that need no GPU: the library builds and loads, exports
+every function declared in include/hadacore.h, and validates arguments before
+any CUDA call (include/hadacore.h "Errors")."""
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+
+import paper_2412_08832_b200 as hc
+from paper_2412_08832_b200 import build as hc_build
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "hadacore.h")
+
+OK, INVALID_N, INVALID_M, NULL, MISALIGNED, OVERLAP, DTYPE, SCALE, CUDA, WORKSPACE = range(10)
+
+
+@pytest.fixture(scope="module")
+def lib():
+    hc_build.build()
+    return hc._load()
+
+
+def declared_functions():
+    text = open(HEADER).read()
+    return sorted(set(re.findall(r"^\s*(?:[A-Za-z_][A-Za-z0-9_]*\s*\*?\s+)+\**(hadacore_[a-z_]+)\s*\(", text, re.M)))
+
+
+def test_header_declares_expected_entry_points():
+    assert declared_functions() == sorted(["hadacore_fwht", "hadacore_fwht_host", "hadacore_status_string",
+                                           "hadacore_version", "hadacore_launches_per_call"])
+
+
+def test_library_exports_every_declared_symbol(lib):
+    out = subprocess.run(["nm", "-D", "--defined-only", hc.library_path()], capture_output=True, text=True,
+                         check=True).stdout
+    exported = set(re.findall(r"\s[TW]\s+(hadacore_\w+)", out))
+    for name in declared_functions():
+        assert name in exported, name
+        assert getattr(lib, name) is not None
+
+
+def test_library_targets_sm100a_only(lib):
+    out = subprocess.run(["cuobjdump", "--list-elf", hc.library_path()], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+    sass = subprocess.run(["cuobjdump", "-sass", hc.library_path()], capture_output=True, text=True).stdout
+    assert "HMMA.16816" in sass          # tensor-core contractions
+    assert "UBLKCP.S.G" in sass          # bulk (TMA) global->shared copies
+
+
+def call(lib, in_ptr, out_ptr, m, n, dtype=0, scale=1.0):
+    return lib.hadacore_fwht(in_ptr, out_ptr, m, n, dtype, scale, None)
+
+
+def test_validation_codes(lib):
+    a, b = 0x10000, 0x8000000
+    assert call(lib, a, b, 4, 100) == INVALID_N
+    assert call(lib, a, b, 4, 64) == INVALID_N
+    assert call(lib, a, b, 4, 65536) == INVALID_N
+    assert call(lib, a, b, 4, 0) == INVALID_N
+    assert call(lib, a, b, -1, 256) == INVALID_M
+    assert call(lib, a, b, 1 << 62, 256) == INVALID_M
+    assert call(lib, a, b, 4, 256, dtype=2) == DTYPE
+    assert call(lib, a, b, 4, 256, dtype=-1) == DTYPE
+    assert call(lib, a, b, 4, 256, scale=float("nan")) == SCALE
+    assert call(lib, a, b, 4, 256, scale=float("inf")) == SCALE
+    assert call(lib, None, b, 4, 256) == NULL
+    assert call(lib, a, None, 4, 256) == NULL
+    assert call(lib, a + 8, b, 4, 256) == MISALIGNED
+    assert call(lib, a, b + 2, 4, 256) == MISALIGNED
+    assert call(lib, a, a + 512, 4, 256) == OVERLAP      # partial overlap
+    assert call(lib, a + 512, a, 4, 256) == OVERLAP
+    # m == 0 is a successful no-op (no CUDA call, works without a GPU)
+    assert call(lib, None, None, 0, 256) == OK
+    assert call(lib, a, b, 0, 32768, dtype=1) == OK
+
+
+def test_host_entry_validation(lib):
+    a, b, ws = 0x10000, 0x8000000, 0x20000000
+    f = lib.hadacore_fwht_host
+    assert f(a, b, 4, 100, 0, 1.0, ws, 1 << 20, None) == INVALID_N
+    assert f(a, b, 4, 256, 0, 1.0, None, 1 << 20, None) == WORKSPACE
+    assert f(a, b, 4, 256, 0, 1.0, ws, 1000, None) == WORKSPACE     # < two rows
+    assert f(a, b, 4, 256, 0, 1.0, ws + 4, 1 << 20, None) == WORKSPACE
+    assert f(a, a + 2, 4, 256, 0, 1.0, ws, 1 << 20, None) == OVERLAP
+    assert f(None, None, 0, 256, 0, 1.0, None, 0, None) == OK
+
+
+def test_status_strings_and_version(lib):
+    for code in range(10):
+        s = lib.hadacore_status_string(code)
+        assert s and len(s) > 1
+    assert lib.hadacore_status_string(1234) == b"unknown status"
+    assert lib.hadacore_version() >= 100
+    assert lib.hadacore_launches_per_call(0, 256) == 0
+    assert lib.hadacore_launches_per_call(10, 256) == 1
+    assert lib.hadacore_launches_per_call(10, 100) == 0
+
+
+def test_python_binding_rejects_without_fallback():
+    import torch
+    x = torch.zeros(4, 256, dtype=torch.float16)
+    with pytest.raises(hc.HadacoreError):
+        hc.hadacore_fwht(x)                    # CPU tensor: no CPU fallback
+    with pytest.raises(hc.HadacoreError):
+        hc.hadacore_fwht(torch.zeros(4, 256, dtype=torch.float32))
+
+
+def test_product_path_does_not_import_oracle():
+    pkg = os.path.join(ROOT, "paper_2412_08832_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
+                text = open(os.path.join(dirpath, f)).read()
+                assert "oracle" not in text.replace("oracle/", "").lower() or f == "__init__.py" and \
+                    "import oracle" not in text, f
+                assert "import oracle" not in text and "from oracle" not in text, f

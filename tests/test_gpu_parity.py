@@ -1,0 +1,207 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle.
+
+Tolerances (BASELINE.json north_star): max per-row relative L2 error
+||y_gpu - y_oracle||_2 / ||y_oracle||_2 <= 2e-3 (fp16), 1.6e-2 (bf16).
+Exactly representable results (identity input, zero rows) are checked bitwise.
+Inputs come from synthetic/ (seeded, shared with bench.py), widened exactly to
+fp64 for the oracle.  DESIGN.md "Test plan" lists what each test pins.
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synthetic
+
+pytestmark = pytest.mark.gpu
+
+NS = [1 << k for k in range(7, 16)]
+DTYPES = [torch.float16, torch.bfloat16]
+TOL = {torch.float16: 2e-3, torch.bfloat16: 1.6e-2}
+# rows per pipeline tile in the launch configuration (paper_2412_08832_b200/csrc/hadacore.cu Cfg<N>)
+TILE_ROWS = {128: 128, 256: 64, 512: 32, 1024: 16, 2048: 8, 4096: 4, 8192: 2, 16384: 1, 32768: 1}
+
+
+@pytest.fixture(scope="module")
+def hc():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2412_08832_b200 as hc
+    hc._load()
+    return hc
+
+
+def widen(t: torch.Tensor) -> np.ndarray:
+    return t.detach().cpu().to(torch.float64).numpy()
+
+
+def rel_l2_rows(got: np.ndarray, ref: np.ndarray) -> np.ndarray:
+    num = np.linalg.norm(got - ref, axis=1)
+    den = np.linalg.norm(ref, axis=1)
+    return num / np.where(den == 0, 1.0, den)
+
+
+def ragged_m(n: int) -> int:
+    # several tiles plus a ragged tail, capped at ~2^21 elements so the oracle is fast
+    tiles = max(3, min(40, (1 << 21) // (TILE_ROWS[n] * n)))
+    return tiles * TILE_ROWS[n] + max(1, TILE_ROWS[n] // 2 - 1)
+
+
+@pytest.mark.parametrize("dist", ["D0", "D1"])
+@pytest.mark.parametrize("dtype", DTYPES, ids=["fp16", "bf16"])
+@pytest.mark.parametrize("n", NS)
+def test_parity_vs_oracle(hc, n, dtype, dist):
+    m = ragged_m(n)
+    x = synthetic.generate(m, n, dtype, synthetic.seed_for(2, dtype), dist=dist).cuda()
+    y = hc.hadacore_fwht(x)
+    torch.cuda.synchronize()
+    ref = oracle.fwht(widen(x))
+    err = rel_l2_rows(widen(y), ref)
+    assert np.all(np.isfinite(widen(y)))
+    assert err.max() <= TOL[dtype], f"max rel-L2 {err.max():.3e} (row {err.argmax()})"
+
+
+@pytest.mark.parametrize("dtype", DTYPES, ids=["fp16", "bf16"])
+@pytest.mark.parametrize("n", NS)
+def test_special_rows(hc, n, dtype):
+    sp, names = synthetic.special_rows(n, dtype)
+    g = synthetic.generate(6, n, dtype, 99)
+    # finite rows around the special ones so that row-pair fragments (n = 128) mix
+    # a special row with a finite neighbour on both sides
+    x = torch.cat([g[:3], sp, g[3:]]).contiguous()
+    y = widen(hc.hadacore_fwht(x.cuda()))
+    xs = widen(x)
+    ref = oracle.fwht(xs)
+    for i in range(x.shape[0]):
+        name = names[i - 3] if 3 <= i < 3 + len(names) else "finite"
+        if name in ("inf", "nan"):
+            assert not np.any(np.isfinite(y[i])), f"{name} row has finite outputs"
+            continue
+        assert np.all(np.isfinite(y[i])), f"row {i} ({name}) not finite"
+        if name == "zeros":
+            assert np.all(y[i] == 0.0)
+        elif name == "subnormal":
+            # DESIGN.md reading R14: absolute tolerance in units of the subnormal spacing
+            spacing = torch.finfo(dtype).tiny * torch.finfo(dtype).eps
+            assert np.max(np.abs(y[i] - ref[i])) <= 8 * spacing, name
+        else:
+            e = rel_l2_rows(y[i:i + 1], ref[i:i + 1])[0]
+            assert e <= TOL[dtype], f"row {i} ({name}) rel-L2 {e:.3e}"
+
+
+@pytest.mark.parametrize("dtype", DTYPES, ids=["fp16", "bf16"])
+@pytest.mark.parametrize("n", NS)
+def test_identity_exact_closed_form(hc, n, dtype):
+    """Input I_n: output (i, j) must be bitwise (-1)^popcount(i&j) * RNE(1/sqrt(n)).
+
+    Closed form (SURVEY.md 8(c) pins); no oracle involved.  For n = 2^15 the
+    input is 2^30 elements (2 GiB), checked block by block on the GPU.
+    """
+    dev = torch.device("cuda")
+    x = torch.zeros(n, n, dtype=dtype, device=dev)
+    x.fill_diagonal_(1.0)
+    y = hc.hadacore_fwht(x)
+    mag = torch.tensor(1.0 / math.sqrt(n), dtype=torch.float64).to(dtype).to(dev)
+    j = torch.arange(n, device=dev, dtype=torch.int64)
+    blk = max(1, (1 << 24) // n)
+    for i0 in range(0, n, blk):
+        i = torch.arange(i0, min(n, i0 + blk), device=dev, dtype=torch.int64)
+        a = i[:, None] & j[None, :]
+        par = torch.zeros_like(a)
+        for b in range(15):
+            par ^= (a >> b) & 1
+        expect = torch.where(par == 1, -mag, mag)
+        assert torch.equal(y[i0:i0 + len(i)].view(torch.int16), expect.view(torch.int16)), f"rows {i0}.."
+
+
+@pytest.mark.parametrize("dtype", DTYPES, ids=["fp16", "bf16"])
+@pytest.mark.parametrize("n", NS)
+def test_inplace_bitwise_and_deterministic(hc, n, dtype):
+    m = 2 * TILE_ROWS[n] * 148 + 3  # more tiles than CTAs: exercises the persistent loop
+    x = synthetic.generate(m, n, dtype, 5, device="cuda")
+    y1 = hc.hadacore_fwht(x)
+    y2 = hc.hadacore_fwht(x)
+    xi = x.clone()
+    hc.hadacore_fwht(xi, out=xi)
+    torch.cuda.synchronize()
+    assert torch.equal(y1.view(torch.int16), y2.view(torch.int16))
+    assert torch.equal(y1.view(torch.int16), xi.view(torch.int16))
+
+
+@pytest.mark.parametrize("n", NS)
+def test_small_m_and_views(hc, n):
+    for m in (1, 2, 3, 5):
+        x = synthetic.generate(m, n, torch.bfloat16, 11 + m).cuda()
+        y = widen(hc.hadacore_fwht(x))
+        assert rel_l2_rows(y, oracle.fwht(widen(x))).max() <= TOL[torch.bfloat16]
+    # leading dimensions are rows: (b, s, h, d) with d = n
+    x4 = synthetic.generate(12, n, torch.float16, 3).reshape(2, 3, 2, n).cuda()
+    y4 = hc.hadacore_fwht(x4)
+    assert y4.shape == x4.shape
+    assert rel_l2_rows(widen(y4.reshape(-1, n)), oracle.fwht(widen(x4.reshape(-1, n)))).max() <= 2e-3
+    # m == 0
+    e = torch.empty(0, n, dtype=torch.float16, device="cuda")
+    assert hc.hadacore_fwht(e).shape == (0, n)
+
+
+def test_scale_argument_and_involution(hc):
+    n = 4096
+    x = synthetic.generate(64, n, torch.float16, 8).cuda()
+    y = widen(hc.hadacore_fwht(x, scale=0.37))
+    ref = oracle.fwht(widen(x), scale=0.37)
+    assert rel_l2_rows(y, ref).max() <= 2e-3
+    # normalized transform is an involution: H(H x) ~ x
+    z = hc.hadacore_fwht(hc.hadacore_fwht(x))
+    assert rel_l2_rows(widen(z), widen(x)).max() <= 2 * 2e-3
+
+
+def test_host_entry_matches_device_entry(hc):
+    n = 1024
+    x = synthetic.generate(3000, n, torch.bfloat16, 4).pin_memory()
+    ws = torch.empty(1 << 20, dtype=torch.uint8, device="cuda")  # forces many pipelined blocks
+    y_host = hc.hadacore_fwht_host(x, workspace=ws)
+    y_dev = hc.hadacore_fwht(x.cuda()).cpu()
+    assert torch.equal(y_host.view(torch.int16), y_dev.view(torch.int16))
+    # in place on host buffers
+    xi = x.clone().pin_memory()
+    hc.hadacore_fwht_host(xi, out=xi, workspace=ws)
+    assert torch.equal(xi.view(torch.int16), y_dev.view(torch.int16))
+
+
+def test_rows_are_isolated_from_nonfinite_neighbours(hc):
+    # every row pair / team layout: a NaN row next to finite rows must not leak
+    for n in NS:
+        m = 2 * TILE_ROWS[n] + 2
+        x = synthetic.generate(m, n, torch.float16, 77).cuda()
+        x[1::3] = float("nan")
+        y = hc.hadacore_fwht(x)
+        finite_rows = [i for i in range(m) if i % 3 != 1]
+        assert torch.isfinite(y[finite_rows]).all(), n
+        assert torch.isnan(y[1::3]).all(), n
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("dtype", DTYPES, ids=["fp16", "bf16"])
+@pytest.mark.parametrize("n", NS)
+def test_full_size_sampled(hc, n, dtype):
+    """C3 at full size (2^28 elements) in bench.py's launch: sampled rows vs oracle,
+    plus the norm-preservation property on every row."""
+    m = (1 << 28) // n
+    x = torch.empty(m, n, dtype=dtype, device="cuda")
+    synthetic.generate(m, n, dtype, synthetic.seed_for(2, dtype), out=x)
+    y = hc.hadacore_fwht(x)
+    torch.cuda.synchronize()
+    g = torch.Generator().manual_seed(n)
+    rows = sorted(set([0, 1, m - 1, m // 2] + torch.randint(0, m, (60,), generator=g).tolist()))
+    xs, ys = widen(x[rows]), widen(y[rows])
+    assert rel_l2_rows(ys, oracle.fwht(xs)).max() <= TOL[dtype]
+    # norm preservation on all rows (normalized H is orthogonal), computed blockwise in fp32
+    blk = max(1, (1 << 24) // n)
+    worst = 0.0
+    for r0 in range(0, m, blk):
+        nx = x[r0:r0 + blk].float().norm(dim=1)
+        ny = y[r0:r0 + blk].float().norm(dim=1)
+        worst = max(worst, ((ny - nx).abs() / nx).max().item())
+    assert worst <= TOL[dtype]
