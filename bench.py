@@ -1,0 +1,381 @@
+#!/usr/bin/env python
+"""Benchmark of the B200-native batched normalized FWHT (HadaCore hot path).
+
+Metric (BASELINE.json): FWHT HBM GB/s vs n = 2^7..2^15 (bf16/fp16) at 1/2/4/8
+B200; % of 8 TB/s.  One STEP = the paper's size sweep (config C3): for each
+dtype in {fp16, bf16} and each n in 2^7..2^15, one hadacore_fwht call over a
+resident 2^28-element matrix (512 MiB in, 512 MiB out, out-of-place) -- 18
+kernel launches.  value = algorithmic bytes (read + write, 4 B/element) of all
+ranks / max-over-ranks device time, in GB/s.  Inputs (512 MiB per launch) are
+larger than the 126 MB L2, so no flush is needed between launches.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl {hadacore,reference}]
+    torchrun --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N ...
+
+Rank 0 prints ONE JSON line.  --impl reference times the fp64 CPU oracle (the
+only reference that exists for this paper) on a bounded sample of the same
+workload on the host cores (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "FWHT HBM GB/s vs n=2^7..2^15 (bf16/fp16) at 1/2/4/8 B200; % of 8 TB/s"
+NS = [1 << k for k in range(7, 16)]
+ELEMS = 1 << 28
+NOMINAL_HBM_GBS = 8000.0
+FALLBACK_HBM_GBS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=int(os.environ.get("WORLD_SIZE", "1")))
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["hadacore", "reference"], default="hadacore")
+    ap.add_argument("--elems", type=int, default=ELEMS, help="elements per (n, dtype) launch per GPU")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    return ap.parse_args()
+
+
+def measured_hbm_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        return float(json.load(open(p))["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic():
+    """Per-launch DRAM bytes from the committed ncu --set full capture, if present."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        return json.load(open(p))
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons, sampled while the timed region runs."""
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+        self.t0 = self.t1 = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                                          "-lms", "20", "-i", str(self.index)], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+            self.reader = threading.Thread(target=self._read, daemon=True)
+            self.reader.start()
+            time.sleep(0.3)
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append((time.time(), line.strip()))
+
+    def mark_start(self):
+        self.t0 = time.time()
+
+    def mark_end(self):
+        self.t1 = time.time()
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.05)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        inside = [r for t, r in self.rows if self.t0 is not None and self.t0 <= t <= (self.t1 or t)]
+        use = inside if inside else [r for _, r in self.rows]
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in use:
+            f = [v.strip() for v in r.split(",")]
+            try:
+                sm.append(float(f[0]))
+                smax.append(float(f[1]))
+            except Exception:
+                continue
+            for nm, v in zip(names, f[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(use), "samples_in_timed_region": len(inside)}
+
+
+def dist_setup(args):
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        return rank, world, local, dist
+    torch.cuda.set_device(0)
+    return 0, 1, 0, None
+
+
+def barrier(dist, torch):
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+
+
+def max_over_ranks(v: float, dist, torch):
+    if dist is None:
+        return v
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def run_oracle_sample(inputs, sample_elems, threads):
+    """Time the fp64 oracle on the first rows of each (dtype, n) input: returns
+    (seconds, elements)."""
+    import numpy as np
+    import oracle
+    tot_t, tot_e = 0.0, 0
+    for (dt, n), x in inputs.items():
+        rows = max(1, sample_elems // n)
+        xs = x[:rows]
+        a = xs.cpu().double().numpy() if hasattr(xs, "cpu") else xs
+        a = np.ascontiguousarray(a)
+        t0 = time.perf_counter()
+        oracle.fwht(a, threads=threads)
+        tot_t += time.perf_counter() - t0
+        tot_e += a.size
+    return tot_t, tot_e
+
+
+def reference_arm(args, rank, world):
+    """--impl reference: the fp64 CPU oracle (as it stands) on host cores, rank 0 only."""
+    if rank != 0:
+        return None
+    import torch
+    import oracle
+    import synthetic
+    oracle.build()
+    threads = oracle.default_threads()
+    sample = 1 << 22  # elements per (dtype, n) per step; bounded so K+W steps finish in minutes
+    inputs = {}
+    for dt in (torch.float16, torch.bfloat16):
+        for n in NS:
+            m = sample // n
+            inputs[(str(dt), n)] = synthetic.generate(m, n, dt, synthetic.seed_for(2, dt)).double().numpy()
+    for _ in range(args.warmup):
+        run_oracle_sample(inputs, sample, threads)
+    t_all, e_all = 0.0, 0
+    for _ in range(args.steps):
+        t, e = run_oracle_sample(inputs, sample, threads)
+        t_all += t
+        e_all += e
+    gbs = 4.0 * e_all / t_all / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(gbs, 4), "unit": "GB/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * t_all / args.steps, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64 (oracle)",
+        "data": "synthetic", "config": config_block(args, world),
+        "cpu_baseline": {"value": round(gbs, 4), "unit": "GB/s", "cores": threads, "kind": "oracle",
+                         "sample": f"{sample} elements per (dtype, n) per step = {sample // (1 << 20)}Mi of the "
+                                   f"{args.elems >> 20}Mi-element C3 matrices, 18 (dtype, n) pairs; fp64 "
+                                   "listing (oracle/fwht_oracle.c), widening excluded"},
+        "e2e": {"value": round(gbs, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    return line
+
+
+def config_block(args, world):
+    return {"workload": "C3 size sweep: n=2^7..2^15 x {fp16, bf16}, 2^28 elements per (n, dtype) per GPU, "
+                        "out-of-place, normalized (scale=1/sqrt(n))",
+            "elements_per_launch": args.elems, "ns": NS, "dtypes": ["fp16", "bf16"],
+            "launches_per_step": 2 * len(NS),
+            "l2": "no flush: every launch reads a 512 MiB input and writes a 512 MiB output (> 126 MB L2)",
+            "parallelism": f"row-sharded x{world}, no collective on the hot path" if world > 1 else "single GPU"}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        # CPU oracle on host cores; under torchrun only rank 0 works, the others exit 0
+        rank = int(os.environ.get("RANK", "0"))
+        world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+        line = reference_arm(args, rank, world)
+        if line is not None:
+            print(json.dumps(line), flush=True)
+        return
+    import torch
+    rank, world, local, dist = dist_setup(args)
+
+    import paper_2412_08832_b200 as hc
+    import synthetic
+    hc._load()  # fails loudly without the CUDA library
+    dev = torch.device("cuda", local)
+    m_of = {n: args.elems // n for n in NS}
+    # resident inputs: one 2^28-element matrix per dtype (each (n) is a view), rows
+    # [rank*m, (rank+1)*m) of the global seeded matrix (weak scaling)
+    xin, xout = {}, {}
+    for dt in (torch.float16, torch.bfloat16):
+        buf = torch.empty(args.elems, dtype=dt, device=dev)
+        synthetic.generate(args.elems // 256, 256, dt, synthetic.seed_for(2, dt), row0=rank * (args.elems // 256),
+                           out=buf.view(-1, 256))
+        xin[dt] = buf
+    obuf = torch.empty(args.elems, dtype=torch.float16, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    pairs = [(dt, n) for dt in (torch.float16, torch.bfloat16) for n in NS]
+
+    def launch(dt, n):
+        x = xin[dt].view(-1, n)
+        o = obuf.view(torch.int16).view(dt).view(-1, n)
+        hc.hadacore_fwht(x, out=o, stream=stream)
+
+    # warm-up
+    for _ in range(args.warmup):
+        for dt, n in pairs:
+            launch(dt, n)
+    barrier(dist, torch)
+
+    def timed_region():
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(args.steps * len(pairs))]
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        barrier(dist, torch)
+        g0.record(stream)
+        i = 0
+        for _ in range(args.steps):
+            for dt, n in pairs:
+                evs[i][0].record(stream)
+                launch(dt, n)
+                evs[i][1].record(stream)
+                i += 1
+        g1.record(stream)
+        torch.cuda.synchronize()
+        total_ms = g0.elapsed_time(g1)
+        per = [a.elapsed_time(b) for a, b in evs]
+        barrier(dist, torch)
+        return total_ms, per
+
+    with ClockSampler(torch.cuda.current_device() if world == 1 else local) as cs:
+        cs.mark_start()
+        total_ms, per = timed_region()
+        cs.mark_end()
+    clocks = cs.summary()
+    bad = {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"}
+    remeasured = False
+    if bad & set(clocks.get("reasons", [])):
+        with ClockSampler(local) as cs:
+            cs.mark_start()
+            total_ms, per = timed_region()
+            cs.mark_end()
+        clocks = cs.summary()
+        remeasured = True
+
+    t_max = max_over_ranks(total_ms, dist, torch)
+    bytes_per_launch = 4.0 * args.elems
+    total_bytes = bytes_per_launch * len(pairs) * args.steps * world
+    value = total_bytes / (t_max * 1e-3) / 1e9
+
+    # per-(dtype, n) breakdown and the roofline of the kernel (device time per launch)
+    per_n = {}
+    for k, (dt, n) in enumerate(pairs):
+        ts = sorted(per[k::len(pairs)])
+        med = ts[len(ts) // 2]
+        per_n.setdefault("fp16" if dt == torch.float16 else "bf16", {})[str(n)] = round(
+            bytes_per_launch / (med * 1e-3) / 1e9, 1)
+    avg_launch_ms = sum(per) / len(per)
+    peak, peak_src = measured_hbm_peak()
+    achieved = bytes_per_launch / (avg_launch_ms * 1e-3) / 1e9
+    traffic = ncu_traffic()
+    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "peak_source": peak_src,
+                "frac_of_8TBps": round(achieved / NOMINAL_HBM_GBS, 4),
+                "algorithmic_bytes_per_launch": int(bytes_per_launch),
+                "traffic": (traffic or {}).get("avg_dram_bytes_per_launch"),
+                "traffic_source": (traffic or {}).get("source")}
+
+    # end to end through the public host-buffer C entry (hadacore_fwht_host)
+    e2e = None
+    if not args.no_e2e:
+        hin = {dt: xin[dt].cpu().pin_memory() for dt in xin}
+        hout = torch.empty(args.elems, dtype=torch.float16).pin_memory()
+        ws = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+        for dt, n in pairs[:2]:
+            hc.hadacore_fwht_host(hin[dt].view(-1, n), out=hout.view(torch.int16).view(dt).view(-1, n), workspace=ws)
+        barrier(dist, torch)
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            for dt, n in pairs:
+                hc.hadacore_fwht_host(hin[dt].view(-1, n), out=hout.view(torch.int16).view(dt).view(-1, n),
+                                      workspace=ws)
+        torch.cuda.synchronize()
+        dt_s = time.perf_counter() - t0
+        dt_s = max_over_ranks(dt_s, dist, torch)
+        e2e = {"value": round(bytes_per_launch * len(pairs) * args.e2e_steps * world / dt_s / 1e9, 2), "unit": "GB/s",
+               "h2d_bytes_per_step": int(2 * args.elems * len(pairs)),
+               "d2h_bytes_per_step": int(2 * args.elems * len(pairs)),
+               "api": "hadacore_fwht_host (C ABI, pinned host buffers, copies + kernel pipelined in the library)",
+               "steps": args.e2e_steps}
+        del hin, hout, ws
+
+    cpu_baseline = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        import oracle
+        oracle.build()
+        threads = oracle.default_threads()
+        sample = 1 << 24
+        inputs = {(str(dt), n): xin[dt][: (sample // n) * n].view(-1, n) for dt, n in pairs}
+        t, e = run_oracle_sample(inputs, sample, threads)
+        cpu_baseline = {"value": round(4.0 * e / t / 1e9, 4), "unit": "GB/s", "cores": threads, "kind": "oracle",
+                        "sample": f"first {sample >> 20}Mi elements of each of the 18 (dtype, n) C3 inputs "
+                                  f"({e} elements total), fp64 listing, {t:.2f} s; widening excluded"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 1), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(t_max / args.steps, 4), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "fp16+bf16 (fp32 last-stage accumulate)",
+            "data": "synthetic (counter-based N(0,1), synthetic/)", "config": config_block(args, world),
+            "pct_of_8TBps": round(100.0 * value / world / NOMINAL_HBM_GBS, 2),
+            "per_n_GBps": per_n, "roofline": roofline, "cpu_baseline": cpu_baseline, "e2e": e2e,
+            "gpu_launches": int(args.steps * sum(hc.launches_per_call(m_of[n], n) for _, n in pairs)),
+            "clocks": clocks, "remeasured_for_clocks": remeasured,
+        }
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

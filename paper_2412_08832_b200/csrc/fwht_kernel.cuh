@@ -102,6 +102,9 @@ __device__ __forceinline__ void lds128(const uint8_t* p, uint32_t& a, uint32_t& 
   c = v.z;
   d = v.w;
 }
+__device__ __forceinline__ void stg_sh128(uint8_t* p, const uint32_t v[4]) {
+  *reinterpret_cast<uint4*>(p) = make_uint4(v[0], v[1], v[2], v[3]);
+}
 __device__ __forceinline__ void stg32(uint16_t* p, uint32_t v) { *reinterpret_cast<uint32_t*>(p) = v; }
 __device__ __forceinline__ void stg64(uint16_t* p, uint32_t a, uint32_t b) {
   *reinterpret_cast<uint2*>(p) = make_uint2(a, b);
@@ -181,6 +184,12 @@ __host__ __device__ constexpr int popc4(uint32_t m) {
 // exact per-stage normalization 2^-floor(h/2) (h = number of H_2 factors)
 __host__ __device__ constexpr int stage_shift(uint32_t m) { return popc4(m) / 2; }
 
+__device__ __forceinline__ uint32_t opaque(uint32_t v) {
+  uint32_t r;
+  asm volatile("mov.b32 %0, %1;" : "=r"(r) : "r"(v));
+  return r;
+}
+
 // A-operand (row-major 16x16) registers of 2^-shift * K(hmask) for this lane.
 template <int DT>
 __device__ __forceinline__ void make_const_a(uint32_t hmask, uint32_t a[4]) {
@@ -190,6 +199,8 @@ __device__ __forceinline__ void make_const_a(uint32_t hmask, uint32_t a[4]) {
   a[1] = pack2<DT>(s * kron_entry(hmask, g + 8, 2 * t), s * kron_entry(hmask, g + 8, 2 * t + 1));
   a[2] = pack2<DT>(s * kron_entry(hmask, g, 2 * t + 8), s * kron_entry(hmask, g, 2 * t + 9));
   a[3] = pack2<DT>(s * kron_entry(hmask, g + 8, 2 * t + 8), s * kron_entry(hmask, g + 8, 2 * t + 9));
+#pragma unroll
+  for (int i = 0; i < 4; ++i) a[i] = opaque(a[i]);
 }
 
 // B-operand (16x8, "col") registers of columns [8T, 8T+8) of 2^-shift * K(hmask).
@@ -200,107 +211,54 @@ __device__ __forceinline__ void make_const_b(uint32_t hmask, int T, uint32_t b[2
   const int n = 8 * T + g;
   b[0] = pack2<DT>(s * kron_entry(hmask, 2 * t, n), s * kron_entry(hmask, 2 * t + 1, n));
   b[1] = pack2<DT>(s * kron_entry(hmask, 2 * t + 8, n), s * kron_entry(hmask, 2 * t + 9, n));
+  b[0] = opaque(b[0]);
+  b[1] = opaque(b[1]);
 }
 
 // ------------------------------------------------------------------ stages
-// "const-A" stage: tile T uses B = (x[rT0], x[rT1]); outputs
-//   y0 = D_0 rows 0..7, y1 = D_0 rows 8..15, y2 = D_1 rows 0..7, y3 = D_1 rows 8..15.
+// "const-A" stage (P:101 two m16n8k16 mma per 16x16 fragment): tile T's B operand
+// is (b_T0, b_T1); D = K * B, so the result comes back transposed for free.
+// Outputs y0 = D_0 rows 0..7, y1 = D_0 rows 8..15, y2 = D_1 rows 0..7, y3 = D_1 rows 8..15.
 template <int DT>
 __device__ __forceinline__ void stage_ca(const uint32_t a[4], uint32_t b00, uint32_t b01, uint32_t b10,
                                          uint32_t b11, uint32_t y[4]) {
   mma_pk<DT>(a, b00, b01, y[0], y[1]);
   mma_pk<DT>(a, b10, b11, y[2], y[3]);
 }
-// Same, final stage: fp32 accumulate, * s_res, RNE pack.
+// Same with fp32 results d[0..3] = tile 0 (pairs y0, y1), d[4..7] = tile 1 (y2, y3).
 template <int DT>
-__device__ __forceinline__ void stage_ca_final(const uint32_t a[4], uint32_t b00, uint32_t b01,
-                                               uint32_t b10, uint32_t b11, float s_res, uint32_t y[4]) {
-  float d0[4], d1[4];
-  mma_f32<DT>(a, b00, b01, d0);
-  mma_f32<DT>(a, b10, b11, d1);
-  y[0] = pack2<DT>(d0[0] * s_res, d0[1] * s_res);
-  y[1] = pack2<DT>(d0[2] * s_res, d0[3] * s_res);
-  y[2] = pack2<DT>(d1[0] * s_res, d1[1] * s_res);
-  y[3] = pack2<DT>(d1[2] * s_res, d1[3] * s_res);
+__device__ __forceinline__ void stage_ca_f32(const uint32_t a[4], uint32_t b00, uint32_t b01, uint32_t b10,
+                                             uint32_t b11, float d[8]) {
+  mma_f32<DT>(a, b00, b01, d);
+  mma_f32<DT>(a, b10, b11, d + 4);
 }
-// "data-as-A" final stage: D = X * Bc (X in A layout, 4 regs); output layout == input.
+// "data-as-A" stage: D = X * Bc with X (4 regs) in the A layout; D has X's layout.
 template <int DT>
-__device__ __forceinline__ void stage_da_final(const uint32_t x[4], const uint32_t bc0[2],
-                                               const uint32_t bc1[2], float s_res, uint32_t y[4]) {
-  float d0[4], d1[4];
-  mma_f32<DT>(x, bc0[0], bc0[1], d0);  // output columns 0..7  -> A-layout regs R0 (rows g), R1 (g+8)
-  mma_f32<DT>(x, bc1[0], bc1[1], d1);  // output columns 8..15 -> R2, R3
-  y[0] = pack2<DT>(d0[0] * s_res, d0[1] * s_res);
-  y[1] = pack2<DT>(d0[2] * s_res, d0[3] * s_res);
-  y[2] = pack2<DT>(d1[0] * s_res, d1[1] * s_res);
-  y[3] = pack2<DT>(d1[2] * s_res, d1[3] * s_res);
+__device__ __forceinline__ void stage_da_f32(const uint32_t x[4], const uint32_t bc0[2], const uint32_t bc1[2],
+                                             float d[8]) {
+  mma_f32<DT>(x, bc0[0], bc0[1], d);      // output columns 0..7  -> regs R0 (rows g), R1 (rows g+8)
+  mma_f32<DT>(x, bc1[0], bc1[1], d + 4);  // output columns 8..15 -> R2, R3
+}
+// fp32 epilogue: * s_res (exact normalization remainder), one RNE rounding to 16 bits.
+template <int DT>
+__device__ __forceinline__ void scale_pack(const float d[8], float s_res, uint32_t y[4]) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i) y[i] = pack2<DT>(d[2 * i] * s_res, d[2 * i + 1] * s_res);
+}
+
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t r[4]) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(addr)
+               : "memory");
+}
+__device__ __forceinline__ void stsm_x4_t(uint32_t addr, const uint32_t r[4]) {
+  asm volatile("stmatrix.sync.aligned.m8n8.x4.trans.shared.b16 [%0], {%1,%2,%3,%4};" ::"r"(addr), "r"(r[0]),
+               "r"(r[1]), "r"(r[2]), "r"(r[3])
+               : "memory");
 }
 
 // ------------------------------------------------------------------ per-n plans
-// Phase-2 slot ids: 0..4 = lane bits (t0, t1, g0, g1, g2), 5 = r1 (X1/X0), 6 = r2 (X2/X0).
-// See tools/fragment_model.py::phase2_plan and DESIGN.md "Phase 2".
-template <int Q>
-struct Phase2Plan;
-#define HC_PLAN(Q, SINGLE, MASK_A, MASK_B, NCH, C0, C1, C2, C3, C4, C5, C6, NW, W0, W1, W2, W3, W4, W5, NLC, \
-                L0, L1, L2, L3, L4, A)                                                                       \
-  template <>                                                                                                \
-  struct Phase2Plan<Q> {                                                                                     \
-    static constexpr bool single = SINGLE;                                                                   \
-    static constexpr uint32_t mask_a = MASK_A, mask_b = MASK_B;                                              \
-    static constexpr int nch = NCH, nw = NW, nlc = NLC, a = A;                                               \
-    __host__ __device__ static constexpr int ch(int i) {                                                     \
-      return i == 0 ? C0 : i == 1 ? C1 : i == 2 ? C2 : i == 3 ? C3 : i == 4 ? C4 : i == 5 ? C5 : C6;          \
-    }                                                                                                        \
-    __host__ __device__ static constexpr int w(int i) {                                                      \
-      return i == 0 ? W0 : i == 1 ? W1 : i == 2 ? W2 : i == 3 ? W3 : i == 4 ? W4 : W5;                        \
-    }                                                                                                        \
-    __host__ __device__ static constexpr int lc(int i) {                                                     \
-      return i == 0 ? L0 : i == 1 ? L1 : i == 2 ? L2 : i == 3 ? L3 : L4;                                      \
-    }                                                                                                        \
-  };
-//     Q  single mask_a mask_b nch chunk slots            nw word slots           nlc lane-chunk slots  a
-HC_PLAN(1, true, 0x8u, 0x0u, 1, 6, 0, 0, 0, 0, 0, 0, 6, 0, 1, 2, 3, 4, 5, 0, 0, 0, 0, 0, 0, 5)
-HC_PLAN(2, true, 0xAu, 0x0u, 2, 6, 0, 0, 0, 0, 0, 0, 5, 1, 2, 3, 4, 5, 0, 1, 0, 0, 0, 0, 0, 4)
-HC_PLAN(3, true, 0xEu, 0x0u, 3, 6, 0, 1, 0, 0, 0, 0, 4, 2, 3, 4, 5, 0, 0, 2, 0, 1, 0, 0, 0, 3)
-HC_PLAN(4, false, 0x8u, 0xBu, 4, 5, 6, 2, 3, 0, 0, 0, 3, 0, 1, 4, 0, 0, 0, 2, 2, 3, 0, 0, 0, 3)
-HC_PLAN(5, false, 0x8u, 0xFu, 5, 5, 6, 2, 3, 4, 0, 0, 2, 0, 1, 0, 0, 0, 0, 3, 2, 3, 4, 0, 0, 2)
-HC_PLAN(6, false, 0xAu, 0xFu, 6, 5, 6, 2, 3, 4, 0, 0, 1, 1, 0, 0, 0, 0, 0, 4, 0, 2, 3, 4, 0, 1)
-HC_PLAN(7, false, 0xEu, 0xFu, 7, 5, 6, 2, 3, 4, 0, 1, 0, 0, 0, 0, 0, 0, 0, 5, 0, 1, 2, 3, 4, 0)
-#undef HC_PLAN
-
-__device__ __forceinline__ int slot_bit(int slot, int lane, int j) {
-  return slot < 5 ? (lane >> slot) & 1 : (j >> (slot - 5)) & 1;
-}
-
-// Per-chunk XOR swizzle of the 32-bit word index inside a 512-byte chunk: the chunk
-// bits that sit in lanes during phase 2 go to bank bits [a, 5) (bank-conflict free).
-template <int Q>
-__device__ __forceinline__ uint32_t swz(uint32_t c) {
-  using P = Phase2Plan<Q>;
-  uint32_t f = 0;
-#pragma unroll
-  for (int r = 0; r < P::nlc; ++r) {
-    int idx = 0;
-#pragma unroll
-    for (int i = 0; i < P::nch; ++i)
-      if (P::ch(i) == P::lc(r)) idx = i;
-    f |= ((c >> idx) & 1u) << (P::a + r);
-  }
-  return f;
-}
-
-// Total power-of-two exponent E applied by the per-stage constants for this n.
-template <int N>
-__host__ __device__ constexpr int total_shift() {
-  if constexpr (N == 128) return stage_shift(0xFu) + stage_shift(0x7u);
-  else if constexpr (N == 256) return 2 * stage_shift(0xFu);
-  else {
-    constexpr int q = (N == 512) ? 1 : (N == 1024) ? 2 : (N == 2048) ? 3 : (N == 4096) ? 4
-                      : (N == 8192) ? 5 : (N == 16384) ? 6 : 7;
-    return 2 * stage_shift(0xFu) + stage_shift(Phase2Plan<q>::mask_a) + stage_shift(Phase2Plan<q>::mask_b);
-  }
-}
-
 template <int N>
 __host__ __device__ constexpr int log2_n() {
   int k = 0;
@@ -308,10 +266,51 @@ __host__ __device__ constexpr int log2_n() {
   return k;
 }
 
+// Phase 2 of rows with n = 256 * 2^Q (tools/fragment_model.py
+// planL/check_rowL).  A phase-2 fragment is one ldmatrix.x4.trans: lane L = 8j + r
+// supplies the address of a 16-byte granule (8 consecutive elements) for matrix j,
+// row r.  Slot bits r0 r1 r2 j0 j1 (+ per-lane extra fragments x0 x1, + loop bits):
+//   chunk bits -> slots in the order r0, r1, r2, j1, j0, x0, x1 (first Q);
+//   granule bits -> the remaining slots (low bits first), loop bits on top.
+// Contraction: M columns (h, t0, t1, j1) = (r0, r1, r2, j1) via data-as-A (one
+// stage); j0 via a second const-A stage (Q >= 5); x0, x1 via fp32 butterflies
+// across per-lane fragments (Q >= 6).  Swizzle: granule ^= chunk & (2^min(Q,3) - 1).
+template <int Q>
+struct PlanL {
+  static constexpr int nx = Q > 5 ? Q - 5 : 0;           // extra per-lane fragments (log2)
+  static constexpr bool two_stage = Q >= 5;              // j0 is a chunk bit
+  static constexpr uint32_t mask_a = (Q >= 4) ? 0xFu : ((1u << Q) - 1u);
+  static constexpr int nloop_bits = Q <= 4 ? Q : 5;      // granule bits on the loop index
+  static constexpr uint32_t swz_mask = (1u << (Q < 3 ? Q : 3)) - 1u;
+};
+
+// Per-lane part of the phase-2 byte offset inside a row: chunk * 512 + 16 * (granule ^ swz).
+template <int Q>
+__device__ __forceinline__ uint32_t phase2_lane_offset(int lane) {
+  const uint32_t r = lane & 7, j = lane >> 3;
+  const uint32_t r0 = r & 1, r1 = (r >> 1) & 1, r2 = (r >> 2) & 1, j0 = j & 1, j1 = (j >> 1) & 1;
+  uint32_t c = 0, g = 0;
+  if constexpr (Q == 1) { c = r0;                               g = j0 | (r1 << 1) | (r2 << 2) | (j1 << 3); }
+  if constexpr (Q == 2) { c = r0 | (r1 << 1);                   g = j0 | (j1 << 1) | (r2 << 2); }
+  if constexpr (Q == 3) { c = r | 0;                            g = j0 | (j1 << 1); }
+  if constexpr (Q == 4) { c = r | (j1 << 3);                    g = j0; }
+  if constexpr (Q >= 5) { c = r | (j1 << 3) | (j0 << 4);        g = 0; }
+  return c * 512u + 16u * (g ^ (c & PlanL<Q>::swz_mask));
+}
+
+// exponent E of the exact power-of-two normalization applied by the constants
+template <int N>
+__host__ __device__ constexpr int total_shift() {
+  if constexpr (N == 128) return stage_shift(0xFu) + stage_shift(0x7u);
+  else if constexpr (N == 256) return 2 * stage_shift(0xFu);
+  else return 2 * stage_shift(0xFu) + stage_shift(PlanL<log2_n<N>() - 8>::mask_a);
+}
+
 // ------------------------------------------------------------------ kernel
 // Template parameters: N (row length), DT (dtype), TILE_ROWS (rows per pipeline
-// stage), STAGES (ring depth), NT (compute warps), P (warps per row team, n>256).
-template <int N, int DT, int TILE_ROWS, int STAGES, int NT, int P>
+// stage), STAGES (ring depth), NT (compute warps), P (warps per row team, n > 256),
+// U (work items per warp processed together, for ILP).
+template <int N, int DT, int TILE_ROWS, int STAGES, int NT, int P, int U>
 __global__ void __launch_bounds__((NT + 1) * 32, 1)
     fwht_kernel(const uint16_t* __restrict__ in, uint16_t* __restrict__ out, int64_t m, float s_res) {
   constexpr int ROW_BYTES = 2 * N;
@@ -355,31 +354,41 @@ __global__ void __launch_bounds__((NT + 1) * 32, 1)
   }
 
   // ---------------- consumers
-  
   int it = 0;
   if constexpr (N == 128) {
     uint32_t A1[4], A2[4];
     make_const_a<DT>(0xFu, A1);  // H_16 over element bits {0,1,2,3}
     make_const_a<DT>(0x7u, A2);  // H_8 over bits {4,5,6} (x) I_2 (bit 1, same row)
     constexpr int FR = TILE_ROWS / 2;  // fragments (row pairs) per tile
+    static_assert(FR % (NT * U) == 0, "n=128 work split");
     for (int64_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
       const int s = it % STAGES;
       mbar_wait(&full[s], (it / STAGES) & 1);
       const int64_t row0 = tile * TILE_ROWS;
       const int rows = (m - row0) < TILE_ROWS ? int(m - row0) : TILE_ROWS;
-      uint8_t* const tb = smem + s * TILE_BYTES;
-#pragma unroll 2
-      for (int f = warp; f < FR; f += NT) {
-        const uint8_t* ra = tb + (2 * f) * ROW_BYTES + lane * 8;
-        const uint8_t* rb = ra + ROW_BYTES;
-        uint32_t x[4], y[4], z[4];
-        lds64(ra, x[0], x[2]);  // row A elements 4l..4l+3
-        lds64(rb, x[1], x[3]);  // row B
-        stage_ca<DT>(A1, x[0], x[2], x[1], x[3], y);
-        stage_ca_final<DT>(A2, y[0], y[1], y[2], y[3], s_res, z);
-        uint16_t* o = out + (row0 + 2 * f) * N + lane * 4;
-        if (2 * f < rows) stg64(o, z[0], z[1]);
-        if (2 * f + 1 < rows) stg64(o + N, z[2], z[3]);
+      const uint8_t* tb = smem + s * TILE_BYTES;
+      for (int f0 = warp; f0 < FR; f0 += NT * U) {
+        uint32_t x[U][4], y[U][4], z[U][4];
+        float d[U][8];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const uint8_t* ra = tb + (2 * (f0 + u * NT)) * ROW_BYTES + lane * 8;
+          lds64(ra, x[u][0], x[u][2]);              // row A elements 4l..4l+3
+          lds64(ra + ROW_BYTES, x[u][1], x[u][3]);  // row B
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          stage_ca<DT>(A1, x[u][0], x[u][2], x[u][1], x[u][3], y[u]);
+          stage_ca_f32<DT>(A2, y[u][0], y[u][1], y[u][2], y[u][3], d[u]);
+          scale_pack<DT>(d[u], s_res, z[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int f = f0 + u * NT;
+          uint16_t* o = out + (row0 + 2 * f) * N + lane * 4;
+          if (2 * f < rows) stg64(o, z[u][0], z[u][1]);
+          if (2 * f + 1 < rows) stg64(o + N, z[u][2], z[u][3]);
+        }
       }
       fence_proxy_async_smem();
       __syncwarp();
@@ -388,19 +397,29 @@ __global__ void __launch_bounds__((NT + 1) * 32, 1)
   } else if constexpr (N == 256) {
     uint32_t A1[4];
     make_const_a<DT>(0xFu, A1);
+    static_assert(TILE_ROWS % (NT * U) == 0, "n=256 work split");
     for (int64_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
       const int s = it % STAGES;
       mbar_wait(&full[s], (it / STAGES) & 1);
       const int64_t row0 = tile * TILE_ROWS;
       const int rows = (m - row0) < TILE_ROWS ? int(m - row0) : TILE_ROWS;
-      uint8_t* const tb = smem + s * TILE_BYTES;
-#pragma unroll 2
-      for (int r = warp; r < TILE_ROWS; r += NT) {
-        uint32_t x[4], y[4], z[4];
-        lds128(tb + r * ROW_BYTES + lane * 16, x[0], x[1], x[2], x[3]);
-        stage_ca<DT>(A1, x[0], x[2], x[1], x[3], y);
-        stage_ca_final<DT>(A1, y[0], y[2], y[1], y[3], s_res, z);
-        if (r < rows) stg128(out + (row0 + r) * N + lane * 8, z[0], z[1], z[2], z[3]);
+      const uint8_t* tb = smem + s * TILE_BYTES;
+      for (int r0 = warp; r0 < TILE_ROWS; r0 += NT * U) {
+        uint32_t x[U][4], y[U][4], z[U][4];
+        float d[U][8];
+#pragma unroll
+        for (int u = 0; u < U; ++u) lds128(tb + (r0 + u * NT) * ROW_BYTES + lane * 16, x[u][0], x[u][1], x[u][2], x[u][3]);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          stage_ca<DT>(A1, x[u][0], x[u][2], x[u][1], x[u][3], y[u]);
+          stage_ca_f32<DT>(A1, y[u][0], y[u][2], y[u][1], y[u][3], d[u]);
+          scale_pack<DT>(d[u], s_res, z[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int r = r0 + u * NT;
+          if (r < rows) stg128(out + (row0 + r) * N + lane * 8, z[u][0], z[u][1], z[u][2], z[u][3]);
+        }
       }
       fence_proxy_async_smem();
       __syncwarp();
@@ -408,36 +427,31 @@ __global__ void __launch_bounds__((NT + 1) * 32, 1)
     }
   } else {
     constexpr int Q = log2_n<N>() - 8;
-    constexpr int C = N / 256;  // chunks per row
-    using PL = Phase2Plan<Q>;
-    constexpr int NFRAG = 1 << (7 - PL::nw);  // phase-2 fragments per row (== C)
-    static_assert(NFRAG == C, "phase-2 fragment count");
+    constexpr int C = N / 256;  // 256-chunks per row
+    using PL = PlanL<Q>;
+    constexpr int NLOOP = 1 << PL::nloop_bits;           // phase-2 items per row
+    static_assert(NLOOP << PL::nx == C, "phase-2 fragment count");
     constexpr int NTEAMS = NT / P;
     static_assert(NT % P == 0 && TILE_ROWS % NTEAMS == 0, "team layout");
-    constexpr int ROWS_PER_TEAM = TILE_ROWS / NTEAMS;
+    constexpr int RPT = TILE_ROWS / NTEAMS;               // rows per team
+    constexpr int ITEMS1 = RPT * C, ITEMS2 = RPT * NLOOP;  // phase-1/3 and phase-2 items per team
+    constexpr int U1 = (ITEMS1 / P) >= U ? U : 1;
+    constexpr int U2 = (ITEMS2 / P) >= U ? U : 1;
+    static_assert(ITEMS1 % (P * U1) == 0 && ITEMS2 % (P * U2) == 0, "work split");
     const int team = warp / P, wt = warp % P;
 
     uint32_t A256[4];
     make_const_a<DT>(0xFu, A256);
     uint32_t Pa[4], Pb[4], Bc0[2], Bc1[2];
-    if constexpr (PL::single) {
+    if constexpr (PL::two_stage) {
+      make_const_a<DT>(0xFu, Pa);   // H_16 over (r0, r1, r2, j1)
+      make_const_a<DT>(0x8u, Pb);   // H_2 over j0 (x) I_8
+    } else {
       make_const_b<DT>(PL::mask_a, 0, Bc0);
       make_const_b<DT>(PL::mask_a, 1, Bc1);
-    } else {
-      make_const_a<DT>(PL::mask_a, Pa);
-      make_const_a<DT>(PL::mask_b, Pb);
     }
-    // per-lane phase-2 word offsets (within a row, in 32-bit words) for the 4 regs
-    uint32_t off2[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      uint32_t c = 0, w = 0;
-#pragma unroll
-      for (int i = 0; i < PL::nch; ++i) c |= uint32_t(slot_bit(PL::ch(i), lane, j)) << i;
-#pragma unroll
-      for (int i = 0; i < PL::nw; ++i) w |= uint32_t(slot_bit(PL::w(i), lane, j)) << i;
-      off2[j] = c * 128u + (w ^ swz<Q>(c));
-    }
+    const uint32_t off2 = phase2_lane_offset<Q>(lane);
+    const uint32_t tile_base_sh = smem_addr(smem);
 
     auto team_sync = [&]() {
       if constexpr (P == 1) {
@@ -454,55 +468,92 @@ __global__ void __launch_bounds__((NT + 1) * 32, 1)
       const int rows = (m - row0) < TILE_ROWS ? int(m - row0) : TILE_ROWS;
       uint8_t* const tb = smem + s * TILE_BYTES;
 
-      // ---- phase 1: H_256 on every 256-chunk of the team's rows
-#pragma unroll 2
-      for (int item = wt; item < ROWS_PER_TEAM * C; item += P) {
-        const int r = team + NTEAMS * (item / C), c = item % C;
-        uint8_t* const cb = tb + r * ROW_BYTES + c * 512;
-        uint32_t x[4], y[4], z[4];
+      // ---- phase 1: H_256 on every 256-chunk, swizzled write-back
+      for (int i0 = wt; i0 < ITEMS1; i0 += P * U1) {
+        uint32_t x[U1][4], y[U1][4], z[U1][4];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) x[j] = lds32(cb + 4 * (lane + 32 * j));
-        stage_ca<DT>(A256, x[0], x[2], x[1], x[3], y);
-        stage_ca<DT>(A256, y[0], y[2], y[1], y[3], z);
-        const uint32_t f = swz<Q>(uint32_t(c));
+        for (int u = 0; u < U1; ++u) {
+          const int item = i0 + u * P, r = team + NTEAMS * (item / C), c = item % C;
+          lds128(tb + r * ROW_BYTES + c * 512 + lane * 16, x[u][0], x[u][1], x[u][2], x[u][3]);
+        }
 #pragma unroll
-        for (int j = 0; j < 4; ++j) sts32(cb + 4 * ((lane + 32 * j) ^ f), z[j]);
+        for (int u = 0; u < U1; ++u) {
+          stage_ca<DT>(A256, x[u][0], x[u][2], x[u][1], x[u][3], y[u]);
+          stage_ca<DT>(A256, y[u][0], y[u][2], y[u][1], y[u][3], z[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < U1; ++u) {
+          const int item = i0 + u * P, r = team + NTEAMS * (item / C), c = item % C;
+          const uint32_t g = uint32_t(lane) ^ (uint32_t(c) & PL::swz_mask);
+          stg_sh128(tb + r * ROW_BYTES + c * 512 + g * 16, z[u]);
+        }
       }
       team_sync();  // P:126 "Sync across the threadblock"
 
-      // ---- phase 2: H_{n/256} across chunks, residual 2^a block
-#pragma unroll 2
-      for (int item = wt; item < ROWS_PER_TEAM * NFRAG; item += P) {
-        const int r = team + NTEAMS * (item / NFRAG), fr = item % NFRAG;
-        uint8_t* const rb = tb + r * ROW_BYTES;
-        const uint32_t fx = uint32_t(fr) << PL::nw;
-        uint32_t x[4], y[4], z[4];
+      // ---- phase 2: H_{n/256} across chunks (residual 2^a factor)
+      for (int i0 = wt; i0 < ITEMS2; i0 += P * U2) {
+        uint32_t x[U2][1 << PL::nx][4];
+        uint32_t addr[U2][1 << PL::nx];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) x[j] = lds32(rb + 4 * (off2[j] ^ fx));
-        if constexpr (PL::single) {
-          stage_da_final<DT>(x, Bc0, Bc1, s_res, z);
-        } else {
-          stage_ca<DT>(Pa, x[0], x[2], x[1], x[3], y);
-          stage_ca_final<DT>(Pb, y[0], y[2], y[1], y[3], s_res, z);
+        for (int u = 0; u < U2; ++u) {
+          const int item = i0 + u * P, r = team + NTEAMS * (item / NLOOP), lp = item % NLOOP;
+          const uint32_t rb = tile_base_sh + s * TILE_BYTES + r * ROW_BYTES;
+#pragma unroll
+          for (int xi = 0; xi < (1 << PL::nx); ++xi) {
+            // loop bits are the top granule bits; extra fragments are chunk bits 5, 6
+            addr[u][xi] = rb + ((off2 ^ (uint32_t(lp) << (4 + 5 - PL::nloop_bits))) + uint32_t(xi) * (32u * 512u));
+            ldsm_x4_t(addr[u][xi], x[u][xi]);
+          }
         }
 #pragma unroll
-        for (int j = 0; j < 4; ++j) sts32(rb + 4 * (off2[j] ^ fx), z[j]);
+        for (int u = 0; u < U2; ++u) {
+          float d[1 << PL::nx][8];
+#pragma unroll
+          for (int xi = 0; xi < (1 << PL::nx); ++xi) {
+            if constexpr (PL::two_stage) {
+              uint32_t y[4];
+              stage_ca<DT>(Pa, x[u][xi][0], x[u][xi][2], x[u][xi][1], x[u][xi][3], y);
+              stage_ca_f32<DT>(Pb, y[0], y[2], y[1], y[3], d[xi]);
+            } else {
+              stage_da_f32<DT>(x[u][xi], Bc0, Bc1, d[xi]);
+            }
+          }
+          // chunk bits 5, 6 live in per-lane fragments: fp32 butterflies (P:50-64 listing)
+#pragma unroll
+          for (int b = 0; b < PL::nx; ++b)
+#pragma unroll
+            for (int xi = 0; xi < (1 << PL::nx); ++xi)
+              if (!((xi >> b) & 1)) {
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                  const float p0 = d[xi][e], p1 = d[xi | (1 << b)][e];
+                  d[xi][e] = p0 + p1;
+                  d[xi | (1 << b)][e] = p0 - p1;
+                }
+              }
+#pragma unroll
+          for (int xi = 0; xi < (1 << PL::nx); ++xi) {
+            uint32_t z[4];
+            scale_pack<DT>(d[xi], s_res, z);
+            stsm_x4_t(addr[u][xi], z);
+          }
+        }
       }
       team_sync();
 
-      // ---- phase 3: un-swizzle and store (coalesced 128 B per warp instruction)
-#pragma unroll 2
-      for (int item = wt; item < ROWS_PER_TEAM * C; item += P) {
-        const int r = team + NTEAMS * (item / C), c = item % C;
-        uint8_t* const cb = tb + r * ROW_BYTES + c * 512;
-        const uint32_t f = swz<Q>(uint32_t(c));
-        uint32_t z[4];
+      // ---- phase 3: un-swizzle and store (512 B per warp instruction)
+      for (int i0 = wt; i0 < ITEMS1; i0 += P * U1) {
+        uint32_t z[U1][4];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) z[j] = lds32(cb + 4 * ((lane + 32 * j) ^ f));
-        if (r < rows) {
-          uint16_t* o = out + (row0 + r) * N + c * 256;
+        for (int u = 0; u < U1; ++u) {
+          const int item = i0 + u * P, r = team + NTEAMS * (item / C), c = item % C;
+          const uint32_t g = uint32_t(lane) ^ (uint32_t(c) & PL::swz_mask);
+          lds128(tb + r * ROW_BYTES + c * 512 + g * 16, z[u][0], z[u][1], z[u][2], z[u][3]);
+        }
 #pragma unroll
-          for (int j = 0; j < 4; ++j) stg32(o + 2 * (lane + 32 * j), z[j]);
+        for (int u = 0; u < U1; ++u) {
+          const int item = i0 + u * P, r = team + NTEAMS * (item / C), c = item % C;
+          if (r < rows) stg128(out + (row0 + r) * N + c * 256 + lane * 8, z[u][0], z[u][1], z[u][2], z[u][3]);
         }
       }
       fence_proxy_async_smem();

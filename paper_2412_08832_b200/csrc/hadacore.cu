@@ -30,27 +30,41 @@ int sm_count(int dev) {
   return v;
 }
 
-// Per-n launch configuration: rows per pipeline
-// stage (32 KiB tiles; 64 KiB for n = 2^15 where one row is 64 KiB), ring depth,
-// compute warps, warps per row team.
+// Per-n launch configuration.  One persistent
+// CTA per SM: NT compute warps + 1 producer warp, a STAGES-deep ring of tiles of
+// ~TILE_KB KiB (whole rows; one 64 KiB row for n = 2^15), rows split into teams of
+// P warps (n > 256) that synchronise with named barriers.  The HC_* macros let
+// tools/tune.py build variants; the defaults are the tuned values.
+#ifndef HC_NT
+#define HC_NT 8
+#endif
+#ifndef HC_TILE_KB
+#define HC_TILE_KB 32
+#endif
+#ifndef HC_STAGES
+#define HC_STAGES 4
+#endif
+#ifndef HC_U
+#define HC_U 2
+#endif
 template <int N>
-struct Cfg;
-template <> struct Cfg<128>   { static constexpr int rows = 128, stages = 4, nt = 8, p = 1; };
-template <> struct Cfg<256>   { static constexpr int rows = 64,  stages = 4, nt = 8, p = 1; };
-template <> struct Cfg<512>   { static constexpr int rows = 32,  stages = 4, nt = 8, p = 1; };
-template <> struct Cfg<1024>  { static constexpr int rows = 16,  stages = 4, nt = 8, p = 1; };
-template <> struct Cfg<2048>  { static constexpr int rows = 8,   stages = 4, nt = 8, p = 1; };
-template <> struct Cfg<4096>  { static constexpr int rows = 4,   stages = 4, nt = 8, p = 2; };
-template <> struct Cfg<8192>  { static constexpr int rows = 2,   stages = 4, nt = 8, p = 4; };
-template <> struct Cfg<16384> { static constexpr int rows = 1,   stages = 4, nt = 8, p = 8; };
-template <> struct Cfg<32768> { static constexpr int rows = 1,   stages = 3, nt = 8, p = 8; };
+struct Cfg {
+  static constexpr int nt = HC_NT;
+  static constexpr int rows = (HC_TILE_KB * 1024) / (2 * N) > 0 ? (HC_TILE_KB * 1024) / (2 * N) : 1;
+  static constexpr int tile_bytes = rows * 2 * N;
+  static constexpr int max_stages = (227 * 1024 - 256) / tile_bytes;
+  static constexpr int stages = HC_STAGES < max_stages ? HC_STAGES : max_stages;
+  static constexpr int nteams = N <= 256 ? 1 : (rows < nt ? rows : nt);
+  static constexpr int p = N <= 256 ? 1 : nt / nteams;
+  static constexpr int u = HC_U;
+  static_assert(stages >= 2, "need at least a double-buffered ring");
+};
 
 template <int N, int DT>
 hadacore_status_t launch(const void* in, void* out, int64_t m, float scale, cudaStream_t stream) {
   using C = Cfg<N>;
-  constexpr int tile_bytes = C::rows * 2 * N;
-  constexpr int smem = C::stages * tile_bytes + 2 * C::stages * 8;
-  auto kern = fwht_kernel<N, DT, C::rows, C::stages, C::nt, C::p>;
+  constexpr int smem = C::stages * C::tile_bytes + 2 * C::stages * 8;
+  auto kern = fwht_kernel<N, DT, C::rows, C::stages, C::nt, C::p, C::u>;
   static std::atomic<uint64_t> attr_done{0};
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return HADACORE_ERR_CUDA;

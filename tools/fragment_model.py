@@ -342,3 +342,143 @@ def main_rows():
         ok, conf, plan, kinds, E = check_row(1 << k)
         print(f"n={1<<k:6d} ok={ok} bank_conflicts={conf} stages={kinds} E={E} "
               f"a={plan['a']} frags={1<<plan['nfrag_bits']} chunk_slots={plan['chunk_slots']} word_slots={plan['word_slots']}")
+
+
+# ---------------------------------------------------------------------------
+# Design "L" (ldmatrix/stmatrix .trans, 16-byte granules): phase 1 LDS.128/STS.128,
+# phase 2 LDSM.T.x4 -> mma -> STSM.T.x4, phase 3 LDS.128/STG.128.
+# Granule = 8 consecutive elements (16 B); a chunk (256 el) has 32 granules.
+# Swizzle: granule' = granule ^ (chunk & ((1 << min(q,3)) - 1)).
+# Phase-2 row slots: lane L = 8*j + r provides the row address of (matrix j, row r);
+# slot bits r0, r1, r2, j0, j1, then fragment-index bits f0, f1, ...
+# ---------------------------------------------------------------------------
+
+
+def planL(q):
+    """chunk bit i -> slot; granule bit i -> slot (slots: r0 r1 r2 j0 j1 f0 f1 ...)."""
+    chunk_slot_order = ["r0", "r1", "r2", "j1", "j0", "x0", "x1"]   # x* = extra (per-lane) fragment bits
+    chunk = chunk_slot_order[:q]
+    # granule bits 0..4: bit i (i<3) prefers slot r_i when free, else next free slot
+    free = [s for s in ["r0", "r1", "r2", "j0", "j1"] if s not in chunk]
+    gran = []
+    for i in range(5):
+        pref = f"r{i}" if i < 3 else None
+        if pref and pref in free:
+            gran.append(pref); free.remove(pref)
+        elif i == 0 and "j0" in free:
+            gran.append("j0"); free.remove("j0")
+        elif i == 1 and "j1" in free:
+            gran.append("j1"); free.remove("j1")
+        elif free:
+            gran.append(free.pop(0))
+        else:
+            gran.append(f"f{i}")  # loop (fragment) index
+    return chunk, gran
+
+
+def swzL(q, c):
+    return c & ((1 << min(q, 3)) - 1)
+
+
+def check_rowL(n, seed=0, verbose=False):
+    k = n.bit_length() - 1
+    q = k - 8
+    C = 1 << q
+    chunk_slots, gran_slots = planL(q)
+    x = np.random.default_rng(seed).standard_normal(n)
+    sm = np.zeros(n)
+
+    def gaddr(c, gr):  # element offset of granule gr of chunk c (after swizzle)
+        return c * 256 + 8 * (gr ^ swzL(q, c))
+
+    A256 = kron_const("HHHH", 0.25)
+    E = 4
+    # phase 1: lane l holds granule l: X_j = elements 8l + 2j + h
+    for c in range(C):
+        vals = np.zeros((32, 4, 2))
+        for l in range(32):
+            vals[l] = x[c * 256 + 8 * l: c * 256 + 8 * l + 8].reshape(4, 2)
+        v = stage_const_a(stage_const_a(vals, A256, (0, 2, 1, 3)), A256, (0, 2, 1, 3))
+        for l in range(32):
+            o = gaddr(c, l)
+            sm[o:o + 8] = v[l].reshape(8)
+    # phase 2
+    nx = max(0, q - 5)                    # extra fragment bits handled in registers
+    loop_bits = [s for s in gran_slots if s.startswith("f")]
+    n_loop = 1 << len(loop_bits)
+    conflicts = 0
+    in_chunk = [s for s in chunk_slots if not s.startswith("x")]
+    mask_a = 0
+    for s in in_chunk:
+        if s in ("r0", "r1", "r2", "j1"):
+            mask_a |= 1 << ["r0", "r1", "r2", "j1"].index(s)
+    two_stage = "j0" in in_chunk
+    for it in range(n_loop):
+        frags = []
+        addrs_all = []
+        for xi in range(1 << nx):
+            slotv = {}
+            for b, s in enumerate(loop_bits):
+                slotv[s] = (it >> b) & 1
+            for b in range(nx):
+                slotv[f"x{b}"] = (xi >> b) & 1
+            addrs = {}
+            for L in range(32):
+                j, r = L // 8, L % 8
+                sv = dict(slotv, r0=r & 1, r1=(r >> 1) & 1, r2=(r >> 2) & 1, j0=j & 1, j1=(j >> 1) & 1)
+                c = sum(sv[s] << i for i, s in enumerate(chunk_slots))
+                gr = sum(sv[s] << i for i, s in enumerate(gran_slots))
+                addrs[(j, r)] = gaddr(c, gr)
+            for j in range(4):
+                groups = {((addrs[(j, r)] * 2) // 16) % 8 for r in range(8)}
+                conflicts += 8 - len(groups)
+            # ldmatrix.trans: lane (g,t) reg j = {M_j[2t][g], M_j[2t+1][g]}, M_j[r][col] = sm[addr(j,r)+col]
+            vals = np.zeros((32, 4, 2))
+            for lane in range(32):
+                g, t = lane >> 2, lane & 3
+                for j in range(4):
+                    for h in range(2):
+                        vals[lane, j, h] = sm[addrs[(j, 2 * t + h)] + g]
+            frags.append(vals)
+            addrs_all.append(addrs)
+        outs = []
+        for vals in frags:
+            if two_stage:
+                v = stage_const_a(vals, kron_const(format(mask_a, "04b")[::-1].replace("1", "H").replace("0", "I"), 0.25 if bin(mask_a).count("1") >= 4 else 2.0 ** -(bin(mask_a).count("1") // 2)), (0, 2, 1, 3))
+                v = stage_const_a(v, kron_const("IIIH", 1.0), (0, 2, 1, 3))
+            else:
+                kinds = "".join("H" if (mask_a >> b) & 1 else "I" for b in range(4))
+                v = stage_data_a(vals, kron_const(kinds, 2.0 ** -(kinds.count("H") // 2)))
+            outs.append(v)
+        # in-register butterflies across the extra fragments (unnormalized)
+        for b in range(nx):
+            for xi in range(1 << nx):
+                if not (xi >> b) & 1:
+                    a_, b_ = outs[xi], outs[xi | (1 << b)]
+                    outs[xi], outs[xi | (1 << b)] = a_ + b_, a_ - b_
+        for vals, addrs in zip(outs, addrs_all):
+            for lane in range(32):
+                g, t = lane >> 2, lane & 3
+                for j in range(4):
+                    for h in range(2):
+                        sm[addrs[(j, 2 * t + h)] + g] = vals[lane, j, h]
+    hb = bin(mask_a).count("1")
+    E += hb // 2 + (0 if not two_stage else 0)
+    # phase 3
+    y = np.zeros(n)
+    for c in range(C):
+        for l in range(32):
+            o = gaddr(c, l)
+            y[c * 256 + 8 * l: c * 256 + 8 * l + 8] = sm[o:o + 8]
+    ref = fwht_np(x[None, :])[0]
+    ratio = y / np.where(ref == 0, 1, ref)
+    scale = np.median(ratio)
+    ok = np.allclose(y, ref * scale)
+    return ok, conflicts, chunk_slots, gran_slots, scale, mask_a, two_stage
+
+
+def main_rowsL():
+    for k in range(9, 16):
+        ok, conf, cs, gs, sc, ma, ts = check_rowL(1 << k)
+        print(f"n={1<<k:6d} ok={ok} ldsm_conflicts={conf} chunk={cs} gran={gs} mask_a={ma:#x} two_stage={ts} "
+              f"scale=2^{np.log2(sc):.1f}")

@@ -1,0 +1,82 @@
+"""Launch-configuration sweep (dev tool): build libhadacore variants with different
+HC_* macros (NT compute warps, tile KiB, ring stages, unroll U) and time each
+(n, dtype) at 2^28 elements on the GPU.
+
+    python tools/tune.py build  "8,32,4,2" "16,32,4,2" ...   # here (nvcc)
+    python tools/tune.py run                                  # on the GPU box
+"""
+import ctypes
+import glob
+import json
+import os
+import subprocess
+import sys
+from concurrent.futures import ThreadPoolExecutor
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+OUT = os.path.join(ROOT, "build", "tune")
+NS = [1 << k for k in range(7, 16)]
+
+
+def build_one(spec):
+    nt, tkb, st, u = spec.split(",")
+    name = f"nt{nt}_t{tkb}_s{st}_u{u}"
+    so = os.path.join(OUT, f"libhc_{name}.so")
+    cmd = ["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
+           "-Xcompiler", "-fPIC", "-shared", f"-DHC_NT={nt}", f"-DHC_TILE_KB={tkb}", f"-DHC_STAGES={st}",
+           f"-DHC_U={u}", "-o", so, os.path.join(ROOT, "paper_2412_08832_b200", "csrc", "hadacore.cu")]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    return name, r.returncode, r.stderr[-2000:]
+
+
+def build(specs):
+    os.makedirs(OUT, exist_ok=True)
+    with ThreadPoolExecutor(max_workers=8) as ex:
+        for name, rc, err in ex.map(build_one, specs):
+            print(name, "ok" if rc == 0 else f"FAILED\n{err}")
+
+
+def run(reps=7, ns=None):
+    import torch
+    libs = sorted(glob.glob(os.path.join(OUT, "libhc_*.so")))
+    elems = 1 << 28
+    src = torch.randn(elems, device="cuda").to(torch.float16)
+    dst = torch.empty_like(src)
+    results = {}
+    for path in libs:
+        name = os.path.basename(path)[6:-3]
+        lib = ctypes.CDLL(path)
+        f = lib.hadacore_fwht
+        f.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int,
+                      ctypes.c_float, ctypes.c_void_p]
+        res = {}
+        st = torch.cuda.current_stream().cuda_stream
+        for dt in (0, 1):
+            for n in (ns or NS):
+                m = elems // n
+                for _ in range(2):
+                    assert f(src.data_ptr(), dst.data_ptr(), m, n, dt, 1.0, st) == 0
+                ts = []
+                for _ in range(reps):
+                    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    a.record()
+                    f(src.data_ptr(), dst.data_ptr(), m, n, dt, 1.0, st)
+                    b.record()
+                    b.synchronize()
+                    ts.append(a.elapsed_time(b))
+                ts.sort()
+                res[f"{'f16' if dt == 0 else 'bf16'}_{n}"] = round(4.0 * elems / (ts[len(ts) // 2] * 1e-3) / 1e9, 0)
+        results[name] = res
+        print(name, " ".join(f"{k}={v:.0f}" for k, v in res.items()), flush=True)
+    # best per (dtype, n)
+    keys = list(next(iter(results.values())).keys())
+    best = {k: max(results, key=lambda nm: results[nm][k]) for k in keys}
+    print("BEST", json.dumps({k: (best[k], results[best[k]][k]) for k in keys}))
+    json.dump(results, open(os.path.join(ROOT, "gpurun_out", "tune.json"), "w"), indent=1)
+
+
+if __name__ == "__main__":
+    if sys.argv[1] == "build":
+        build(sys.argv[2:])
+    else:
+        run()
