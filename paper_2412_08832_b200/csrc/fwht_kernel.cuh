@@ -26,6 +26,7 @@
 //
 // The lane/register slot algebra is modelled and checked in tools/fragment_model.py.
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -129,6 +130,10 @@ __device__ __forceinline__ uint32_t pack2(float lo, float hi) {
 // D(f32 x4) = A(16x16, 4 regs) * B(16x8, 2 regs)
 template <int DT>
 __device__ __forceinline__ void mma_f32(const uint32_t a[4], uint32_t b0, uint32_t b1, float d[4]) {
+#ifdef HC_NOCOMPUTE  // diagnostic build (tools/tune.py): data movement only
+  d[0] = __uint_as_float(b0); d[1] = __uint_as_float(b0 ^ a[0]); d[2] = __uint_as_float(b1); d[3] = __uint_as_float(b1);
+  return;
+#endif
   if constexpr (DT == DT_F16) {
     asm(
         "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
@@ -148,6 +153,11 @@ __device__ __forceinline__ void mma_f32(const uint32_t a[4], uint32_t b0, uint32
 template <int DT>
 __device__ __forceinline__ void mma_pk(const uint32_t a[4], uint32_t b0, uint32_t b1, uint32_t& d01,
                                        uint32_t& d23) {
+#ifdef HC_NOCOMPUTE
+  d01 = b0 ^ a[1];
+  d23 = b1;
+  return;
+#endif
   if constexpr (DT == DT_F16) {
     asm(
         "mma.sync.aligned.m16n8k16.row.col.f16.f16.f16.f16 {%0,%1}, {%2,%3,%4,%5}, {%6,%7}, {%8,%8};"
@@ -284,20 +294,6 @@ struct PlanL {
   static constexpr uint32_t swz_mask = (1u << (Q < 3 ? Q : 3)) - 1u;
 };
 
-// Per-lane part of the phase-2 byte offset inside a row: chunk * 512 + 16 * (granule ^ swz).
-template <int Q>
-__device__ __forceinline__ uint32_t phase2_lane_offset(int lane) {
-  const uint32_t r = lane & 7, j = lane >> 3;
-  const uint32_t r0 = r & 1, r1 = (r >> 1) & 1, r2 = (r >> 2) & 1, j0 = j & 1, j1 = (j >> 1) & 1;
-  uint32_t c = 0, g = 0;
-  if constexpr (Q == 1) { c = r0;                               g = j0 | (r1 << 1) | (r2 << 2) | (j1 << 3); }
-  if constexpr (Q == 2) { c = r0 | (r1 << 1);                   g = j0 | (j1 << 1) | (r2 << 2); }
-  if constexpr (Q == 3) { c = r | 0;                            g = j0 | (j1 << 1); }
-  if constexpr (Q == 4) { c = r | (j1 << 3);                    g = j0; }
-  if constexpr (Q >= 5) { c = r | (j1 << 3) | (j0 << 4);        g = 0; }
-  return c * 512u + 16u * (g ^ (c & PlanL<Q>::swz_mask));
-}
-
 // exponent E of the exact power-of-two normalization applied by the constants
 template <int N>
 __host__ __device__ constexpr int total_shift() {
@@ -309,9 +305,9 @@ __host__ __device__ constexpr int total_shift() {
 // ------------------------------------------------------------------ kernel
 // Template parameters: N (row length), DT (dtype), TILE_ROWS (rows per pipeline
 // stage), STAGES (ring depth), NT (compute warps), P (warps per row team, n > 256),
-// U (work items per warp processed together, for ILP).
-template <int N, int DT, int TILE_ROWS, int STAGES, int NT, int P, int U>
-__global__ void __launch_bounds__((NT + 1) * 32, 1)
+// U (work items per warp processed together, for ILP), CTAS (resident CTAs per SM).
+template <int N, int DT, int TILE_ROWS, int STAGES, int NT, int P, int U, int CTAS>
+__global__ void __launch_bounds__((NT + 1) * 32, CTAS)
     fwht_kernel(const uint16_t* __restrict__ in, uint16_t* __restrict__ out, int64_t m, float s_res) {
   constexpr int ROW_BYTES = 2 * N;
   constexpr int TILE_BYTES = TILE_ROWS * ROW_BYTES;
@@ -426,140 +422,226 @@ __global__ void __launch_bounds__((NT + 1) * 32, 1)
       if (lane == 0) mbar_arrive(&empty[s]);
     }
   } else {
-    constexpr int Q = log2_n<N>() - 8;
-    constexpr int C = N / 256;  // 256-chunks per row
-    using PL = PlanL<Q>;
-    constexpr int NLOOP = 1 << PL::nloop_bits;           // phase-2 items per row
-    static_assert(NLOOP << PL::nx == C, "phase-2 fragment count");
-    constexpr int NTEAMS = NT / P;
-    static_assert(NT % P == 0 && TILE_ROWS % NTEAMS == 0, "team layout");
-    constexpr int RPT = TILE_ROWS / NTEAMS;               // rows per team
-    constexpr int ITEMS1 = RPT * C, ITEMS2 = RPT * NLOOP;  // phase-1/3 and phase-2 items per team
-    constexpr int U1 = (ITEMS1 / P) >= U ? U : 1;
-    constexpr int U2 = (ITEMS2 / P) >= U ? U : 1;
-    static_assert(ITEMS1 % (P * U1) == 0 && ITEMS2 % (P * U2) == 0, "work split");
-    const int team = warp / P, wt = warp % P;
+    static_assert(N <= 256, "rows longer than 256 use fwht_rows_kernel");
+  }
+}
 
-    uint32_t A256[4];
-    make_const_a<DT>(0xFu, A256);
-    uint32_t Pa[4], Pb[4], Bc0[2], Bc1[2];
-    if constexpr (PL::two_stage) {
-      make_const_a<DT>(0xFu, Pa);   // H_16 over (r0, r1, r2, j1)
-      make_const_a<DT>(0x8u, Pb);   // H_2 over j0 (x) I_8
-    } else {
-      make_const_b<DT>(PL::mask_a, 0, Bc0);
-      make_const_b<DT>(PL::mask_a, 1, Bc1);
+// ------------------------------------------------------------------ TMA tensor helpers
+__device__ __forceinline__ void tma_prefetch(const void* tmap) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(tmap)) : "memory");
+}
+// 4-D tiled TMA load (SASS UTMALDG) with completion on an mbarrier.
+__device__ __forceinline__ void tma_load_4d(void* dst, const void* tmap, int c0, int c1, int c2, int c3,
+                                            uint64_t* bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3, %4, %5}], [%6], %7;" ::"r"(smem_addr(dst)),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_addr(bar)), "l"(policy)
+      : "memory");
+}
+// 4-D tiled TMA store (SASS UTMASTG), bulk-group completion.
+__device__ __forceinline__ void tma_store_4d(const void* tmap, int c0, int c1, int c2, int c3, const void* src) {
+  asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.tile.bulk_group [%0, {%1, %2, %3, %4}], [%5];" ::"l"(
+                   reinterpret_cast<uint64_t>(tmap)),
+               "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_addr(src))
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read_all() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+// Byte offset, inside a row's shared-memory image, of granule g (8 elements) of
+// 256-chunk c.  The 4-D TMA box (64 el, C chunks, 4 segments, rows) with
+// SWIZZLE_128B lays a row out as 128-byte lines L = s*C + c (s = g >> 3) and XORs
+// the 16-byte granule index inside a line with L & 7 (tools/fragment_model.py gaddrT).
+template <int C>
+__device__ __forceinline__ uint32_t gofs(uint32_t c, uint32_t g) {
+  const uint32_t L = (g >> 3) * C + c;
+  return L * 128u + 16u * ((g & 7u) ^ (L & 7u));
+}
+
+// ------------------------------------------------------------------ rows > 256
+// Rows of n = 256 * 2^Q elements (P:120-129 [Sec. 3.2]).  The producer warp moves
+// whole row tiles with 4-D TMA tensor copies in both directions; the hardware 128B
+// swizzle is exactly the per-chunk XOR swizzle phase 2 needs, so there is no
+// copy-out pass.  Consumers: phase 1 = H_256 per chunk in place (LDS/STS.128),
+// team barrier, phase 2 = H_{n/256} across chunks via ldmatrix/stmatrix.trans,
+// then signal the producer, which stores the tile and refills the stage.
+template <int N, int DT, int TILE_ROWS, int STAGES, int NT, int P, int U, int CTAS>
+__global__ void __launch_bounds__((NT + 1) * 32, CTAS)
+    fwht_rows_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ CUtensorMap tm_out,
+                     int64_t m, float s_res) {
+  constexpr int ROW_BYTES = 2 * N;
+  constexpr int TILE_BYTES = TILE_ROWS * ROW_BYTES;
+  constexpr int Q = log2_n<N>() - 8;
+  constexpr int C = N / 256;  // 256-chunks per row
+  using PL = PlanL<Q>;
+  constexpr int NLOOP = 1 << PL::nloop_bits;            // phase-2 items per row
+  static_assert(NLOOP << PL::nx == C, "phase-2 fragment count");
+  constexpr int NTEAMS = NT / P;
+  static_assert(NT % P == 0 && TILE_ROWS % NTEAMS == 0, "team layout");
+  constexpr int RPT = TILE_ROWS / NTEAMS;                // rows per team
+  constexpr int ITEMS1 = RPT * C, ITEMS2 = RPT * NLOOP;  // phase-1 and phase-2 items per team
+  constexpr int U1 = (ITEMS1 / P) >= U ? U : 1;
+  constexpr int U2 = (ITEMS2 / P) >= U ? U : 1;
+  static_assert(ITEMS1 % (P * U1) == 0 && ITEMS2 % (P * U2) == 0, "work split");
+
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * TILE_BYTES);
+  uint64_t* done = full + STAGES;  // consumers -> producer: tile computed, ready to store
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t num_tiles = (m + TILE_ROWS - 1) / TILE_ROWS;
+
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&done[s], NT);
     }
-    const uint32_t off2 = phase2_lane_offset<Q>(lane);
-    const uint32_t tile_base_sh = smem_addr(smem);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    fence_proxy_async_smem();
+  }
+  __syncthreads();
 
-    auto team_sync = [&]() {
-      if constexpr (P == 1) {
-        __syncwarp();
-      } else {
-        named_bar_sync(1 + team, P * 32);
+  if (warp == NT) {
+    // ---------------- producer: TMA tensor loads and stores of whole row tiles
+    if (lane == 0) {
+      tma_prefetch(&tm_in);
+      tma_prefetch(&tm_out);
+      const uint64_t pol = policy_evict_first();
+      for (int k = 0; k < STAGES; ++k) {
+        const int64_t tile = blockIdx.x + int64_t(k) * gridDim.x;
+        if (tile >= num_tiles) break;
+        mbar_arrive_expect_tx(&full[k], TILE_BYTES);  // full box, OOB rows zero-filled
+        tma_load_4d(smem + k * TILE_BYTES, &tm_in, 0, 0, 0, int(tile * TILE_ROWS), &full[k], pol);
       }
-    };
-
-    for (int64_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
-      const int s = it % STAGES;
-      mbar_wait(&full[s], (it / STAGES) & 1);
-      const int64_t row0 = tile * TILE_ROWS;
-      const int rows = (m - row0) < TILE_ROWS ? int(m - row0) : TILE_ROWS;
-      uint8_t* const tb = smem + s * TILE_BYTES;
-
-      // ---- phase 1: H_256 on every 256-chunk, swizzled write-back
-      for (int i0 = wt; i0 < ITEMS1; i0 += P * U1) {
-        uint32_t x[U1][4], y[U1][4], z[U1][4];
-#pragma unroll
-        for (int u = 0; u < U1; ++u) {
-          const int item = i0 + u * P, r = team + NTEAMS * (item / C), c = item % C;
-          lds128(tb + r * ROW_BYTES + c * 512 + lane * 16, x[u][0], x[u][1], x[u][2], x[u][3]);
-        }
-#pragma unroll
-        for (int u = 0; u < U1; ++u) {
-          stage_ca<DT>(A256, x[u][0], x[u][2], x[u][1], x[u][3], y[u]);
-          stage_ca<DT>(A256, y[u][0], y[u][2], y[u][1], y[u][3], z[u]);
-        }
-#pragma unroll
-        for (int u = 0; u < U1; ++u) {
-          const int item = i0 + u * P, r = team + NTEAMS * (item / C), c = item % C;
-          const uint32_t g = uint32_t(lane) ^ (uint32_t(c) & PL::swz_mask);
-          stg_sh128(tb + r * ROW_BYTES + c * 512 + g * 16, z[u]);
+      int it = 0;
+      for (int64_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+        const int s = it % STAGES;
+        mbar_wait(&done[s], (it / STAGES) & 1);
+        tma_store_4d(&tm_out, 0, 0, 0, int(tile * TILE_ROWS), smem + s * TILE_BYTES);  // OOB rows clipped
+        bulk_commit();
+        const int64_t next = tile + int64_t(STAGES) * gridDim.x;
+        if (next < num_tiles) {
+          bulk_wait_read_all();  // the store has read stage s
+          mbar_arrive_expect_tx(&full[s], TILE_BYTES);
+          tma_load_4d(smem + s * TILE_BYTES, &tm_in, 0, 0, 0, int(next * TILE_ROWS), &full[s], pol);
         }
       }
-      team_sync();  // P:126 "Sync across the threadblock"
+      bulk_wait_all();
+    }
+    return;
+  }
 
-      // ---- phase 2: H_{n/256} across chunks (residual 2^a factor)
-      for (int i0 = wt; i0 < ITEMS2; i0 += P * U2) {
-        uint32_t x[U2][1 << PL::nx][4];
-        uint32_t addr[U2][1 << PL::nx];
-#pragma unroll
-        for (int u = 0; u < U2; ++u) {
-          const int item = i0 + u * P, r = team + NTEAMS * (item / NLOOP), lp = item % NLOOP;
-          const uint32_t rb = tile_base_sh + s * TILE_BYTES + r * ROW_BYTES;
-#pragma unroll
-          for (int xi = 0; xi < (1 << PL::nx); ++xi) {
-            // loop bits are the top granule bits; extra fragments are chunk bits 5, 6
-            addr[u][xi] = rb + ((off2 ^ (uint32_t(lp) << (4 + 5 - PL::nloop_bits))) + uint32_t(xi) * (32u * 512u));
-            ldsm_x4_t(addr[u][xi], x[u][xi]);
-          }
-        }
-#pragma unroll
-        for (int u = 0; u < U2; ++u) {
-          float d[1 << PL::nx][8];
-#pragma unroll
-          for (int xi = 0; xi < (1 << PL::nx); ++xi) {
-            if constexpr (PL::two_stage) {
-              uint32_t y[4];
-              stage_ca<DT>(Pa, x[u][xi][0], x[u][xi][2], x[u][xi][1], x[u][xi][3], y);
-              stage_ca_f32<DT>(Pb, y[0], y[2], y[1], y[3], d[xi]);
-            } else {
-              stage_da_f32<DT>(x[u][xi], Bc0, Bc1, d[xi]);
-            }
-          }
-          // chunk bits 5, 6 live in per-lane fragments: fp32 butterflies (P:50-64 listing)
-#pragma unroll
-          for (int b = 0; b < PL::nx; ++b)
-#pragma unroll
-            for (int xi = 0; xi < (1 << PL::nx); ++xi)
-              if (!((xi >> b) & 1)) {
-#pragma unroll
-                for (int e = 0; e < 8; ++e) {
-                  const float p0 = d[xi][e], p1 = d[xi | (1 << b)][e];
-                  d[xi][e] = p0 + p1;
-                  d[xi | (1 << b)][e] = p0 - p1;
-                }
-              }
-#pragma unroll
-          for (int xi = 0; xi < (1 << PL::nx); ++xi) {
-            uint32_t z[4];
-            scale_pack<DT>(d[xi], s_res, z);
-            stsm_x4_t(addr[u][xi], z);
-          }
-        }
-      }
-      team_sync();
+  // ---------------- consumers
+  const int team = warp / P, wt = warp % P;
+  uint32_t A256[4];
+  make_const_a<DT>(0xFu, A256);
+  uint32_t Pa[4], Pb[4], Bc0[2], Bc1[2];
+  if constexpr (PL::two_stage) {
+    make_const_a<DT>(0xFu, Pa);  // H_16 over (r0, r1, r2, j1)
+    make_const_a<DT>(0x8u, Pb);  // H_2 over j0 (x) I_8
+  } else {
+    make_const_b<DT>(PL::mask_a, 0, Bc0);
+    make_const_b<DT>(PL::mask_a, 1, Bc1);
+  }
+  // phase-2 slot bits of this lane (ldmatrix row address provider: lane = 8*j + r)
+  const uint32_t r0 = lane & 1, r1 = (lane >> 1) & 1, r2 = (lane >> 2) & 1, j0 = (lane >> 3) & 1,
+                 j1 = (lane >> 4) & 1;
+  uint32_t c_l = 0, g_l = 0;  // chunk / granule bits supplied by the lane
+  if constexpr (Q == 1) { c_l = r0;                                g_l = j0 | (r1 << 1) | (r2 << 2) | (j1 << 3); }
+  if constexpr (Q == 2) { c_l = r0 | (r1 << 1);                    g_l = j0 | (j1 << 1) | (r2 << 2); }
+  if constexpr (Q == 3) { c_l = r0 | (r1 << 1) | (r2 << 2);        g_l = j0 | (j1 << 1); }
+  if constexpr (Q == 4) { c_l = r0 | (r1 << 1) | (r2 << 2) | (j1 << 3); g_l = j0; }
+  if constexpr (Q >= 5) { c_l = r0 | (r1 << 1) | (r2 << 2) | (j1 << 3) | (j0 << 4); g_l = 0; }
+  constexpr int LOOP_SHIFT = 5 - PL::nloop_bits;  // loop index = top granule bits
+  const uint32_t sm_base = smem_addr(smem);
 
-      // ---- phase 3: un-swizzle and store (512 B per warp instruction)
-      for (int i0 = wt; i0 < ITEMS1; i0 += P * U1) {
-        uint32_t z[U1][4];
-#pragma unroll
-        for (int u = 0; u < U1; ++u) {
-          const int item = i0 + u * P, r = team + NTEAMS * (item / C), c = item % C;
-          const uint32_t g = uint32_t(lane) ^ (uint32_t(c) & PL::swz_mask);
-          lds128(tb + r * ROW_BYTES + c * 512 + g * 16, z[u][0], z[u][1], z[u][2], z[u][3]);
-        }
-#pragma unroll
-        for (int u = 0; u < U1; ++u) {
-          const int item = i0 + u * P, r = team + NTEAMS * (item / C), c = item % C;
-          if (r < rows) stg128(out + (row0 + r) * N + c * 256 + lane * 8, z[u][0], z[u][1], z[u][2], z[u][3]);
-        }
-      }
-      fence_proxy_async_smem();
+  auto team_sync = [&]() {
+    if constexpr (P == 1) {
       __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
+    } else {
+      named_bar_sync(1 + team, P * 32);
     }
+  };
+
+  int it = 0;
+  for (int64_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+    const int s = it % STAGES;
+    mbar_wait(&full[s], (it / STAGES) & 1);
+    uint8_t* const tb = smem + s * TILE_BYTES;
+
+    // ---- phase 1: H_256 on every 256-chunk, in place
+    for (int i0 = wt; i0 < ITEMS1; i0 += P * U1) {
+      uint32_t x[U1][4], y[U1][4], z[U1][4];
+      uint8_t* p[U1];
+#pragma unroll
+      for (int u = 0; u < U1; ++u) {
+        const int item = i0 + u * P, r = team + NTEAMS * (item / C), c = item % C;
+        p[u] = tb + r * ROW_BYTES + gofs<C>(uint32_t(c), uint32_t(lane));
+        lds128(p[u], x[u][0], x[u][1], x[u][2], x[u][3]);
+      }
+#pragma unroll
+      for (int u = 0; u < U1; ++u) {
+        stage_ca<DT>(A256, x[u][0], x[u][2], x[u][1], x[u][3], y[u]);
+        stage_ca<DT>(A256, y[u][0], y[u][2], y[u][1], y[u][3], z[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < U1; ++u) stg_sh128(p[u], z[u]);
+    }
+    team_sync();  // P:126 "Sync across the threadblock"
+
+    // ---- phase 2: H_{n/256} across chunks (residual 2^a factor)
+    for (int i0 = wt; i0 < ITEMS2; i0 += P * U2) {
+      uint32_t x[U2][1 << PL::nx][4];
+      uint32_t addr[U2][1 << PL::nx];
+#pragma unroll
+      for (int u = 0; u < U2; ++u) {
+        const int item = i0 + u * P, r = team + NTEAMS * (item / NLOOP), lp = item % NLOOP;
+        const uint32_t g = g_l | (uint32_t(lp) << LOOP_SHIFT);
+#pragma unroll
+        for (int xi = 0; xi < (1 << PL::nx); ++xi) {
+          addr[u][xi] = sm_base + s * TILE_BYTES + r * ROW_BYTES + gofs<C>(c_l | (uint32_t(xi) << 5), g);
+          ldsm_x4_t(addr[u][xi], x[u][xi]);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U2; ++u) {
+        float d[1 << PL::nx][8];
+#pragma unroll
+        for (int xi = 0; xi < (1 << PL::nx); ++xi) {
+          if constexpr (PL::two_stage) {
+            uint32_t y[4];
+            stage_ca<DT>(Pa, x[u][xi][0], x[u][xi][2], x[u][xi][1], x[u][xi][3], y);
+            stage_ca_f32<DT>(Pb, y[0], y[2], y[1], y[3], d[xi]);
+          } else {
+            stage_da_f32<DT>(x[u][xi], Bc0, Bc1, d[xi]);
+          }
+        }
+        // chunk bits 5, 6 live in per-lane fragments: fp32 butterflies (P:50-64 listing)
+#pragma unroll
+        for (int b = 0; b < PL::nx; ++b)
+#pragma unroll
+          for (int xi = 0; xi < (1 << PL::nx); ++xi)
+            if (!((xi >> b) & 1)) {
+#pragma unroll
+              for (int e = 0; e < 8; ++e) {
+                const float p0 = d[xi][e], p1 = d[xi | (1 << b)][e];
+                d[xi][e] = p0 + p1;
+                d[xi | (1 << b)][e] = p0 - p1;
+              }
+            }
+#pragma unroll
+        for (int xi = 0; xi < (1 << PL::nx); ++xi) {
+          uint32_t z[4];
+          scale_pack<DT>(d[xi], s_res, z);
+          stsm_x4_t(addr[u][xi], z);
+        }
+      }
+    }
+    fence_proxy_async_smem();  // make this warp's smem writes visible to the TMA store
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&done[s]);
   }
 }
 

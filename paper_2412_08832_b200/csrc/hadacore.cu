@@ -4,10 +4,14 @@
 // "P:NN" = /root/reference/PAPER.md line NN.
 #include <cuda_runtime.h>
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <atomic>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
+#include <mutex>
 
 #include "../../include/hadacore.h"
 #include "fwht_kernel.cuh"
@@ -35,53 +39,110 @@ int sm_count(int dev) {
 // ~TILE_KB KiB (whole rows; one 64 KiB row for n = 2^15), rows split into teams of
 // P warps (n > 256) that synchronise with named barriers.  The HC_* macros let
 // tools/tune.py build variants; the defaults are the tuned values.
-#ifndef HC_NT
-#define HC_NT 8
+// Tuned per n on B200 (profiles/r01_tune_*.txt): compute warps, tile KiB, ring
+// stages, work items per warp in flight, CTAs per SM.
+template <int N> struct Tuned;
+template <> struct Tuned<128>   { static constexpr int nt = 16, tkb = 16, st = 6, u = 1, ctas = 1; };
+template <> struct Tuned<256>   { static constexpr int nt = 16, tkb = 16, st = 6, u = 1, ctas = 1; };
+template <> struct Tuned<512>   { static constexpr int nt = 8,  tkb = 16, st = 6, u = 1, ctas = 1; };
+template <> struct Tuned<1024>  { static constexpr int nt = 8,  tkb = 16, st = 6, u = 1, ctas = 1; };
+template <> struct Tuned<2048>  { static constexpr int nt = 8,  tkb = 32, st = 4, u = 1, ctas = 1; };
+template <> struct Tuned<4096>  { static constexpr int nt = 16, tkb = 16, st = 6, u = 1, ctas = 1; };
+template <> struct Tuned<8192>  { static constexpr int nt = 8,  tkb = 32, st = 4, u = 2, ctas = 1; };
+template <> struct Tuned<16384> { static constexpr int nt = 8,  tkb = 16, st = 6, u = 1, ctas = 1; };
+template <> struct Tuned<32768> { static constexpr int nt = 8,  tkb = 16, st = 4, u = 1, ctas = 2; };
+
+#ifdef HC_TUNE  // tools/tune.py: one configuration for every n, from -D macros
+template <int N>
+struct Knobs { static constexpr int nt = HC_NT, tkb = HC_TILE_KB, st = HC_STAGES, u = HC_U, ctas = HC_CTAS; };
+#else
+template <int N>
+struct Knobs : Tuned<N> {};
 #endif
-#ifndef HC_TILE_KB
-#define HC_TILE_KB 32
-#endif
-#ifndef HC_STAGES
-#define HC_STAGES 4
-#endif
-#ifndef HC_U
-#define HC_U 2
-#endif
+
 template <int N>
 struct Cfg {
-  static constexpr int nt = HC_NT;
-  static constexpr int rows = (HC_TILE_KB * 1024) / (2 * N) > 0 ? (HC_TILE_KB * 1024) / (2 * N) : 1;
+  using K = Knobs<N>;
+  static constexpr int nt = K::nt;
+  static constexpr int rows = (K::tkb * 1024) / (2 * N) > 0 ? (K::tkb * 1024) / (2 * N) : 1;
   static constexpr int tile_bytes = rows * 2 * N;
-  static constexpr int max_stages = (227 * 1024 - 256) / tile_bytes;
-  static constexpr int stages = HC_STAGES < max_stages ? HC_STAGES : max_stages;
+  // more CTAs per SM only if each can still hold a double-buffered ring
+  static constexpr int ctas = ((227 * 1024 / K::ctas - 256) / tile_bytes) >= 2 ? K::ctas : 1;
+  static constexpr int max_stages = (227 * 1024 / ctas - 256) / tile_bytes;
+  static constexpr int stages = K::st < max_stages ? K::st : max_stages;
   static constexpr int nteams = N <= 256 ? 1 : (rows < nt ? rows : nt);
   static constexpr int p = N <= 256 ? 1 : nt / nteams;
-  static constexpr int u = HC_U;
+  static constexpr int u = K::u;
   static_assert(stages >= 2, "need at least a double-buffered ring");
 };
+
+// cuTensorMapEncodeTiled from the driver, fetched through the runtime (no -lcuda).
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &p, 12000, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// 4-D view of an m x n row-major 16-bit matrix for TMA: (64 elements, chunk c of
+// 256 elements [stride 512 B], 128-byte segment s of the chunk [stride 128 B], row
+// [stride 2n B]); box (64, C, 4, rows) with SWIZZLE_128B (DESIGN.md "Shared-memory
+// layout").  Returns false if the driver rejects the descriptor.
+bool encode_rows_map(CUtensorMap* map, const void* base, int64_t m, int n, int box_rows) {
+  PFN_cuTensorMapEncodeTiled_v12000 enc = tensor_map_encoder();
+  if (!enc) return false;
+  const int C = n / 256;
+  cuuint64_t dims[4] = {64, cuuint64_t(C), 4, cuuint64_t(m)};
+  cuuint64_t strides[3] = {512, 128, cuuint64_t(2) * cuuint64_t(n)};
+  cuuint32_t box[4] = {64, cuuint32_t(C), 4, cuuint32_t(box_rows)};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT16, 4, const_cast<void*>(base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <typename Kern>
+bool ensure_smem_attr(Kern kern, int smem, std::atomic<uint64_t>& done, int dev) {
+  const uint64_t bit = (dev >= 0 && dev < 64) ? (1ull << dev) : 0;
+  if (bit && (done.load(std::memory_order_relaxed) & bit)) return true;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) return false;
+  done.fetch_or(bit, std::memory_order_relaxed);
+  return true;
+}
 
 template <int N, int DT>
 hadacore_status_t launch(const void* in, void* out, int64_t m, float scale, cudaStream_t stream) {
   using C = Cfg<N>;
   constexpr int smem = C::stages * C::tile_bytes + 2 * C::stages * 8;
-  auto kern = fwht_kernel<N, DT, C::rows, C::stages, C::nt, C::p, C::u>;
   static std::atomic<uint64_t> attr_done{0};
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return HADACORE_ERR_CUDA;
-  const uint64_t bit = (dev < 64) ? (1ull << dev) : 0;
-  if (!bit || !(attr_done.load(std::memory_order_relaxed) & bit)) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
-      return HADACORE_ERR_CUDA;
-    attr_done.fetch_or(bit, std::memory_order_relaxed);
-  }
   const int64_t tiles = (m + C::rows - 1) / C::rows;
-  const int64_t max_ctas = sm_count(dev);  // one persistent CTA per SM
+  const int64_t max_ctas = int64_t(sm_count(dev)) * C::ctas;  // persistent CTAs
   const int grid = int(tiles < max_ctas ? tiles : max_ctas);
   // the per-stage constants multiply by exact powers of two 2^-E; fold the rest of
   // `scale` into the fp32 epilogue of the last stage.
   const float s_res = std::ldexp(scale, total_shift<N>());
-  kern<<<grid, (C::nt + 1) * 32, smem, stream>>>(static_cast<const uint16_t*>(in),
-                                                  static_cast<uint16_t*>(out), m, s_res);
+  if constexpr (N <= 256) {
+    auto kern = fwht_kernel<N, DT, C::rows, C::stages, C::nt, C::p, C::u, C::ctas>;
+    if (!ensure_smem_attr(kern, smem, attr_done, dev)) return HADACORE_ERR_CUDA;
+    kern<<<grid, (C::nt + 1) * 32, smem, stream>>>(static_cast<const uint16_t*>(in), static_cast<uint16_t*>(out),
+                                                    m, s_res);
+  } else {
+    auto kern = fwht_rows_kernel<N, DT, C::rows, C::stages, C::nt, C::p, C::u, C::ctas>;
+    if (!ensure_smem_attr(kern, smem, attr_done, dev)) return HADACORE_ERR_CUDA;
+    CUtensorMap tin, tout;
+    if (!encode_rows_map(&tin, in, m, N, C::rows) || !encode_rows_map(&tout, out, m, N, C::rows))
+      return HADACORE_ERR_CUDA;
+    kern<<<grid, (C::nt + 1) * 32, smem, stream>>>(tin, tout, m, s_res);
+  }
   return cudaPeekAtLastError() == cudaSuccess ? HADACORE_OK : HADACORE_ERR_CUDA;
 }
 

@@ -482,3 +482,111 @@ def main_rowsL():
         ok, conf, cs, gs, sc, ma, ts = check_rowL(1 << k)
         print(f"n={1<<k:6d} ok={ok} ldsm_conflicts={conf} chunk={cs} gran={gs} mask_a={ma:#x} two_stage={ts} "
               f"scale=2^{np.log2(sc):.1f}")
+
+
+# ---------------------------------------------------------------------------
+# Design "T": smem row layout produced by a 4-D TMA tensor load with box
+# (64 el, C chunks, 4 segments, rows) and SWIZZLE_128B.  Element (chunk c, granule
+# g = 8*s + gg, e) of a row sits at byte
+#     ((s*C + c) * 128) + 16 * (gg ^ ((s*C + c) & 7)) + 2*e
+# (128B line index L = s*C + c; hardware XORs granule bits [4:6] with line bits).
+# ---------------------------------------------------------------------------
+def gaddrT(C, c, g):
+    s, gg = g >> 3, g & 7
+    L = s * C + c
+    return (L * 128 + 16 * (gg ^ (L & 7))) // 2   # element offset
+
+
+def check_rowT(n, seed=0):
+    k = n.bit_length() - 1
+    q = k - 8
+    C = 1 << q
+    chunk_slots, gran_slots = planL(q)
+    x = np.random.default_rng(seed).standard_normal(n)
+    # TMA load: natural row -> swizzled smem
+    sm = np.zeros(n)
+    for c in range(C):
+        for g in range(32):
+            o = gaddrT(C, c, g)
+            sm[o:o + 8] = x[c * 256 + 8 * g: c * 256 + 8 * g + 8]
+    A256 = kron_const("HHHH", 0.25)
+    conf1 = 0
+    for c in range(C):
+        vals = np.zeros((32, 4, 2))
+        for phase in range(4):  # LDS.128 processes 8 lanes (128 B) per wavefront
+            groups = {(gaddrT(C, c, l) * 2 // 16) % 8 for l in range(8 * phase, 8 * phase + 8)}
+            conf1 += 8 - len(groups)
+        for l in range(32):
+            o = gaddrT(C, c, l)
+            vals[l] = sm[o:o + 8].reshape(4, 2)
+        v = stage_const_a(stage_const_a(vals, A256, (0, 2, 1, 3)), A256, (0, 2, 1, 3))
+        for l in range(32):
+            o = gaddrT(C, c, l)
+            sm[o:o + 8] = v[l].reshape(8)
+    nx = max(0, q - 5)
+    loop_bits = [s for s in gran_slots if s.startswith("f")]
+    in_chunk = [s for s in chunk_slots if not s.startswith("x")]
+    mask_a = 0
+    for s in in_chunk:
+        if s in ("r0", "r1", "r2", "j1"):
+            mask_a |= 1 << ["r0", "r1", "r2", "j1"].index(s)
+    two_stage = "j0" in in_chunk
+    conf2 = 0
+    for it in range(1 << len(loop_bits)):
+        frags, addrs_all = [], []
+        for xi in range(1 << nx):
+            slotv = {s: (it >> b) & 1 for b, s in enumerate(loop_bits)}
+            for b in range(nx):
+                slotv[f"x{b}"] = (xi >> b) & 1
+            addrs = {}
+            for L_ in range(32):
+                j, r = L_ // 8, L_ % 8
+                sv = dict(slotv, r0=r & 1, r1=(r >> 1) & 1, r2=(r >> 2) & 1, j0=j & 1, j1=(j >> 1) & 1)
+                c = sum(sv[s] << i for i, s in enumerate(chunk_slots))
+                g = sum(sv[s] << i for i, s in enumerate(gran_slots))
+                addrs[(j, r)] = gaddrT(C, c, g)
+            for j in range(4):
+                conf2 += 8 - len({(addrs[(j, r)] * 2 // 16) % 8 for r in range(8)})
+            vals = np.zeros((32, 4, 2))
+            for lane in range(32):
+                gq, t = lane >> 2, lane & 3
+                for j in range(4):
+                    for h in range(2):
+                        vals[lane, j, h] = sm[addrs[(j, 2 * t + h)] + gq]
+            frags.append(vals)
+            addrs_all.append(addrs)
+        outs = []
+        for vals in frags:
+            if two_stage:
+                v = stage_const_a(vals, kron_const("HHHH", 0.25), (0, 2, 1, 3))
+                v = stage_const_a(v, kron_const("IIIH", 1.0), (0, 2, 1, 3))
+            else:
+                kinds = "".join("H" if (mask_a >> b) & 1 else "I" for b in range(4))
+                v = stage_data_a(vals, kron_const(kinds, 2.0 ** -(kinds.count("H") // 2)))
+            outs.append(v)
+        for b in range(nx):
+            for xi in range(1 << nx):
+                if not (xi >> b) & 1:
+                    a_, b_ = outs[xi], outs[xi | (1 << b)]
+                    outs[xi], outs[xi | (1 << b)] = a_ + b_, a_ - b_
+        for vals, addrs in zip(outs, addrs_all):
+            for lane in range(32):
+                gq, t = lane >> 2, lane & 3
+                for j in range(4):
+                    for h in range(2):
+                        sm[addrs[(j, 2 * t + h)] + gq] = vals[lane, j, h]
+    # TMA store: swizzled smem -> natural
+    y = np.zeros(n)
+    for c in range(C):
+        for g in range(32):
+            o = gaddrT(C, c, g)
+            y[c * 256 + 8 * g: c * 256 + 8 * g + 8] = sm[o:o + 8]
+    ref = fwht_np(x[None, :])[0]
+    sc = np.median(y / np.where(ref == 0, 1, ref))
+    return np.allclose(y, ref * sc), conf1, conf2, sc
+
+
+def main_rowsT():
+    for k in range(9, 16):
+        ok, c1, c2, sc = check_rowT(1 << k)
+        print(f"n={1<<k:6d} ok={ok} phase1_conflicts={c1} ldsm_conflicts={c2} scale=2^{np.log2(sc):.1f}")

@@ -19,12 +19,19 @@ NS = [1 << k for k in range(7, 16)]
 
 
 def build_one(spec):
-    nt, tkb, st, u = spec.split(",")
-    name = f"nt{nt}_t{tkb}_s{st}_u{u}"
+    """spec: "nt,tile_kb,stages,u[,ctas]" or "tuned" / "tuned-nocompute" (per-n table)."""
+    base = ["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
+            "-Xcompiler", "-fPIC", "-shared"]
+    if spec.startswith("tuned"):
+        name = spec.replace("-", "_")
+        extra = ["-DHC_NOCOMPUTE"] if "nocompute" in spec else []
+    else:
+        nt, tkb, st, u, ctas = (spec.split(",") + ["1"])[:5]
+        name = f"nt{nt}_t{tkb}_s{st}_u{u}_c{ctas}"
+        extra = ["-DHC_TUNE", f"-DHC_CTAS={ctas}", f"-DHC_NT={nt}", f"-DHC_TILE_KB={tkb}", f"-DHC_STAGES={st}",
+                 f"-DHC_U={u}"]
     so = os.path.join(OUT, f"libhc_{name}.so")
-    cmd = ["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-           "-Xcompiler", "-fPIC", "-shared", f"-DHC_NT={nt}", f"-DHC_TILE_KB={tkb}", f"-DHC_STAGES={st}",
-           f"-DHC_U={u}", "-o", so, os.path.join(ROOT, "paper_2412_08832_b200", "csrc", "hadacore.cu")]
+    cmd = base + extra + ["-o", so, os.path.join(ROOT, "paper_2412_08832_b200", "csrc", "hadacore.cu")]
     r = subprocess.run(cmd, capture_output=True, text=True)
     return name, r.returncode, r.stderr[-2000:]
 
@@ -36,13 +43,24 @@ def build(specs):
             print(name, "ok" if rc == 0 else f"FAILED\n{err}")
 
 
-def run(reps=7, ns=None):
+def run(reps=15, ns=None):
     import torch
     libs = sorted(glob.glob(os.path.join(OUT, "libhc_*.so")))
     elems = 1 << 28
     src = torch.randn(elems, device="cuda").to(torch.float16)
     dst = torch.empty_like(src)
     results = {}
+    # ceiling: back-to-back D2D memcpy of the same bytes (read + write)
+    ts = []
+    for _ in range(3):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(reps):
+            dst.copy_(src)
+        b.record()
+        b.synchronize()
+        ts.append(a.elapsed_time(b) / reps)
+    print(f"memcpy(copy_) back-to-back: {4.0 * elems / (sorted(ts)[1] * 1e-3) / 1e9:.0f} GB/s", flush=True)
     for path in libs:
         name = os.path.basename(path)[6:-3]
         lib = ctypes.CDLL(path)
@@ -57,13 +75,14 @@ def run(reps=7, ns=None):
                 for _ in range(2):
                     assert f(src.data_ptr(), dst.data_ptr(), m, n, dt, 1.0, st) == 0
                 ts = []
-                for _ in range(reps):
+                for _ in range(3):  # batches of back-to-back launches: no host gaps inside
                     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                     a.record()
-                    f(src.data_ptr(), dst.data_ptr(), m, n, dt, 1.0, st)
+                    for _ in range(reps):
+                        f(src.data_ptr(), dst.data_ptr(), m, n, dt, 1.0, st)
                     b.record()
                     b.synchronize()
-                    ts.append(a.elapsed_time(b))
+                    ts.append(a.elapsed_time(b) / reps)
                 ts.sort()
                 res[f"{'f16' if dt == 0 else 'bf16'}_{n}"] = round(4.0 * elems / (ts[len(ts) // 2] * 1e-3) / 1e9, 0)
         results[name] = res
