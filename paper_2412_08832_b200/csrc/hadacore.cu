@@ -42,15 +42,15 @@ int sm_count(int dev) {
 // Tuned per n on B200 (profiles/r01_tune_*.txt): compute warps, tile KiB, ring
 // stages, work items per warp in flight, CTAs per SM.
 template <int N> struct Tuned;
-template <> struct Tuned<128>   { static constexpr int nt = 16, tkb = 16, st = 6, u = 1, ctas = 1; };
-template <> struct Tuned<256>   { static constexpr int nt = 16, tkb = 16, st = 6, u = 1, ctas = 1; };
-template <> struct Tuned<512>   { static constexpr int nt = 8,  tkb = 16, st = 6, u = 1, ctas = 1; };
-template <> struct Tuned<1024>  { static constexpr int nt = 8,  tkb = 16, st = 6, u = 1, ctas = 1; };
-template <> struct Tuned<2048>  { static constexpr int nt = 8,  tkb = 32, st = 4, u = 1, ctas = 1; };
-template <> struct Tuned<4096>  { static constexpr int nt = 16, tkb = 16, st = 6, u = 1, ctas = 1; };
-template <> struct Tuned<8192>  { static constexpr int nt = 8,  tkb = 32, st = 4, u = 2, ctas = 1; };
-template <> struct Tuned<16384> { static constexpr int nt = 8,  tkb = 16, st = 6, u = 1, ctas = 1; };
-template <> struct Tuned<32768> { static constexpr int nt = 8,  tkb = 16, st = 4, u = 1, ctas = 2; };
+template <> struct Tuned<128>   { static constexpr int nt = 16, tkb = 16, st = 4, u = 1, ctas = 1; };
+template <> struct Tuned<256>   { static constexpr int nt = 16, tkb = 16, st = 4, u = 1, ctas = 1; };
+template <> struct Tuned<512>   { static constexpr int nt = 16, tkb = 16, st = 4, u = 1, ctas = 1; };
+template <> struct Tuned<1024>  { static constexpr int nt = 16, tkb = 16, st = 4, u = 1, ctas = 1; };
+template <> struct Tuned<2048>  { static constexpr int nt = 16, tkb = 16, st = 4, u = 1, ctas = 1; };
+template <> struct Tuned<4096>  { static constexpr int nt = 16, tkb = 16, st = 4, u = 1, ctas = 1; };
+template <> struct Tuned<8192>  { static constexpr int nt = 16, tkb = 32, st = 4, u = 1, ctas = 1; };
+template <> struct Tuned<16384> { static constexpr int nt = 8,  tkb = 16, st = 8, u = 1, ctas = 1; };
+template <> struct Tuned<32768> { static constexpr int nt = 8,  tkb = 64, st = 3, u = 1, ctas = 1; };
 
 #ifdef HC_TUNE  // tools/tune.py: one configuration for every n, from -D macros
 template <int N>

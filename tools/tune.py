@@ -43,55 +43,56 @@ def build(specs):
             print(name, "ok" if rc == 0 else f"FAILED\n{err}")
 
 
-def run(reps=15, ns=None):
+def run(reps=15, ns=None, repeats=3):
+    """Times every built variant; the whole sweep is repeated `repeats` times
+    (variants interleaved) and the median per (variant, dtype, n) is reported."""
+    import statistics
+
     import torch
     libs = sorted(glob.glob(os.path.join(OUT, "libhc_*.so")))
     elems = 1 << 28
     src = torch.randn(elems, device="cuda").to(torch.float16)
     dst = torch.empty_like(src)
-    results = {}
-    # ceiling: back-to-back D2D memcpy of the same bytes (read + write)
-    ts = []
-    for _ in range(3):
+    st = torch.cuda.current_stream().cuda_stream
+
+    def batch_ms(fn):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
         for _ in range(reps):
-            dst.copy_(src)
+            fn()
         b.record()
         b.synchronize()
-        ts.append(a.elapsed_time(b) / reps)
-    print(f"memcpy(copy_) back-to-back: {4.0 * elems / (sorted(ts)[1] * 1e-3) / 1e9:.0f} GB/s", flush=True)
+        return a.elapsed_time(b) / reps
+
+    fns = {}
     for path in libs:
-        name = os.path.basename(path)[6:-3]
         lib = ctypes.CDLL(path)
         f = lib.hadacore_fwht
         f.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int,
                       ctypes.c_float, ctypes.c_void_p]
-        res = {}
-        st = torch.cuda.current_stream().cuda_stream
-        for dt in (0, 1):
-            for n in (ns or NS):
-                m = elems // n
-                for _ in range(2):
-                    assert f(src.data_ptr(), dst.data_ptr(), m, n, dt, 1.0, st) == 0
-                ts = []
-                for _ in range(3):  # batches of back-to-back launches: no host gaps inside
-                    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                    a.record()
-                    for _ in range(reps):
-                        f(src.data_ptr(), dst.data_ptr(), m, n, dt, 1.0, st)
-                    b.record()
-                    b.synchronize()
-                    ts.append(a.elapsed_time(b) / reps)
-                ts.sort()
-                res[f"{'f16' if dt == 0 else 'bf16'}_{n}"] = round(4.0 * elems / (ts[len(ts) // 2] * 1e-3) / 1e9, 0)
-        results[name] = res
-        print(name, " ".join(f"{k}={v:.0f}" for k, v in res.items()), flush=True)
-    # best per (dtype, n)
+        fns[os.path.basename(path)[6:-3]] = f
+    samples = {}
+    mem = []
+    for rep in range(repeats):
+        mem.append(4.0 * elems / (batch_ms(lambda: dst.copy_(src)) * 1e-3) / 1e9)
+        for name, f in fns.items():
+            for dt in (0, 1):
+                for n in (ns or NS):
+                    m = elems // n
+                    call = lambda: f(src.data_ptr(), dst.data_ptr(), m, n, dt, 1.0, st)
+                    call()
+                    gbs = 4.0 * elems / (batch_ms(call) * 1e-3) / 1e9
+                    samples.setdefault(name, {}).setdefault(f"{'f16' if dt == 0 else 'bf16'}_{n}", []).append(gbs)
+    print(f"memcpy(copy_) back-to-back: median {statistics.median(mem):.0f} GB/s  samples {[round(v) for v in mem]}")
+    results = {nm: {k: round(statistics.median(v)) for k, v in d.items()} for nm, d in samples.items()}
+    spread = {nm: {k: round(max(v) - min(v)) for k, v in d.items()} for nm, d in samples.items()}
+    for nm, res in results.items():
+        print(nm, " ".join(f"{k}={v}" for k, v in res.items()), flush=True)
     keys = list(next(iter(results.values())).keys())
     best = {k: max(results, key=lambda nm: results[nm][k]) for k in keys}
-    print("BEST", json.dumps({k: (best[k], results[best[k]][k]) for k in keys}))
-    json.dump(results, open(os.path.join(ROOT, "gpurun_out", "tune.json"), "w"), indent=1)
+    print("BEST", json.dumps({k: (best[k], results[best[k]][k], spread[best[k]][k]) for k in keys}))
+    json.dump({"median": results, "spread": spread, "memcpy": mem}, open(os.path.join(ROOT, "gpurun_out", "tune.json"), "w"),
+              indent=1)
 
 
 if __name__ == "__main__":
