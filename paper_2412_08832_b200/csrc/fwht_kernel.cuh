@@ -27,6 +27,7 @@
 // The lane/register slot algebra is modelled and checked in tools/fragment_model.py.
 #pragma once
 #include <cuda.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -256,6 +257,59 @@ __device__ __forceinline__ void scale_pack(const float d[8], float s_res, uint32
   for (int i = 0; i < 4; ++i) y[i] = pack2<DT>(d[2 * i] * s_res, d[2 * i + 1] * s_res);
 }
 
+// ------------------------------------------------------------------ SIMT ablation
+// HC_SIMT builds replace every tensor-core stage by fp32 warp-shuffle butterflies
+// on the same fragment (tools/tune.py "tuned-simt"), to measure whether the mma
+// contractions beat shuffle butterflies (north_star).  Fragment value index
+// i = 2*j + h (register X_j, half h); fragment bits: b0 = h, b1/b2 = lane bits 0/1,
+// b3 = j bit 1, b4..b6 = lane bits 2..4, b7 = j bit 0.
+template <int DT>
+__device__ __forceinline__ void unpack8(const uint32_t x[4], float v[8]) {
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    if constexpr (DT == DT_F16) {
+      const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&x[j]));
+      v[2 * j] = f.x;
+      v[2 * j + 1] = f.y;
+    } else {
+      v[2 * j] = __uint_as_float(x[j] << 16);
+      v[2 * j + 1] = __uint_as_float(x[j] & 0xffff0000u);
+    }
+  }
+}
+__device__ __forceinline__ void simt_butterflies(float v[8], uint32_t mask8) {
+  const int lane = threadIdx.x & 31;
+  constexpr int reg_bit[8] = {0, -1, -1, 2, -1, -1, -1, 1};   // b -> bit of the value index
+  constexpr int lane_bit[8] = {-1, 0, 1, -1, 2, 3, 4, -1};    // b -> lane bit
+#pragma unroll
+  for (int b = 0; b < 8; ++b) {
+    if (!((mask8 >> b) & 1u)) continue;
+    if (reg_bit[b] >= 0) {
+      const int st = 1 << reg_bit[b];
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        if (!(i & st)) {
+          const float p0 = v[i], p1 = v[i | st];
+          v[i] = p0 + p1;
+          v[i | st] = p0 - p1;
+        }
+    } else {
+      const int lb = 1 << lane_bit[b];
+      const float sg = (lane & lb) ? -1.f : 1.f;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v[i] = fmaf(v[i], sg, __shfl_xor_sync(0xffffffffu, v[i], lb));
+    }
+  }
+}
+template <int DT>
+__device__ __forceinline__ void simt_fwht_pack(const uint32_t x[4], uint32_t mask8, float mul, uint32_t z[4]) {
+  float v[8];
+  unpack8<DT>(x, v);
+  simt_butterflies(v, mask8);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) z[j] = pack2<DT>(v[2 * j] * mul, v[2 * j + 1] * mul);
+}
+
 __device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t r[4]) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
@@ -374,9 +428,16 @@ __global__ void __launch_bounds__((NT + 1) * 32, CTAS)
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
+#ifdef HC_SIMT
+          simt_fwht_pack<DT>(x[u], 0x7Fu, ldexpf(s_res, -total_shift<N>()), z[u]);  // all bits but the row bit b7
+          const uint32_t t1 = z[u][1];  // natural slots: row A in (z0, z2), row B in (z1, z3)
+          z[u][1] = z[u][2];
+          z[u][2] = t1;
+#else
           stage_ca<DT>(A1, x[u][0], x[u][2], x[u][1], x[u][3], y[u]);
           stage_ca_f32<DT>(A2, y[u][0], y[u][1], y[u][2], y[u][3], d[u]);
           scale_pack<DT>(d[u], s_res, z[u]);
+#endif
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
@@ -407,9 +468,13 @@ __global__ void __launch_bounds__((NT + 1) * 32, CTAS)
         for (int u = 0; u < U; ++u) lds128(tb + (r0 + u * NT) * ROW_BYTES + lane * 16, x[u][0], x[u][1], x[u][2], x[u][3]);
 #pragma unroll
         for (int u = 0; u < U; ++u) {
+#ifdef HC_SIMT
+          simt_fwht_pack<DT>(x[u], 0xFFu, ldexpf(s_res, -total_shift<N>()), z[u]);
+#else
           stage_ca<DT>(A1, x[u][0], x[u][2], x[u][1], x[u][3], y[u]);
           stage_ca_f32<DT>(A1, y[u][0], y[u][2], y[u][1], y[u][3], d[u]);
           scale_pack<DT>(d[u], s_res, z[u]);
+#endif
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
@@ -583,8 +648,12 @@ __global__ void __launch_bounds__((NT + 1) * 32, CTAS)
       }
 #pragma unroll
       for (int u = 0; u < U1; ++u) {
+#ifdef HC_SIMT
+        simt_fwht_pack<DT>(x[u], 0xFFu, 0.0625f, z[u]);
+#else
         stage_ca<DT>(A256, x[u][0], x[u][2], x[u][1], x[u][3], y[u]);
         stage_ca<DT>(A256, y[u][0], y[u][2], y[u][1], y[u][3], z[u]);
+#endif
       }
 #pragma unroll
       for (int u = 0; u < U1; ++u) stg_sh128(p[u], z[u]);
@@ -610,6 +679,12 @@ __global__ void __launch_bounds__((NT + 1) * 32, CTAS)
         float d[1 << PL::nx][8];
 #pragma unroll
         for (int xi = 0; xi < (1 << PL::nx); ++xi) {
+#ifdef HC_SIMT
+          unpack8<DT>(x[u][xi], d[xi]);
+          simt_butterflies(d[xi], PL::mask_a | (PL::two_stage ? 0x80u : 0u));
+#pragma unroll
+          for (int e = 0; e < 8; ++e) d[xi][e] *= ldexpf(1.f, -stage_shift(PL::mask_a));
+#else
           if constexpr (PL::two_stage) {
             uint32_t y[4];
             stage_ca<DT>(Pa, x[u][xi][0], x[u][xi][2], x[u][xi][1], x[u][xi][3], y);
@@ -617,6 +692,7 @@ __global__ void __launch_bounds__((NT + 1) * 32, CTAS)
           } else {
             stage_da_f32<DT>(x[u][xi], Bc0, Bc1, d[xi]);
           }
+#endif
         }
         // chunk bits 5, 6 live in per-lane fragments: fp32 butterflies (P:50-64 listing)
 #pragma unroll

@@ -24,7 +24,7 @@ def build_one(spec):
             "-Xcompiler", "-fPIC", "-shared"]
     if spec.startswith("tuned"):
         name = spec.replace("-", "_")
-        extra = ["-DHC_NOCOMPUTE"] if "nocompute" in spec else []
+        extra = (["-DHC_NOCOMPUTE"] if "nocompute" in spec else []) + (["-DHC_SIMT"] if "simt" in spec else [])
     else:
         nt, tkb, st, u, ctas = (spec.split(",") + ["1"])[:5]
         name = f"nt{nt}_t{tkb}_s{st}_u{u}_c{ctas}"
@@ -84,6 +84,24 @@ def run(reps=15, ns=None, repeats=3):
                     gbs = 4.0 * elems / (batch_ms(call) * 1e-3) / 1e9
                     samples.setdefault(name, {}).setdefault(f"{'f16' if dt == 0 else 'bf16'}_{n}", []).append(gbs)
     print(f"memcpy(copy_) back-to-back: median {statistics.median(mem):.0f} GB/s  samples {[round(v) for v in mem]}")
+    # each variant must agree with the parity-tested default library (nocompute excluded)
+    sys.path.insert(0, ROOT)
+    import paper_2412_08832_b200 as hc
+    small = torch.randn(1 << 20, device="cuda")
+    for name, f in fns.items():
+        if "nocompute" in name:
+            continue
+        worst = 0.0
+        for dt, tdt in ((0, torch.float16), (1, torch.bfloat16)):
+            x = small.to(tdt)
+            for n in (ns or NS):
+                xv = x.view(-1, n)
+                ref = hc.hadacore_fwht(xv).float()
+                o = torch.empty_like(xv)
+                assert f(xv.data_ptr(), o.data_ptr(), xv.shape[0], n, dt, 1.0 / n ** 0.5, st) == 0
+                err = ((o.float() - ref).norm(dim=1) / ref.norm(dim=1)).max().item()
+                worst = max(worst, err)
+        print(f"agreement {name}: max rel-L2 vs default library {worst:.2e}")
     results = {nm: {k: round(statistics.median(v)) for k, v in d.items()} for nm, d in samples.items()}
     spread = {nm: {k: round(max(v) - min(v)) for k, v in d.items()} for nm, d in samples.items()}
     for nm, res in results.items():
