@@ -140,9 +140,14 @@ def dist_setup(args):
     if world > 1:
         import torch.distributed as dist
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        return rank, world, local, dist
+        ndev = torch.cuda.device_count()
+        dev = local % ndev
+        torch.cuda.set_device(dev)
+        if ndev >= world:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:  # more ranks than GPUs (code-path check only): NCCL forbids sharing a GPU
+            dist.init_process_group("gloo")
+        return rank, world, dev, dist
     torch.cuda.set_device(0)
     return 0, 1, 0, None
 
@@ -157,7 +162,8 @@ def barrier(dist, torch):
 def max_over_ranks(v: float, dist, torch):
     if dist is None:
         return v
-    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([v], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 

@@ -28,6 +28,7 @@
 #pragma once
 #include <cuda.h>
 #include <cuda_fp16.h>
+#include <type_traits>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -514,6 +515,10 @@ __device__ __forceinline__ void tma_store_4d(const void* tmap, int c0, int c1, i
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read_all() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+template <int PENDING>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(PENDING) : "memory");
+}
 
 // Byte offset, inside a row's shared-memory image, of granule g (8 elements) of
 // 256-chunk c.  The 4-D TMA box (64 el, C chunks, 4 segments, rows) with
@@ -523,6 +528,38 @@ template <int C>
 __device__ __forceinline__ uint32_t gofs(uint32_t c, uint32_t g) {
   const uint32_t L = (g >> 3) * C + c;
   return L * 128u + 16u * ((g & 7u) ^ (L & 7u));
+}
+
+// Build switches (tools/tune.py diagnostics): HC_STG_OUT = copy-out with LDS.128 +
+// STG.128 by the consumers instead of TMA tensor stores; HC_SEG = per-segment boxes.
+#ifdef HC_STG_OUT
+constexpr bool kStgOut = true;
+#else
+constexpr bool kStgOut = false;
+#endif
+// SEG mode of fwht_rows_kernel (n >= 8192, tiles of <= 4 rows): every (row, 128-byte-
+// line segment) of a tile is its own TMA box, stored as soon as its 8 phase-2 items
+// are final and refilled as soon as that store has read it.  Shared with the host so
+// the tensor-map box always matches what the kernel expects.
+__host__ __device__ constexpr bool seg_mode(int n, int tile_rows) {
+#ifdef HC_SEG  // opt-in: measured slower than whole-tile boxes (profiles/r01_tune_sweep11_paired.txt)
+  return !kStgOut && tile_rows <= 4 && n >= 8192;
+#else
+  return false;
+#endif
+}
+
+// Loads boxes K..NB-1 of a SEG tile (box k = row k/4, segment k%4); with WAIT, box k
+// first waits until the store that read the same bytes (issued k-th of NB) is done.
+template <int K, int NB, int ROW_BYTES, bool WAIT>
+__device__ __forceinline__ void seg_loads(uint8_t* stage, const void* tmap, int row0, uint64_t* bar,
+                                          uint64_t pol) {
+  if constexpr (K < NB) {
+    if constexpr (WAIT) bulk_wait_read<NB - 1 - K>();
+    tma_load_4d(stage + (K / 4) * ROW_BYTES + (K % 4) * (ROW_BYTES / 4), tmap, 0, 0, K % 4, row0 + K / 4, bar,
+                pol);
+    seg_loads<K + 1, NB, ROW_BYTES, WAIT>(stage, tmap, row0, bar, pol);
+  }
 }
 
 // ------------------------------------------------------------------ rows > 256
@@ -535,7 +572,7 @@ __device__ __forceinline__ uint32_t gofs(uint32_t c, uint32_t g) {
 template <int N, int DT, int TILE_ROWS, int STAGES, int NT, int P, int U, int CTAS>
 __global__ void __launch_bounds__((NT + 1) * 32, CTAS)
     fwht_rows_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ CUtensorMap tm_out,
-                     int64_t m, float s_res) {
+                     uint16_t* __restrict__ out, int64_t m, float s_res) {
   constexpr int ROW_BYTES = 2 * N;
   constexpr int TILE_BYTES = TILE_ROWS * ROW_BYTES;
   constexpr int Q = log2_n<N>() - 8;
@@ -551,9 +588,16 @@ __global__ void __launch_bounds__((NT + 1) * 32, CTAS)
   constexpr int U2 = (ITEMS2 / P) >= U ? U : 1;
   static_assert(ITEMS1 % (P * U1) == 0 && ITEMS2 % (P * U2) == 0, "work split");
 
+  // SEG: phase-2 items are the rows' 32 granule columns; each (row, segment) box is
+  // stored (and refilled) as soon as its 8 items are done (seg_mode above).
+  constexpr bool STG_OUT = kStgOut;
+  constexpr bool SEG = seg_mode(N, TILE_ROWS);
+  constexpr int NSEG = SEG ? 4 * TILE_ROWS : 1;  // boxes (and done barriers) per tile
+  constexpr int SEG_BYTES = ROW_BYTES / 4;
+
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * TILE_BYTES);
-  uint64_t* done = full + STAGES;  // consumers -> producer: tile computed, ready to store
+  uint64_t* done = full + STAGES;  // [STAGES][NSEG] consumers -> producer: ready to store
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t num_tiles = (m + TILE_ROWS - 1) / TILE_ROWS;
 
@@ -561,7 +605,8 @@ __global__ void __launch_bounds__((NT + 1) * 32, CTAS)
 #pragma unroll
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&done[s], NT);
+#pragma unroll
+      for (int g = 0; g < NSEG; ++g) mbar_init(&done[s * NSEG + g], SEG ? NLOOP / 4 : NT);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     fence_proxy_async_smem();
@@ -574,23 +619,51 @@ __global__ void __launch_bounds__((NT + 1) * 32, CTAS)
       tma_prefetch(&tm_in);
       tma_prefetch(&tm_out);
       const uint64_t pol = policy_evict_first();
+      auto load_tile = [&](int st, int64_t tile, auto wait_store_read) {
+        mbar_arrive_expect_tx(&full[st], TILE_BYTES);  // full box, OOB rows zero-filled
+        if constexpr (SEG) {
+          if constexpr (decltype(wait_store_read(0))::value) {
+            seg_loads<0, NSEG, ROW_BYTES, true>(smem + st * TILE_BYTES, &tm_in, int(tile * TILE_ROWS), &full[st], pol);
+          } else {
+            seg_loads<0, NSEG, ROW_BYTES, false>(smem + st * TILE_BYTES, &tm_in, int(tile * TILE_ROWS), &full[st], pol);
+          }
+        } else {
+          if constexpr (decltype(wait_store_read(0))::value) bulk_wait_read<0>();
+          tma_load_4d(smem + st * TILE_BYTES, &tm_in, 0, 0, 0, int(tile * TILE_ROWS), &full[st], pol);
+        }
+      };
+      // the tag says whether a refill must first wait for the previous occupant's
+      // stores to have read the stage
+      auto no_wait = [](int) { return std::false_type{}; };
+      auto wait_reads = [](int) { return std::true_type{}; };
       for (int k = 0; k < STAGES; ++k) {
         const int64_t tile = blockIdx.x + int64_t(k) * gridDim.x;
         if (tile >= num_tiles) break;
-        mbar_arrive_expect_tx(&full[k], TILE_BYTES);  // full box, OOB rows zero-filled
-        tma_load_4d(smem + k * TILE_BYTES, &tm_in, 0, 0, 0, int(tile * TILE_ROWS), &full[k], pol);
+        load_tile(k, tile, no_wait);
       }
       int it = 0;
       for (int64_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
         const int s = it % STAGES;
-        mbar_wait(&done[s], (it / STAGES) & 1);
-        tma_store_4d(&tm_out, 0, 0, 0, int(tile * TILE_ROWS), smem + s * TILE_BYTES);  // OOB rows clipped
-        bulk_commit();
+        const uint32_t ph = (it / STAGES) & 1;
+#pragma unroll
+        for (int g = 0; g < NSEG; ++g) {
+          mbar_wait(&done[s * NSEG + g], ph);
+          if constexpr (STG_OUT) continue;
+          if constexpr (SEG) {
+            tma_store_4d(&tm_out, 0, 0, g % 4, int(tile * TILE_ROWS) + g / 4,
+                         smem + s * TILE_BYTES + (g / 4) * ROW_BYTES + (g % 4) * SEG_BYTES);
+          } else {
+            tma_store_4d(&tm_out, 0, 0, 0, int(tile * TILE_ROWS), smem + s * TILE_BYTES);  // OOB rows clipped
+          }
+          bulk_commit();
+        }
         const int64_t next = tile + int64_t(STAGES) * gridDim.x;
         if (next < num_tiles) {
-          bulk_wait_read_all();  // the store has read stage s
-          mbar_arrive_expect_tx(&full[s], TILE_BYTES);
-          tma_load_4d(smem + s * TILE_BYTES, &tm_in, 0, 0, 0, int(next * TILE_ROWS), &full[s], pol);
+          if constexpr (STG_OUT) {
+            load_tile(s, next, no_wait);
+          } else {
+            load_tile(s, next, wait_reads);
+          }
         }
       }
       bulk_wait_all();
@@ -713,11 +786,36 @@ __global__ void __launch_bounds__((NT + 1) * 32, CTAS)
           scale_pack<DT>(d[xi], s_res, z);
           stsm_x4_t(addr[u][xi], z);
         }
+        if constexpr (SEG) {  // this item's granule column is final: count it for its (row, segment)
+          const int item = i0 + u * P, r = team + NTEAMS * (item / NLOOP), lp = item % NLOOP;
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&done[s * NSEG + 4 * r + (lp >> 3)]);
+        }
       }
     }
-    fence_proxy_async_smem();  // make this warp's smem writes visible to the TMA store
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&done[s]);
+    if constexpr (STG_OUT) {
+      team_sync();
+      const int64_t row0 = tile * TILE_ROWS;
+      for (int i0 = wt; i0 < ITEMS1; i0 += P * U1) {
+        uint32_t z[U1][4];
+#pragma unroll
+        for (int u = 0; u < U1; ++u) {
+          const int item = i0 + u * P, r = team + NTEAMS * (item / C), c = item % C;
+          lds128(tb + r * ROW_BYTES + gofs<C>(uint32_t(c), uint32_t(lane)), z[u][0], z[u][1], z[u][2], z[u][3]);
+        }
+#pragma unroll
+        for (int u = 0; u < U1; ++u) {
+          const int item = i0 + u * P, r = team + NTEAMS * (item / C), c = item % C;
+          if (row0 + r < m) stg128(out + (row0 + r) * N + c * 256 + lane * 8, z[u][0], z[u][1], z[u][2], z[u][3]);
+        }
+      }
+    }
+    if constexpr (!SEG) {
+      fence_proxy_async_smem();  // make this warp's smem writes visible to the TMA store
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&done[s]);
+    }
   }
 }
 

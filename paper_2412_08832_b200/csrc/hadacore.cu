@@ -68,7 +68,7 @@ struct Cfg {
   static constexpr int tile_bytes = rows * 2 * N;
   // more CTAs per SM only if each can still hold a double-buffered ring
   static constexpr int ctas = ((227 * 1024 / K::ctas - 256) / tile_bytes) >= 2 ? K::ctas : 1;
-  static constexpr int max_stages = (227 * 1024 / ctas - 256) / tile_bytes;
+  static constexpr int max_stages = (227 * 1024 / ctas - 1280) / tile_bytes;
   static constexpr int stages = K::st < max_stages ? K::st : max_stages;
   static constexpr int nteams = N <= 256 ? 1 : (rows < nt ? rows : nt);
   static constexpr int p = N <= 256 ? 1 : nt / nteams;
@@ -95,13 +95,13 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
 // 256 elements [stride 512 B], 128-byte segment s of the chunk [stride 128 B], row
 // [stride 2n B]); box (64, C, 4, rows) with SWIZZLE_128B (DESIGN.md "Shared-memory
 // layout").  Returns false if the driver rejects the descriptor.
-bool encode_rows_map(CUtensorMap* map, const void* base, int64_t m, int n, int box_rows) {
+bool encode_rows_map(CUtensorMap* map, const void* base, int64_t m, int n, int box_rows, int box_segs) {
   PFN_cuTensorMapEncodeTiled_v12000 enc = tensor_map_encoder();
   if (!enc) return false;
   const int C = n / 256;
   cuuint64_t dims[4] = {64, cuuint64_t(C), 4, cuuint64_t(m)};
   cuuint64_t strides[3] = {512, 128, cuuint64_t(2) * cuuint64_t(n)};
-  cuuint32_t box[4] = {64, cuuint32_t(C), 4, cuuint32_t(box_rows)};
+  cuuint32_t box[4] = {64, cuuint32_t(C), cuuint32_t(box_segs), cuuint32_t(box_rows)};
   cuuint32_t estr[4] = {1, 1, 1, 1};
   return enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT16, 4, const_cast<void*>(base), dims, strides, box, estr,
              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -120,7 +120,9 @@ bool ensure_smem_attr(Kern kern, int smem, std::atomic<uint64_t>& done, int dev)
 template <int N, int DT>
 hadacore_status_t launch(const void* in, void* out, int64_t m, float scale, cudaStream_t stream) {
   using C = Cfg<N>;
-  constexpr int smem = C::stages * C::tile_bytes + 2 * C::stages * 8;
+  // SEG mode (n >= 8192): each (row, 128-byte-line segment) is its own TMA box
+  constexpr int box_segs = seg_mode(N, C::rows) ? 1 : 4;
+  constexpr int smem = C::stages * C::tile_bytes + 17 * C::stages * 8;  // + full[] and done[][<=16]
   static std::atomic<uint64_t> attr_done{0};
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return HADACORE_ERR_CUDA;
@@ -139,9 +141,10 @@ hadacore_status_t launch(const void* in, void* out, int64_t m, float scale, cuda
     auto kern = fwht_rows_kernel<N, DT, C::rows, C::stages, C::nt, C::p, C::u, C::ctas>;
     if (!ensure_smem_attr(kern, smem, attr_done, dev)) return HADACORE_ERR_CUDA;
     CUtensorMap tin, tout;
-    if (!encode_rows_map(&tin, in, m, N, C::rows) || !encode_rows_map(&tout, out, m, N, C::rows))
+    constexpr int box_rows = seg_mode(N, C::rows) ? 1 : C::rows;
+    if (!encode_rows_map(&tin, in, m, N, box_rows, box_segs) || !encode_rows_map(&tout, out, m, N, box_rows, box_segs))
       return HADACORE_ERR_CUDA;
-    kern<<<grid, (C::nt + 1) * 32, smem, stream>>>(tin, tout, m, s_res);
+    kern<<<grid, (C::nt + 1) * 32, smem, stream>>>(tin, tout, static_cast<uint16_t*>(out), m, s_res);
   }
   return cudaPeekAtLastError() == cudaSuccess ? HADACORE_OK : HADACORE_ERR_CUDA;
 }

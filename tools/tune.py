@@ -24,7 +24,8 @@ def build_one(spec):
             "-Xcompiler", "-fPIC", "-shared"]
     if spec.startswith("tuned"):
         name = spec.replace("-", "_")
-        extra = (["-DHC_NOCOMPUTE"] if "nocompute" in spec else []) + (["-DHC_SIMT"] if "simt" in spec else [])
+        extra = (["-DHC_NOCOMPUTE"] if "nocompute" in spec else []) + (["-DHC_SIMT"] if "simt" in spec else []) + \
+            (["-DHC_SEG"] if "-seg" in spec else []) + (["-DHC_STG_OUT"] if "stgout" in spec else [])
     else:
         nt, tkb, st, u, ctas = (spec.split(",") + ["1"])[:5]
         name = f"nt{nt}_t{tkb}_s{st}_u{u}_c{ctas}"
@@ -73,16 +74,22 @@ def run(reps=15, ns=None, repeats=3):
         fns[os.path.basename(path)[6:-3]] = f
     samples = {}
     mem = []
+    # paired design: all variants are measured back to back for each (repeat, dtype, n),
+    # so slow drifts of the box affect every variant alike
     for rep in range(repeats):
         mem.append(4.0 * elems / (batch_ms(lambda: dst.copy_(src)) * 1e-3) / 1e9)
-        for name, f in fns.items():
-            for dt in (0, 1):
-                for n in (ns or NS):
-                    m = elems // n
+        for dt in (0, 1):
+            for n in (ns or NS):
+                m = elems // n
+                for name, f in fns.items():
                     call = lambda: f(src.data_ptr(), dst.data_ptr(), m, n, dt, 1.0, st)
                     call()
                     gbs = 4.0 * elems / (batch_ms(call) * 1e-3) / 1e9
                     samples.setdefault(name, {}).setdefault(f"{'f16' if dt == 0 else 'bf16'}_{n}", []).append(gbs)
+    base = sorted(fns)[0] if "tuned" not in fns else "tuned"
+    for name in fns:
+        rel = {k: statistics.median([a / b for a, b in zip(v, samples[base][k])]) for k, v in samples[name].items()}
+        print(f"paired ratio vs {base}: {name} " + " ".join(f"{k}={r:.3f}" for k, r in rel.items()), flush=True)
     print(f"memcpy(copy_) back-to-back: median {statistics.median(mem):.0f} GB/s  samples {[round(v) for v in mem]}")
     # each variant must agree with the parity-tested default library (nocompute excluded)
     sys.path.insert(0, ROOT)
@@ -117,4 +124,5 @@ if __name__ == "__main__":
     if sys.argv[1] == "build":
         build(sys.argv[2:])
     else:
-        run()
+        ns = [int(v) for v in os.environ["TUNE_NS"].split(",")] if os.environ.get("TUNE_NS") else None
+        run(ns=ns, repeats=int(os.environ.get("TUNE_REPEATS", "3")))
