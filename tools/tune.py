@@ -74,22 +74,30 @@ def run(reps=15, ns=None, repeats=3):
         fns[os.path.basename(path)[6:-3]] = f
     samples = {}
     mem = []
-    # paired design: all variants are measured back to back for each (repeat, dtype, n),
-    # so slow drifts of the box affect every variant alike
+    # bench-like paired design: each variant runs whole C3 steps (18 different launches
+    # back to back, each timed with its own events, as bench.py does); variants
+    # alternate step by step so slow drifts of the box affect all of them alike
+    pairs = [(dt, n) for dt in (0, 1) for n in (ns or NS)]
     for rep in range(repeats):
         mem.append(4.0 * elems / (batch_ms(lambda: dst.copy_(src)) * 1e-3) / 1e9)
-        for dt in (0, 1):
-            for n in (ns or NS):
-                m = elems // n
-                for name, f in fns.items():
-                    call = lambda: f(src.data_ptr(), dst.data_ptr(), m, n, dt, 1.0, st)
-                    call()
-                    gbs = 4.0 * elems / (batch_ms(call) * 1e-3) / 1e9
-                    samples.setdefault(name, {}).setdefault(f"{'f16' if dt == 0 else 'bf16'}_{n}", []).append(gbs)
+        for name, f in fns.items():
+            for _ in range(2):  # 1 warm-up step + 1 timed step per repeat
+                evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in pairs]
+                for (dt, n), (a, b) in zip(pairs, evs):
+                    a.record()
+                    f(src.data_ptr(), dst.data_ptr(), elems // n, n, dt, 1.0, st)
+                    b.record()
+                torch.cuda.synchronize()
+            for (dt, n), (a, b) in zip(pairs, evs):
+                samples.setdefault(name, {}).setdefault(f"{'f16' if dt == 0 else 'bf16'}_{n}", []).append(
+                    4.0 * elems / (a.elapsed_time(b) * 1e-3) / 1e9)
     base = sorted(fns)[0] if "tuned" not in fns else "tuned"
     for name in fns:
         rel = {k: statistics.median([a / b for a, b in zip(v, samples[base][k])]) for k, v in samples[name].items()}
-        print(f"paired ratio vs {base}: {name} " + " ".join(f"{k}={r:.3f}" for k, r in rel.items()), flush=True)
+        agg = statistics.median([len(pairs) / sum(1.0 / samples[name][k][i] for k in samples[name])
+                                 for i in range(repeats)])
+        print(f"paired ratio vs {base}: {name} step-GB/s={agg:.0f} " + " ".join(f"{k}={r:.3f}" for k, r in rel.items()),
+              flush=True)
     print(f"memcpy(copy_) back-to-back: median {statistics.median(mem):.0f} GB/s  samples {[round(v) for v in mem]}")
     # each variant must agree with the parity-tested default library (nocompute excluded)
     sys.path.insert(0, ROOT)
