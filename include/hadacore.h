@@ -56,6 +56,12 @@ typedef enum {
   HADACORE_BF16 = 1  /* bfloat16 */
 } hadacore_dtype_t;
 
+/* Code formats of the fused quantized output (hadacore_fwht_quant). */
+typedef enum {
+  HADACORE_Q_E4M3 = 0, /* FP8 E4M3 ("e4m3fn": no infinities, max finite 448), RNE, saturating */
+  HADACORE_Q_INT8 = 1  /* signed 8-bit integer, RNE, clamped to [-127, 127] */
+} hadacore_qtype_t;
+
 typedef enum {
   HADACORE_OK = 0,
   HADACORE_ERR_INVALID_N = 1,   /* n is not a power of two in [128, 32768] */
@@ -91,6 +97,23 @@ hadacore_status_t hadacore_fwht(const void* in, void* out, int64_t m, int64_t n,
 hadacore_status_t hadacore_fwht_host(const void* in_host, void* out_host, int64_t m, int64_t n,
                                      hadacore_dtype_t dtype, float scale, void* workspace,
                                      size_t workspace_bytes, hadacore_stream_t stream);
+
+/*
+ * Fused transform + per-row symmetric quantization (the
+ * paper's future work "fused Hadamard transform and quantization", P:207 [Sec. 5],
+ * for its FP8-attention use, P:180 [Sec. 4.2]):
+ *     y = scale * H_n * in[i, :]            (as hadacore_fwht, never written out)
+ *     row_scale[i] = max_j |y_j| / Q        (Q = 448 for E4M3, 127 for INT8; 1 if y == 0)
+ *     out_q[i, j]  = round(y_j / row_scale[i])   (E4M3 saturating / INT8 clamped)
+ * so out_q[i, j] * row_scale[i] ~= y_j.  A row containing Inf/NaN gets a non-finite
+ * row_scale.  out_q: m x n bytes, row-major, 16-byte aligned; row_scale: m floats
+ * (fp32).  Neither may overlap `in`.  HBM traffic: 2 B read + 1 B written per element.
+ * Same validation, stream and error behaviour as hadacore_fwht; qtype outside the
+ * enum returns HADACORE_ERR_DTYPE.
+ */
+hadacore_status_t hadacore_fwht_quant(const void* in, void* out_q, float* row_scale, int64_t m, int64_t n,
+                                      hadacore_dtype_t dtype, hadacore_qtype_t qtype, float scale,
+                                      hadacore_stream_t stream);
 
 /* Static, human-readable description of a status code (never NULL). */
 const char* hadacore_status_string(hadacore_status_t status);

@@ -53,6 +53,13 @@ def _load():
         lib.oracle_dense_f64.restype = ctypes.c_int
         lib.oracle_dense_entry_f64.argtypes = [dp, ctypes.c_int64, ctypes.c_int64, ctypes.c_double]
         lib.oracle_dense_entry_f64.restype = ctypes.c_double
+        lib.oracle_e4m3_value.argtypes = [ctypes.c_int]
+        lib.oracle_e4m3_value.restype = ctypes.c_double
+        lib.oracle_e4m3_encode.argtypes = [ctypes.c_double]
+        lib.oracle_e4m3_encode.restype = ctypes.c_int
+        lib.oracle_quantize_rows_f64.argtypes = [dp, ctypes.POINTER(ctypes.c_uint8), dp, ctypes.c_int64,
+                                                 ctypes.c_int64, ctypes.c_int]
+        lib.oracle_quantize_rows_f64.restype = ctypes.c_int
         _lib = lib
     return _lib
 
@@ -110,3 +117,44 @@ def dense_entry(row, l: int, scale: float | None = None) -> float:
     if scale is None:
         scale = 1.0 / np.sqrt(n)
     return float(_load().oracle_dense_entry_f64(_ptr(a), n, int(l), float(scale)))
+
+
+QTYPES = {"e4m3": 0, "int8": 1}
+
+
+def e4m3_value(code: int) -> float:
+    """Value of an FP8 E4M3 (OCP e4m3fn) code, fp64."""
+    return _load().oracle_e4m3_value(int(code))
+
+
+def e4m3_encode(x: float) -> int:
+    """Nearest-even E4M3 code of x, saturating at +-448."""
+    return _load().oracle_e4m3_encode(float(x))
+
+
+def quantize_rows(y, qtype: str):
+    """Per-row symmetric quantization of transformed rows.
+
+    Returns (codes uint8 (m, n), scales float64 (m,)): scale = max|y|/Q (Q = 448 for
+    e4m3, 127 for int8; 1 for an all-zero row), codes = round(y / scale).
+    """
+    a = _as_f64_2d(y)
+    m, n = a.shape
+    codes = np.empty((m, n), dtype=np.uint8)
+    scales = np.empty(m, dtype=np.float64)
+    rc = _load().oracle_quantize_rows_f64(_ptr(a), codes.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8)),
+                                          _ptr(scales), m, n, QTYPES[qtype])
+    if rc != 0:
+        raise ValueError("oracle_quantize_rows_f64 rejected its arguments")
+    return codes, scales
+
+
+def dequantize_rows(codes, scales, qtype: str) -> np.ndarray:
+    """codes (m, n) uint8 and per-row scales -> fp64 values."""
+    codes = np.asarray(codes, dtype=np.uint8)
+    if qtype == "int8":
+        v = codes.view(np.int8).astype(np.float64)
+    else:
+        table = np.array([e4m3_value(c) for c in range(256)])
+        v = table[codes]
+    return v * np.asarray(scales, dtype=np.float64)[:, None]

@@ -124,3 +124,64 @@ int oracle_dense_f64(const double* in, double* out, int64_t m, int64_t n, double
     for (int64_t l = 0; l < n; ++l) out[r * n + l] = oracle_dense_entry_f64(in + r * n, n, l, scale);
   return 0;
 }
+
+/* ------------------------------------------------------------------------------
+ * Symmetric per-row quantization of a transformed row (the
+ * paper's stated future work "fused Hadamard transform and quantization"
+ * [Sec. 5], and its FP8-attention use, P:180 [Sec. 4.2]).  SPEC S:423-431: scale =
+ * max_abs / Q with Q = 448 (FP8 E4M3) or 127 (INT8); codes = round(x / scale);
+ * an all-zero row has scale 1 and zero codes.
+ *
+ * qtype 0 = FP8 E4M3 (OCP "e4m3fn": bias 7, no infinities, 0x7F/0xFF = NaN, max
+ *           finite 448): the code of the representable value nearest to x/scale,
+ *           ties to the even code, magnitudes above 448 saturate to 448.
+ * qtype 1 = INT8: round-half-to-even of x/scale, clamped to [-127, 127].
+ * Everything in fp64; the e4m3 encoder enumerates the 127 non-negative finite codes.
+ * ------------------------------------------------------------------------------ */
+double oracle_e4m3_value(int code) {
+  const int s = (code >> 7) & 1, e = (code >> 3) & 15, mant = code & 7;
+  if (e == 15 && mant == 7) return NAN;
+  double v = (e == 0) ? (mant / 8.0) * ldexp(1.0, -6) : (1.0 + mant / 8.0) * ldexp(1.0, e - 7);
+  return s ? -v : v;
+}
+
+int oracle_e4m3_encode(double x) {
+  if (x != x) return 0x7F;
+  const int neg = x < 0;
+  const double a = fabs(x);
+  int best = 0;
+  double best_err = INFINITY;
+  for (int c = 0; c <= 0x7E; ++c) { /* non-negative finite codes in increasing order */
+    const double err = fabs(oracle_e4m3_value(c) - a);
+    if (err < best_err || (err == best_err && (c & 1) == 0)) {
+      best = c;
+      best_err = err;
+    }
+  }
+  return (neg ? 0x80 : 0) | best; /* |x| > 448 lands on 0x7E (448): saturation */
+}
+
+/* y: m x n fp64 (already transformed); codes: m x n bytes; scales: m doubles. */
+int oracle_quantize_rows_f64(const double* y, uint8_t* codes, double* scales, int64_t m, int64_t n, int qtype) {
+  if (m < 0 || n < 1 || (qtype != 0 && qtype != 1)) return -1;
+  const double qmax = qtype == 0 ? 448.0 : 127.0;
+  for (int64_t r = 0; r < m; ++r) {
+    const double* row = y + r * n;
+    double amax = 0.0;
+    for (int64_t j = 0; j < n; ++j) amax = fmax(amax, fabs(row[j]));
+    const double s = amax > 0.0 ? amax / qmax : 1.0;
+    scales[r] = s;
+    for (int64_t j = 0; j < n; ++j) {
+      const double v = amax > 0.0 ? row[j] / s : 0.0;
+      if (qtype == 0) {
+        codes[r * n + j] = (uint8_t)oracle_e4m3_encode(v);
+      } else {
+        double q = nearbyint(v); /* default rounding mode: to nearest, ties to even */
+        if (q > 127.0) q = 127.0;
+        if (q < -127.0) q = -127.0;
+        codes[r * n + j] = (uint8_t)(int8_t)q;
+      }
+    }
+  }
+  return 0;
+}

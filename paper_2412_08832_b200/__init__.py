@@ -20,8 +20,8 @@ import os
 
 import torch
 
-__all__ = ["hadacore_fwht", "hadacore_fwht_host", "fwht", "HadacoreError", "library_path", "version",
-           "launches_per_call", "STATUS"]
+__all__ = ["hadacore_fwht", "hadacore_fwht_host", "hadacore_fwht_quant", "fwht", "HadacoreError", "library_path",
+           "version", "launches_per_call", "STATUS", "QTYPES"]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_HERE, "libhadacore.so")
@@ -33,6 +33,7 @@ STATUS = {
     7: "HADACORE_ERR_SCALE", 8: "HADACORE_ERR_CUDA", 9: "HADACORE_ERR_WORKSPACE",
 }
 _DTYPES = {torch.float16: 0, torch.bfloat16: 1}
+QTYPES = {"e4m3": (0, torch.float8_e4m3fn), "int8": (1, torch.int8)}
 
 
 class HadacoreError(RuntimeError):
@@ -58,6 +59,8 @@ def _load():
     lib.hadacore_fwht.restype = ctypes.c_int
     lib.hadacore_fwht_host.argtypes = [vp, vp, i64, i64, ctypes.c_int, f32, vp, ctypes.c_size_t, vp]
     lib.hadacore_fwht_host.restype = ctypes.c_int
+    lib.hadacore_fwht_quant.argtypes = [vp, vp, vp, i64, i64, ctypes.c_int, ctypes.c_int, f32, vp]
+    lib.hadacore_fwht_quant.restype = ctypes.c_int
     lib.hadacore_status_string.argtypes = [ctypes.c_int]
     lib.hadacore_status_string.restype = ctypes.c_char_p
     lib.hadacore_version.argtypes = []
@@ -145,3 +148,35 @@ def hadacore_fwht_host(x: torch.Tensor, out: torch.Tensor | None = None, scale: 
         _check(_load().hadacore_fwht_host(x.data_ptr(), out.data_ptr(), m, n, _DTYPES[x.dtype], float(scale),
                                           workspace.data_ptr(), workspace.numel(), st.cuda_stream))
     return out
+
+
+def hadacore_fwht_quant(x: torch.Tensor, qtype: str = "e4m3", scale: float | None = None,
+                        out: torch.Tensor | None = None, row_scale: torch.Tensor | None = None,
+                        stream: torch.cuda.Stream | None = None):
+    """Fused transform + per-row symmetric quantization (C: hadacore_fwht_quant).
+
+    Returns ``(q, row_scale)``: ``q`` has x's shape and dtype float8_e4m3fn ("e4m3")
+    or int8 ("int8"); ``row_scale`` is float32 with x's shape minus the last dim, so
+    ``q.float() * row_scale[..., None]`` ~= ``hadacore_fwht(x, scale=scale)``.
+    """
+    m, n = _shape(x)
+    if qtype not in QTYPES:
+        raise HadacoreError(6, f"qtype {qtype!r} (expected one of {sorted(QTYPES)})")
+    code, qdt = QTYPES[qtype]
+    if not x.is_cuda or not x.is_contiguous():
+        raise HadacoreError(8, "x must be a contiguous CUDA tensor")
+    if out is None:
+        out = torch.empty(x.shape, dtype=qdt, device=x.device)
+    if row_scale is None:
+        row_scale = torch.empty(x.shape[:-1], dtype=torch.float32, device=x.device)
+    if out.dtype != qdt or out.shape != x.shape or not out.is_contiguous() or out.device != x.device:
+        raise HadacoreError(3, f"out must be a contiguous {qdt} tensor with x's shape on x's device")
+    if row_scale.dtype != torch.float32 or row_scale.numel() != m or not row_scale.is_contiguous():
+        raise HadacoreError(3, "row_scale must be a contiguous float32 tensor with one entry per row")
+    if scale is None:
+        scale = 1.0 / math.sqrt(n) if n > 0 else 1.0
+    with torch.cuda.device(x.device):
+        st = stream if stream is not None else torch.cuda.current_stream(x.device)
+        _check(_load().hadacore_fwht_quant(x.data_ptr(), out.data_ptr(), row_scale.data_ptr(), m, n,
+                                           _DTYPES[x.dtype], code, float(scale), st.cuda_stream))
+    return out, row_scale

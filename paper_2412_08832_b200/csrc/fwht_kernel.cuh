@@ -311,6 +311,42 @@ __device__ __forceinline__ void simt_fwht_pack(const uint32_t x[4], uint32_t mas
   for (int j = 0; j < 4; ++j) z[j] = pack2<DT>(v[2 * j] * mul, v[2 * j + 1] * mul);
 }
 
+// ------------------------------------------------------------------ fused quantization
+// NEXT-1 ("fused Hadamard transform and quantization"):
+// per-row symmetric scale s = max|y| / Q (Q = 448 for FP8 E4M3, 127 for INT8; s = 1
+// for an all-zero row), codes = RNE(y / s) (E4M3 saturating, INT8 clamped to +-127).
+// A non-finite value in a row makes that row's scale non-finite.
+enum : int { QT_NONE = -1, QT_E4M3 = 0, QT_INT8 = 1 };
+template <int QT>
+__host__ __device__ constexpr float qmax_of() {
+  return QT == QT_E4M3 ? 448.f : 127.f;
+}
+// max that propagates NaN (a NaN anywhere in the row poisons the row's scale)
+__device__ __forceinline__ float nanmax(float a, float b) { return (b > a || b != b) ? b : a; }
+__device__ __forceinline__ float warp_nanmax(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = nanmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+template <int QT>
+__device__ __forceinline__ uint32_t quant4(float a, float b, float c, float d) {
+  if constexpr (QT == QT_E4M3) {
+    uint16_t lo, hi;
+    asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(lo) : "f"(b), "f"(a));
+    asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(hi) : "f"(d), "f"(c));
+    return uint32_t(lo) | (uint32_t(hi) << 16);
+  } else {
+    auto q = [](float v) { return uint32_t(min(127, max(-127, __float2int_rn(v)))) & 0xffu; };
+    return q(a) | (q(b) << 8) | (q(c) << 16) | (q(d) << 24);
+  }
+}
+// row scale and reciprocal from the row's max |y| (NaN propagates, Inf -> inv 0)
+template <int QT>
+__device__ __forceinline__ void row_scale_of(float amax, float& scale, float& inv) {
+  scale = amax > 0.f ? amax / qmax_of<QT>() : (amax == 0.f ? 1.f : amax);
+  inv = amax > 0.f ? qmax_of<QT>() / amax : (amax == 0.f ? 0.f : amax);
+}
+
 __device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t r[4]) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
@@ -361,9 +397,10 @@ __host__ __device__ constexpr int total_shift() {
 // Template parameters: N (row length), DT (dtype), TILE_ROWS (rows per pipeline
 // stage), STAGES (ring depth), NT (compute warps), P (warps per row team, n > 256),
 // U (work items per warp processed together, for ILP), CTAS (resident CTAs per SM).
-template <int N, int DT, int TILE_ROWS, int STAGES, int NT, int P, int U, int CTAS>
+template <int N, int DT, int TILE_ROWS, int STAGES, int NT, int P, int U, int CTAS, int QT>
 __global__ void __launch_bounds__((NT + 1) * 32, CTAS)
-    fwht_kernel(const uint16_t* __restrict__ in, uint16_t* __restrict__ out, int64_t m, float s_res) {
+    fwht_kernel(const uint16_t* __restrict__ in, uint16_t* __restrict__ out, uint8_t* __restrict__ out_q,
+                float* __restrict__ row_scale, int64_t m, float s_res) {
   constexpr int ROW_BYTES = 2 * N;
   constexpr int TILE_BYTES = TILE_ROWS * ROW_BYTES;
   static_assert(TILE_BYTES % 16 == 0, "bulk copy granularity");
@@ -430,6 +467,11 @@ __global__ void __launch_bounds__((NT + 1) * 32, CTAS)
 #pragma unroll
         for (int u = 0; u < U; ++u) {
 #ifdef HC_SIMT
+          if constexpr (QT >= 0) {
+            stage_ca<DT>(A1, x[u][0], x[u][2], x[u][1], x[u][3], y[u]);
+            stage_ca_f32<DT>(A2, y[u][0], y[u][1], y[u][2], y[u][3], d[u]);
+            continue;
+          }
           simt_fwht_pack<DT>(x[u], 0x7Fu, ldexpf(s_res, -total_shift<N>()), z[u]);  // all bits but the row bit b7
           const uint32_t t1 = z[u][1];  // natural slots: row A in (z0, z2), row B in (z1, z3)
           z[u][1] = z[u][2];
@@ -443,9 +485,30 @@ __global__ void __launch_bounds__((NT + 1) * 32, CTAS)
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           const int f = f0 + u * NT;
-          uint16_t* o = out + (row0 + 2 * f) * N + lane * 4;
-          if (2 * f < rows) stg64(o, z[u][0], z[u][1]);
-          if (2 * f + 1 < rows) stg64(o + N, z[u][2], z[u][3]);
+          if constexpr (QT >= 0) {  // rows A (d[0..3] = elements 4l..4l+3) and B (d[4..7])
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              float yv[4], a = 0.f;
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                yv[e] = d[u][4 * h + e] * s_res;
+                a = nanmax(a, fabsf(yv[e]));
+              }
+              a = warp_nanmax(a);
+              float sc, inv;
+              row_scale_of<QT>(a, sc, inv);
+              const int64_t row = row0 + 2 * f + h;
+              if (2 * f + h < rows) {
+                *reinterpret_cast<uint32_t*>(out_q + row * N + lane * 4) =
+                    quant4<QT>(yv[0] * inv, yv[1] * inv, yv[2] * inv, yv[3] * inv);
+                if (lane == 0) row_scale[row] = sc;
+              }
+            }
+          } else {
+            uint16_t* o = out + (row0 + 2 * f) * N + lane * 4;
+            if (2 * f < rows) stg64(o, z[u][0], z[u][1]);
+            if (2 * f + 1 < rows) stg64(o + N, z[u][2], z[u][3]);
+          }
         }
       }
       fence_proxy_async_smem();
@@ -470,17 +533,37 @@ __global__ void __launch_bounds__((NT + 1) * 32, CTAS)
 #pragma unroll
         for (int u = 0; u < U; ++u) {
 #ifdef HC_SIMT
-          simt_fwht_pack<DT>(x[u], 0xFFu, ldexpf(s_res, -total_shift<N>()), z[u]);
-#else
+          if constexpr (QT < 0) {
+            simt_fwht_pack<DT>(x[u], 0xFFu, ldexpf(s_res, -total_shift<N>()), z[u]);
+            continue;
+          }
+#endif
           stage_ca<DT>(A1, x[u][0], x[u][2], x[u][1], x[u][3], y[u]);
           stage_ca_f32<DT>(A1, y[u][0], y[u][2], y[u][1], y[u][3], d[u]);
-          scale_pack<DT>(d[u], s_res, z[u]);
-#endif
+          if constexpr (QT < 0) scale_pack<DT>(d[u], s_res, z[u]);
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           const int r = r0 + u * NT;
-          if (r < rows) stg128(out + (row0 + r) * N + lane * 8, z[u][0], z[u][1], z[u][2], z[u][3]);
+          if constexpr (QT >= 0) {  // d[0..7] = elements 8l..8l+7 of row r
+            float yv[8], a = 0.f;
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              yv[e] = d[u][e] * s_res;
+              a = nanmax(a, fabsf(yv[e]));
+            }
+            a = warp_nanmax(a);
+            float sc, inv;
+            row_scale_of<QT>(a, sc, inv);
+            if (r < rows) {
+              *reinterpret_cast<uint2*>(out_q + (row0 + r) * N + lane * 8) =
+                  make_uint2(quant4<QT>(yv[0] * inv, yv[1] * inv, yv[2] * inv, yv[3] * inv),
+                             quant4<QT>(yv[4] * inv, yv[5] * inv, yv[6] * inv, yv[7] * inv));
+              if (lane == 0) row_scale[row0 + r] = sc;
+            }
+          } else {
+            if (r < rows) stg128(out + (row0 + r) * N + lane * 8, z[u][0], z[u][1], z[u][2], z[u][3]);
+          }
         }
       }
       fence_proxy_async_smem();
@@ -489,6 +572,8 @@ __global__ void __launch_bounds__((NT + 1) * 32, CTAS)
     }
   } else {
     static_assert(N <= 256, "rows longer than 256 use fwht_rows_kernel");
+    (void)out_q;
+    (void)row_scale;
   }
 }
 
@@ -569,10 +654,11 @@ __device__ __forceinline__ void seg_loads(uint8_t* stage, const void* tmap, int 
 // copy-out pass.  Consumers: phase 1 = H_256 per chunk in place (LDS/STS.128),
 // team barrier, phase 2 = H_{n/256} across chunks via ldmatrix/stmatrix.trans,
 // then signal the producer, which stores the tile and refills the stage.
-template <int N, int DT, int TILE_ROWS, int STAGES, int NT, int P, int U, int CTAS>
+template <int N, int DT, int TILE_ROWS, int STAGES, int NT, int P, int U, int CTAS, int QT>
 __global__ void __launch_bounds__((NT + 1) * 32, CTAS)
     fwht_rows_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ CUtensorMap tm_out,
-                     uint16_t* __restrict__ out, int64_t m, float s_res) {
+                     uint16_t* __restrict__ out, uint8_t* __restrict__ out_q, float* __restrict__ row_scale,
+                     int64_t m, float s_res) {
   constexpr int ROW_BYTES = 2 * N;
   constexpr int TILE_BYTES = TILE_ROWS * ROW_BYTES;
   constexpr int Q = log2_n<N>() - 8;
@@ -590,14 +676,15 @@ __global__ void __launch_bounds__((NT + 1) * 32, CTAS)
 
   // SEG: phase-2 items are the rows' 32 granule columns; each (row, segment) box is
   // stored (and refilled) as soon as its 8 items are done (seg_mode above).
-  constexpr bool STG_OUT = kStgOut;
-  constexpr bool SEG = seg_mode(N, TILE_ROWS);
+  constexpr bool STG_OUT = kStgOut || QT >= 0;  // quantized output is written by the consumers
+  constexpr bool SEG = QT < 0 && seg_mode(N, TILE_ROWS);
   constexpr int NSEG = SEG ? 4 * TILE_ROWS : 1;  // boxes (and done barriers) per tile
   constexpr int SEG_BYTES = ROW_BYTES / 4;
 
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * TILE_BYTES);
   uint64_t* done = full + STAGES;  // [STAGES][NSEG] consumers -> producer: ready to store
+  float* red = reinterpret_cast<float*>(smem + STAGES * TILE_BYTES + 17 * STAGES * 8);  // [NTEAMS][RPT][P] row max
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t num_tiles = (m + TILE_ROWS - 1) / TILE_ROWS;
 
@@ -734,6 +821,9 @@ __global__ void __launch_bounds__((NT + 1) * 32, CTAS)
     team_sync();  // P:126 "Sync across the threadblock"
 
     // ---- phase 2: H_{n/256} across chunks (residual 2^a factor)
+    float amax_r[RPT];  // fused quantization: running max |y| of each of the team's rows
+#pragma unroll
+    for (int k = 0; k < RPT; ++k) amax_r[k] = 0.f;
     for (int i0 = wt; i0 < ITEMS2; i0 += P * U2) {
       uint32_t x[U2][1 << PL::nx][4];
       uint32_t addr[U2][1 << PL::nx];
@@ -780,6 +870,17 @@ __global__ void __launch_bounds__((NT + 1) * 32, CTAS)
                 d[xi | (1 << b)][e] = p0 - p1;
               }
             }
+        if constexpr (QT >= 0) {
+          const int rl = (i0 + u * P) / NLOOP;
+          float a = 0.f;
+#pragma unroll
+          for (int xi = 0; xi < (1 << PL::nx); ++xi)
+#pragma unroll
+            for (int e = 0; e < 8; ++e) a = nanmax(a, fabsf(d[xi][e] * s_res));
+#pragma unroll
+          for (int k = 0; k < RPT; ++k)
+            if (k == rl) amax_r[k] = nanmax(amax_r[k], a);
+        }
 #pragma unroll
         for (int xi = 0; xi < (1 << PL::nx); ++xi) {
           uint32_t z[4];
@@ -794,7 +895,49 @@ __global__ void __launch_bounds__((NT + 1) * 32, CTAS)
         }
       }
     }
-    if constexpr (STG_OUT) {
+    if constexpr (QT >= 0) {
+      // ---- fused quantization (NEXT-1): row max over the team, then codes + scales
+#pragma unroll
+      for (int k = 0; k < RPT; ++k) {
+        const float a = warp_nanmax(amax_r[k]);
+        if (lane == 0) red[(team * RPT + k) * P + wt] = a;
+      }
+      team_sync();
+      float inv_r[RPT];
+      const int64_t row0 = tile * TILE_ROWS;
+#pragma unroll
+      for (int k = 0; k < RPT; ++k) {
+        float a = 0.f;
+        for (int w = 0; w < P; ++w) a = nanmax(a, red[(team * RPT + k) * P + w]);
+        float sc;
+        row_scale_of<QT>(a, sc, inv_r[k]);
+        const int r = team + NTEAMS * k;
+        if (wt == 0 && lane == 0 && row0 + r < m) row_scale[row0 + r] = sc;
+      }
+      for (int i0 = wt; i0 < ITEMS1; i0 += P * U1) {
+        uint32_t z[U1][4];
+#pragma unroll
+        for (int u = 0; u < U1; ++u) {
+          const int item = i0 + u * P, r = team + NTEAMS * (item / C), c = item % C;
+          lds128(tb + r * ROW_BYTES + gofs<C>(uint32_t(c), uint32_t(lane)), z[u][0], z[u][1], z[u][2], z[u][3]);
+        }
+#pragma unroll
+        for (int u = 0; u < U1; ++u) {
+          const int item = i0 + u * P, rl = item / C, r = team + NTEAMS * rl, c = item % C;
+          float inv = 0.f;
+#pragma unroll
+          for (int k = 0; k < RPT; ++k)
+            if (k == rl) inv = inv_r[k];
+          float v[8];
+          unpack8<DT>(z[u], v);
+          if (row0 + r < m)
+            *reinterpret_cast<uint2*>(out_q + (row0 + r) * N + c * 256 + lane * 8) =
+                make_uint2(quant4<QT>(v[0] * inv, v[1] * inv, v[2] * inv, v[3] * inv),
+                           quant4<QT>(v[4] * inv, v[5] * inv, v[6] * inv, v[7] * inv));
+        }
+      }
+      // (red[] is rewritten only after the next tile's phase-1 barrier: no race)
+    } else if constexpr (STG_OUT) {
       team_sync();
       const int64_t row0 = tile * TILE_ROWS;
       for (int i0 = wt; i0 < ITEMS1; i0 += P * U1) {

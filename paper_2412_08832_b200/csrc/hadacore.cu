@@ -118,12 +118,14 @@ bool ensure_smem_attr(Kern kern, int smem, std::atomic<uint64_t>& done, int dev)
   return true;
 }
 
-template <int N, int DT>
-hadacore_status_t launch(const void* in, void* out, int64_t m, float scale, cudaStream_t stream) {
+template <int N, int DT, int QT>
+hadacore_status_t launch(const void* in, void* out, uint8_t* out_q, float* row_scale, int64_t m, float scale,
+                         cudaStream_t stream) {
   using C = Cfg<N>;
   // SEG mode (n >= 8192): each (row, 128-byte-line segment) is its own TMA box
   constexpr int box_segs = seg_mode(N, C::rows) ? 1 : 4;
-  constexpr int smem = C::stages * C::tile_bytes + 17 * C::stages * 8;  // + full[] and done[][<=16]
+  // + full[], done[][<=16] and the fused-quantization row-max scratch (one float per warp)
+  constexpr int smem = C::stages * C::tile_bytes + 17 * C::stages * 8 + 4 * C::nt * (N > 256 ? C::rows : 1);
   static std::atomic<uint64_t> attr_done{0};
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return HADACORE_ERR_CUDA;
@@ -134,35 +136,37 @@ hadacore_status_t launch(const void* in, void* out, int64_t m, float scale, cuda
   // `scale` into the fp32 epilogue of the last stage.
   const float s_res = std::ldexp(scale, total_shift<N>());
   if constexpr (N <= 256) {
-    auto kern = fwht_kernel<N, DT, C::rows, C::stages, C::nt, C::p, C::u, C::ctas>;
+    auto kern = fwht_kernel<N, DT, C::rows, C::stages, C::nt, C::p, C::u, C::ctas, QT>;
     if (!ensure_smem_attr(kern, smem, attr_done, dev)) return HADACORE_ERR_CUDA;
     kern<<<grid, (C::nt + 1) * 32, smem, stream>>>(static_cast<const uint16_t*>(in), static_cast<uint16_t*>(out),
-                                                    m, s_res);
+                                                    out_q, row_scale, m, s_res);
   } else {
-    auto kern = fwht_rows_kernel<N, DT, C::rows, C::stages, C::nt, C::p, C::u, C::ctas>;
+    auto kern = fwht_rows_kernel<N, DT, C::rows, C::stages, C::nt, C::p, C::u, C::ctas, QT>;
     if (!ensure_smem_attr(kern, smem, attr_done, dev)) return HADACORE_ERR_CUDA;
     CUtensorMap tin, tout;
     constexpr int box_rows = seg_mode(N, C::rows) ? 1 : C::rows;
-    if (!encode_rows_map(&tin, in, m, N, box_rows, box_segs) || !encode_rows_map(&tout, out, m, N, box_rows, box_segs))
+    if (!encode_rows_map(&tin, in, m, N, box_rows, box_segs) ||
+        !encode_rows_map(&tout, QT >= 0 ? in : out, m, N, box_rows, box_segs))  // unused when quantizing
       return HADACORE_ERR_CUDA;
-    kern<<<grid, (C::nt + 1) * 32, smem, stream>>>(tin, tout, static_cast<uint16_t*>(out), m, s_res);
+    kern<<<grid, (C::nt + 1) * 32, smem, stream>>>(tin, tout, static_cast<uint16_t*>(out), out_q, row_scale, m,
+                                                    s_res);
   }
   return cudaPeekAtLastError() == cudaSuccess ? HADACORE_OK : HADACORE_ERR_CUDA;
 }
 
-template <int DT>
-hadacore_status_t dispatch_n(const void* in, void* out, int64_t m, int64_t n, float scale,
+template <int DT, int QT>
+hadacore_status_t dispatch_n(const void* in, void* out, uint8_t* q, float* rs, int64_t m, int64_t n, float scale,
                              cudaStream_t st) {
   switch (n) {
-    case 128: return launch<128, DT>(in, out, m, scale, st);
-    case 256: return launch<256, DT>(in, out, m, scale, st);
-    case 512: return launch<512, DT>(in, out, m, scale, st);
-    case 1024: return launch<1024, DT>(in, out, m, scale, st);
-    case 2048: return launch<2048, DT>(in, out, m, scale, st);
-    case 4096: return launch<4096, DT>(in, out, m, scale, st);
-    case 8192: return launch<8192, DT>(in, out, m, scale, st);
-    case 16384: return launch<16384, DT>(in, out, m, scale, st);
-    case 32768: return launch<32768, DT>(in, out, m, scale, st);
+    case 128: return launch<128, DT, QT>(in, out, q, rs, m, scale, st);
+    case 256: return launch<256, DT, QT>(in, out, q, rs, m, scale, st);
+    case 512: return launch<512, DT, QT>(in, out, q, rs, m, scale, st);
+    case 1024: return launch<1024, DT, QT>(in, out, q, rs, m, scale, st);
+    case 2048: return launch<2048, DT, QT>(in, out, q, rs, m, scale, st);
+    case 4096: return launch<4096, DT, QT>(in, out, q, rs, m, scale, st);
+    case 8192: return launch<8192, DT, QT>(in, out, q, rs, m, scale, st);
+    case 16384: return launch<16384, DT, QT>(in, out, q, rs, m, scale, st);
+    case 32768: return launch<32768, DT, QT>(in, out, q, rs, m, scale, st);
     default: return HADACORE_ERR_INVALID_N;
   }
 }
@@ -190,8 +194,22 @@ hadacore_status_t validate(const void* in, const void* out, int64_t m, int64_t n
 
 hadacore_status_t run(const void* in, void* out, int64_t m, int64_t n, int dtype, float scale,
                       cudaStream_t st) {
-  return dtype == HADACORE_F16 ? dispatch_n<DT_F16>(in, out, m, n, scale, st)
-                               : dispatch_n<DT_BF16>(in, out, m, n, scale, st);
+  return dtype == HADACORE_F16 ? dispatch_n<DT_F16, QT_NONE>(in, out, nullptr, nullptr, m, n, scale, st)
+                               : dispatch_n<DT_BF16, QT_NONE>(in, out, nullptr, nullptr, m, n, scale, st);
+}
+
+hadacore_status_t run_quant(const void* in, uint8_t* q, float* rs, int64_t m, int64_t n, int dtype, int qtype,
+                            float scale, cudaStream_t st) {
+  if (dtype == HADACORE_F16)
+    return qtype == HADACORE_Q_E4M3 ? dispatch_n<DT_F16, QT_E4M3>(in, nullptr, q, rs, m, n, scale, st)
+                                    : dispatch_n<DT_F16, QT_INT8>(in, nullptr, q, rs, m, n, scale, st);
+  return qtype == HADACORE_Q_E4M3 ? dispatch_n<DT_BF16, QT_E4M3>(in, nullptr, q, rs, m, n, scale, st)
+                                  : dispatch_n<DT_BF16, QT_INT8>(in, nullptr, q, rs, m, n, scale, st);
+}
+
+bool ranges_overlap(const void* a, size_t abytes, const void* b, size_t bbytes) {
+  const uintptr_t x = reinterpret_cast<uintptr_t>(a), y = reinterpret_cast<uintptr_t>(b);
+  return x < y + bbytes && y < x + abytes;
 }
 
 }  // namespace
@@ -204,6 +222,24 @@ extern "C" hadacore_status_t hadacore_fwht(const void* in, void* out, int64_t m,
   const hadacore_status_t v = validate(in, out, m, n, int(dtype), scale, true);
   if (v != HADACORE_OK || m == 0) return v;
   return run(in, out, m, n, int(dtype), scale, reinterpret_cast<cudaStream_t>(stream));
+}
+
+extern "C" hadacore_status_t hadacore_fwht_quant(const void* in, void* out_q, float* row_scale, int64_t m,
+                                                 int64_t n, hadacore_dtype_t dtype, hadacore_qtype_t qtype,
+                                                 float scale, hadacore_stream_t stream) {
+  if (qtype != HADACORE_Q_E4M3 && qtype != HADACORE_Q_INT8) return HADACORE_ERR_DTYPE;
+  // validate `in` (and m, n, dtype, scale) exactly like hadacore_fwht, with out = in
+  const hadacore_status_t v = validate(in, in, m, n, int(dtype), scale, true);
+  if (v != HADACORE_OK || m == 0) return v;
+  if (!out_q || !row_scale) return HADACORE_ERR_NULL;
+  if ((reinterpret_cast<uintptr_t>(out_q) & 15u) || (reinterpret_cast<uintptr_t>(row_scale) & 3u))
+    return HADACORE_ERR_MISALIGNED;
+  const size_t in_bytes = size_t(m) * size_t(n) * 2, q_bytes = size_t(m) * size_t(n), s_bytes = size_t(m) * 4;
+  if (ranges_overlap(in, in_bytes, out_q, q_bytes) || ranges_overlap(in, in_bytes, row_scale, s_bytes) ||
+      ranges_overlap(out_q, q_bytes, row_scale, s_bytes))
+    return HADACORE_ERR_OVERLAP;
+  return run_quant(in, static_cast<uint8_t*>(out_q), row_scale, m, n, int(dtype), int(qtype), scale,
+                   reinterpret_cast<cudaStream_t>(stream));
 }
 
 extern "C" hadacore_status_t hadacore_fwht_host(const void* in_host, void* out_host, int64_t m, int64_t n,

@@ -29,8 +29,9 @@ def declared_functions():
 
 
 def test_header_declares_expected_entry_points():
-    assert declared_functions() == sorted(["hadacore_fwht", "hadacore_fwht_host", "hadacore_status_string",
-                                           "hadacore_version", "hadacore_launches_per_call"])
+    assert declared_functions() == sorted(["hadacore_fwht", "hadacore_fwht_host", "hadacore_fwht_quant",
+                                           "hadacore_status_string", "hadacore_version",
+                                           "hadacore_launches_per_call"])
 
 
 def test_library_exports_every_declared_symbol(lib):
@@ -88,6 +89,23 @@ def test_host_entry_validation(lib):
     assert f(a, b, 4, 256, 0, 1.0, ws + 4, 1 << 20, None) == WORKSPACE
     assert f(a, a + 2, 4, 256, 0, 1.0, ws, 1 << 20, None) == OVERLAP
     assert f(None, None, 0, 256, 0, 1.0, None, 0, None) == OK
+
+
+def test_quant_entry_validation(lib):
+    a, q, rs = 0x10000, 0x8000000, 0x20000000
+    f = lib.hadacore_fwht_quant
+    assert f(a, q, rs, 4, 256, 0, 2, 1.0, None) == DTYPE          # unknown qtype
+    assert f(a, q, rs, 4, 256, 3, 0, 1.0, None) == DTYPE          # unknown dtype
+    assert f(a, q, rs, 4, 100, 0, 0, 1.0, None) == INVALID_N
+    assert f(a, q, rs, 4, 256, 0, 1, float("nan"), None) == SCALE
+    assert f(a, None, rs, 4, 256, 0, 0, 1.0, None) == NULL
+    assert f(a, q, None, 4, 256, 0, 0, 1.0, None) == NULL
+    assert f(a, q + 8, rs, 4, 256, 0, 0, 1.0, None) == MISALIGNED
+    assert f(a, q, rs + 2, 4, 256, 0, 0, 1.0, None) == MISALIGNED
+    assert f(a, a + 1024, rs, 4, 256, 0, 0, 1.0, None) == OVERLAP  # codes inside the input
+    assert f(a, q, a + 64, 4, 256, 0, 0, 1.0, None) == OVERLAP     # scales inside the input
+    assert f(a, q, q + 256, 4, 256, 0, 0, 1.0, None) == OVERLAP    # scales inside the codes
+    assert f(None, None, None, 0, 256, 1, 1, 1.0, None) == OK
 
 
 def test_status_strings_and_version(lib):

@@ -177,3 +177,59 @@ def test_rejects_bad_sizes():
     with pytest.raises(ValueError):
         oracle.dense(np.zeros((2, 12)))
     assert oracle.fwht(np.zeros((0, 64))).shape == (0, 64)
+
+
+# ---------------------------------------------------------------- quantization oracle
+# Pins for oracle.quantize_rows / e4m3.
+
+def test_e4m3_codes_match_torch_float8():
+    # an independent implementation (torch.float8_e4m3fn, RNE) over the finite range
+    import torch
+    x = np.concatenate([np.random.default_rng(1).standard_normal(20000) * s for s in (1e-3, 0.1, 1, 10, 100)])
+    # fp32-representable inputs: torch converts via fp32, which would double-round fp64 values
+    x = x[np.abs(x) <= 448].astype(np.float32).astype(np.float64)
+    ours = np.array([oracle.e4m3_encode(v) for v in x], dtype=np.uint8)
+    ref = torch.from_numpy(x).to(torch.float8_e4m3fn).view(torch.uint8).numpy()
+    assert np.array_equal(ours, ref)
+    # every finite code round-trips ("identity on all valid codes")
+    for c in list(range(0, 0x7F)) + list(range(0x80, 0xFF)):
+        v = oracle.e4m3_value(c)
+        assert oracle.e4m3_value(oracle.e4m3_encode(v)) == v
+
+
+def test_e4m3_worked_values_and_saturation():
+    assert oracle.e4m3_value(oracle.e4m3_encode(30.0)) == 30.0      # S:284 exact
+    assert oracle.e4m3_encode(448.0) == 0x7E                         # max finite
+    assert oracle.e4m3_encode(1e6) == 0x7E and oracle.e4m3_encode(-1e6) == 0xFE   # satfinite
+    assert oracle.e4m3_encode(1.0) == 0x38
+    assert oracle.e4m3_value(0x01) == 2.0 ** -9                      # smallest subnormal
+
+
+def test_quantize_rows_closed_forms():
+    # max_abs = 127 -> scale 1, integers round-trip exactly
+    y = np.array([[127.0, -3.0, 0.0, 64.0]])
+    codes, s = oracle.quantize_rows(y, "int8")
+    assert s[0] == 1.0 and list(codes[0].view(np.int8)) == [127, -3, 0, 64]
+    # [448, 0] in e4m3 round-trips exactly
+    codes, s = oracle.quantize_rows(np.array([[448.0, 0.0]]), "e4m3")
+    assert s[0] == 1.0 and list(codes[0]) == [0x7E, 0x00]
+    # all-zero row: scale 1, zero codes (S:431 AllZeroInput)
+    codes, s = oracle.quantize_rows(np.zeros((1, 8)), "int8")
+    assert s[0] == 1.0 and not codes.any()
+    # ties to even: 2.5 -> 2, 3.5 -> 4 (scale 1 via a 127 anchor)
+    codes, _ = oracle.quantize_rows(np.array([[127.0, 2.5, 3.5, -2.5]]), "int8")
+    assert list(codes[0].view(np.int8)) == [127, 2, 4, -2]
+
+
+def test_quantization_error_bounds_on_random_rows():
+    rng = np.random.default_rng(3)
+    y = rng.standard_normal((20, 1024))
+    for qtype in ("int8", "e4m3"):
+        codes, s = oracle.quantize_rows(y, qtype)
+        deq = oracle.dequantize_rows(codes, s, qtype)
+        err = np.abs(deq - y)
+        if qtype == "int8":
+            assert np.all(err <= s[:, None] / 2 + 1e-12)
+        else:  # relative 2^-4 in the normal range, half the subnormal spacing below it
+            assert np.all(err <= np.abs(y) * 2.0 ** -4 + s[:, None] * 2.0 ** -10 + 1e-12)
+        assert np.allclose(np.abs(deq).max(axis=1), np.abs(y).max(axis=1))   # the max is exact
