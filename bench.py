@@ -48,6 +48,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--workload", choices=["fwht", "quant-e4m3", "quant-int8"], default="fwht",
+                    help="fwht = the metric's C3 sweep (default); quant-* = the fused FWHT + per-row "
+                         "quantization row (NEXT-1) on the same inputs")
     return ap.parse_args()
 
 
@@ -227,7 +230,7 @@ def config_block(args, world):
     return {"workload": "C3 size sweep: n=2^7..2^15 x {fp16, bf16}, 2^28 elements per (n, dtype) per GPU, "
                         "out-of-place, normalized (scale=1/sqrt(n))",
             "elements_per_launch": args.elems, "ns": NS, "dtypes": ["fp16", "bf16"],
-            "launches_per_step": 2 * len(NS),
+            "launches_per_step": 2 * len(NS), "path": getattr(args, "workload", "fwht"),
             "l2": "no flush: every launch reads a 512 MiB input and writes a 512 MiB output (> 126 MB L2)",
             "parallelism": f"row-sharded x{world}, no collective on the hot path" if world > 1 else "single GPU"}
 
@@ -261,9 +264,18 @@ def main():
     obuf = torch.empty(args.elems, dtype=torch.float16, device=dev)
     stream = torch.cuda.current_stream(dev)
     pairs = [(dt, n) for dt in (torch.float16, torch.bfloat16) for n in NS]
+    quant = args.workload.startswith("quant")
+    qtype = args.workload.split("-")[1] if quant else None
+    if quant:
+        qbuf = torch.empty(args.elems, dtype=hc.QTYPES[qtype][1], device=dev)
+        sbuf = torch.empty(args.elems // 128, dtype=torch.float32, device=dev)
 
     def launch(dt, n):
         x = xin[dt].view(-1, n)
+        if quant:
+            hc.hadacore_fwht_quant(x, qtype=qtype, out=qbuf.view(-1, n), row_scale=sbuf[: x.shape[0]],
+                                   stream=stream)
+            return
         o = obuf.view(torch.int16).view(dt).view(-1, n)
         hc.hadacore_fwht(x, out=o, stream=stream)
 
@@ -309,7 +321,10 @@ def main():
         remeasured = True
 
     t_max = max_over_ranks(total_ms, dist, torch)
-    bytes_per_launch = 4.0 * args.elems
+    # algorithmic bytes: 2 B read + 2 B written per element (fwht); 2 + 1 B plus one fp32
+    # scale per row for the fused quantization (per-n average over the sweep)
+    bytes_per_launch = 4.0 * args.elems if not quant else \
+        sum(3.0 * args.elems + 4.0 * (args.elems // n) for n in NS) / len(NS)
     total_bytes = bytes_per_launch * len(pairs) * args.steps * world
     value = total_bytes / (t_max * 1e-3) / 1e9
 
@@ -318,12 +333,12 @@ def main():
     for k, (dt, n) in enumerate(pairs):
         ts = sorted(per[k::len(pairs)])
         med = ts[len(ts) // 2]
-        per_n.setdefault("fp16" if dt == torch.float16 else "bf16", {})[str(n)] = round(
-            bytes_per_launch / (med * 1e-3) / 1e9, 1)
+        b_n = 4.0 * args.elems if not quant else 3.0 * args.elems + 4.0 * (args.elems // n)
+        per_n.setdefault("fp16" if dt == torch.float16 else "bf16", {})[str(n)] = round(b_n / (med * 1e-3) / 1e9, 1)
     avg_launch_ms = sum(per) / len(per)
     peak, peak_src = measured_hbm_peak()
     achieved = bytes_per_launch / (avg_launch_ms * 1e-3) / 1e9
-    traffic = ncu_traffic()
+    traffic = ncu_traffic() if not quant else None
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "peak_source": peak_src,
                 "frac_of_8TBps": round(achieved / NOMINAL_HBM_GBS, 4),
@@ -333,7 +348,7 @@ def main():
 
     # end to end through the public host-buffer C entry (hadacore_fwht_host)
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and not quant:
         hin = {dt: xin[dt].cpu().pin_memory() for dt in xin}
         hout = torch.empty(args.elems, dtype=torch.float16).pin_memory()
         ws = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
@@ -356,7 +371,7 @@ def main():
         del hin, hout, ws
 
     cpu_baseline = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and not quant:
         import oracle
         oracle.build()
         threads = oracle.default_threads()
@@ -368,8 +383,10 @@ def main():
                                   f"({e} elements total), fp64 listing, {t:.2f} s; widening excluded"}
 
     if rank == 0:
+        metric = METRIC if not quant else (f"Fused FWHT + per-row {qtype.upper()} quantization HBM GB/s vs "
+                                           "n=2^7..2^15 (bf16/fp16 in, 8-bit codes + fp32 row scales out)")
         line = {
-            "metric": METRIC, "value": round(value, 1), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "metric": metric, "value": round(value, 1), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(t_max / args.steps, 4), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "fp16+bf16 (fp32 last-stage accumulate)",
             "data": "synthetic (counter-based N(0,1), synthetic/)", "config": config_block(args, world),

@@ -321,12 +321,17 @@ template <int QT>
 __host__ __device__ constexpr float qmax_of() {
   return QT == QT_E4M3 ? 448.f : 127.f;
 }
-// max that propagates NaN (a NaN anywhere in the row poisons the row's scale)
-__device__ __forceinline__ float nanmax(float a, float b) { return (b > a || b != b) ? b : a; }
-__device__ __forceinline__ float warp_nanmax(float v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v = nanmax(v, __shfl_xor_sync(0xffffffffu, v, o));
-  return v;
+// max of |v| that propagates NaN (max.NaN, one FMNMX.NAN): a NaN anywhere in a row
+// poisons the row's scale, an Inf makes it Inf
+__device__ __forceinline__ float absmax_nan(float acc, float v) {
+  float r;
+  asm("max.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(acc), "f"(fabsf(v)));
+  return r;
+}
+// warp-wide max of non-negative floats (or +NaN): their bit patterns order like
+// unsigned integers (NaN > Inf > finite), so one redux.sync.max.u32 (REDUX) does it
+__device__ __forceinline__ float warp_absmax(float v) {
+  return __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(v)));
 }
 template <int QT>
 __device__ __forceinline__ uint32_t quant4(float a, float b, float c, float d) {
@@ -336,15 +341,23 @@ __device__ __forceinline__ uint32_t quant4(float a, float b, float c, float d) {
     asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(hi) : "f"(d), "f"(c));
     return uint32_t(lo) | (uint32_t(hi) << 16);
   } else {
-    auto q = [](float v) { return uint32_t(min(127, max(-127, __float2int_rn(v)))) & 0xffu; };
-    return q(a) | (q(b) << 8) | (q(c) << 16) | (q(d) << 24);
+    // RNE with saturation to [-128, 127]; -128 cannot occur because |v| <= Q (up to
+    // the rounding of the reciprocal, which stays below 127.5)
+    int qa, qb, qc, qd;
+    asm("cvt.rni.sat.s8.f32 %0, %1;" : "=r"(qa) : "f"(a));
+    asm("cvt.rni.sat.s8.f32 %0, %1;" : "=r"(qb) : "f"(b));
+    asm("cvt.rni.sat.s8.f32 %0, %1;" : "=r"(qc) : "f"(c));
+    asm("cvt.rni.sat.s8.f32 %0, %1;" : "=r"(qd) : "f"(d));
+    return __byte_perm(__byte_perm(uint32_t(qa), uint32_t(qb), 0x0040), __byte_perm(uint32_t(qc), uint32_t(qd), 0x0040),
+                       0x5410);
   }
 }
-// row scale and reciprocal from the row's max |y| (NaN propagates, Inf -> inv 0)
+// row scale s = amax / Q and the code multiplier Q / amax (amax = max |y| >= 0, Inf or NaN)
 template <int QT>
 __device__ __forceinline__ void row_scale_of(float amax, float& scale, float& inv) {
-  scale = amax > 0.f ? amax / qmax_of<QT>() : (amax == 0.f ? 1.f : amax);
-  inv = amax > 0.f ? qmax_of<QT>() / amax : (amax == 0.f ? 0.f : amax);
+  const bool pos = amax > 0.f;  // false for 0 and NaN
+  scale = pos ? amax * (1.f / qmax_of<QT>()) : (amax == 0.f ? 1.f : amax);
+  inv = pos ? qmax_of<QT>() * __frcp_rn(amax) : (amax == 0.f ? 0.f : amax);
 }
 
 __device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t r[4]) {
@@ -488,19 +501,16 @@ __global__ void __launch_bounds__((NT + 1) * 32, CTAS)
           if constexpr (QT >= 0) {  // rows A (d[0..3] = elements 4l..4l+3) and B (d[4..7])
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
-              float yv[4], a = 0.f;
+              float a = 0.f;
 #pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                yv[e] = d[u][4 * h + e] * s_res;
-                a = nanmax(a, fabsf(yv[e]));
-              }
-              a = warp_nanmax(a);
+              for (int e = 0; e < 4; ++e) a = absmax_nan(a, d[u][4 * h + e]);
               float sc, inv;
-              row_scale_of<QT>(a, sc, inv);
+              row_scale_of<QT>(warp_absmax(a) * fabsf(s_res), sc, inv);
+              const float mul = s_res * inv;
               const int64_t row = row0 + 2 * f + h;
               if (2 * f + h < rows) {
                 *reinterpret_cast<uint32_t*>(out_q + row * N + lane * 4) =
-                    quant4<QT>(yv[0] * inv, yv[1] * inv, yv[2] * inv, yv[3] * inv);
+                    quant4<QT>(d[u][4 * h] * mul, d[u][4 * h + 1] * mul, d[u][4 * h + 2] * mul, d[u][4 * h + 3] * mul);
                 if (lane == 0) row_scale[row] = sc;
               }
             }
@@ -546,19 +556,16 @@ __global__ void __launch_bounds__((NT + 1) * 32, CTAS)
         for (int u = 0; u < U; ++u) {
           const int r = r0 + u * NT;
           if constexpr (QT >= 0) {  // d[0..7] = elements 8l..8l+7 of row r
-            float yv[8], a = 0.f;
+            float a = 0.f;
 #pragma unroll
-            for (int e = 0; e < 8; ++e) {
-              yv[e] = d[u][e] * s_res;
-              a = nanmax(a, fabsf(yv[e]));
-            }
-            a = warp_nanmax(a);
+            for (int e = 0; e < 8; ++e) a = absmax_nan(a, d[u][e]);
             float sc, inv;
-            row_scale_of<QT>(a, sc, inv);
+            row_scale_of<QT>(warp_absmax(a) * fabsf(s_res), sc, inv);
+            const float mul = s_res * inv;
             if (r < rows) {
               *reinterpret_cast<uint2*>(out_q + (row0 + r) * N + lane * 8) =
-                  make_uint2(quant4<QT>(yv[0] * inv, yv[1] * inv, yv[2] * inv, yv[3] * inv),
-                             quant4<QT>(yv[4] * inv, yv[5] * inv, yv[6] * inv, yv[7] * inv));
+                  make_uint2(quant4<QT>(d[u][0] * mul, d[u][1] * mul, d[u][2] * mul, d[u][3] * mul),
+                             quant4<QT>(d[u][4] * mul, d[u][5] * mul, d[u][6] * mul, d[u][7] * mul));
               if (lane == 0) row_scale[row0 + r] = sc;
             }
           } else {
@@ -876,10 +883,10 @@ __global__ void __launch_bounds__((NT + 1) * 32, CTAS)
 #pragma unroll
           for (int xi = 0; xi < (1 << PL::nx); ++xi)
 #pragma unroll
-            for (int e = 0; e < 8; ++e) a = nanmax(a, fabsf(d[xi][e] * s_res));
+            for (int e = 0; e < 8; ++e) a = absmax_nan(a, d[xi][e]);
 #pragma unroll
           for (int k = 0; k < RPT; ++k)
-            if (k == rl) amax_r[k] = nanmax(amax_r[k], a);
+            if (k == rl) amax_r[k] = absmax_nan(amax_r[k], a);
         }
 #pragma unroll
         for (int xi = 0; xi < (1 << PL::nx); ++xi) {
@@ -899,7 +906,7 @@ __global__ void __launch_bounds__((NT + 1) * 32, CTAS)
       // ---- fused quantization (NEXT-1): row max over the team, then codes + scales
 #pragma unroll
       for (int k = 0; k < RPT; ++k) {
-        const float a = warp_nanmax(amax_r[k]);
+        const float a = warp_absmax(amax_r[k]) * fabsf(s_res);
         if (lane == 0) red[(team * RPT + k) * P + wt] = a;
       }
       team_sync();
@@ -908,7 +915,7 @@ __global__ void __launch_bounds__((NT + 1) * 32, CTAS)
 #pragma unroll
       for (int k = 0; k < RPT; ++k) {
         float a = 0.f;
-        for (int w = 0; w < P; ++w) a = nanmax(a, red[(team * RPT + k) * P + w]);
+        for (int w = 0; w < P; ++w) a = absmax_nan(a, red[(team * RPT + k) * P + w]);
         float sc;
         row_scale_of<QT>(a, sc, inv_r[k]);
         const int r = team + NTEAMS * k;
