@@ -357,7 +357,9 @@ template <int QT>
 __device__ __forceinline__ void row_scale_of(float amax, float& scale, float& inv) {
   const bool pos = amax > 0.f;  // false for 0 and NaN
   scale = pos ? amax * (1.f / qmax_of<QT>()) : (amax == 0.f ? 1.f : amax);
-  inv = pos ? qmax_of<QT>() * __frcp_rn(amax) : (amax == 0.f ? 0.f : amax);
+  float r;
+  asm("rcp.approx.f32 %0, %1;" : "=f"(r) : "f"(amax));  // MUFU.RCP; codes tolerate its ~1 ulp
+  inv = pos ? qmax_of<QT>() * r : (amax == 0.f ? 0.f : amax);
 }
 
 __device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t r[4]) {
@@ -492,7 +494,7 @@ __global__ void __launch_bounds__((NT + 1) * 32, CTAS)
 #else
           stage_ca<DT>(A1, x[u][0], x[u][2], x[u][1], x[u][3], y[u]);
           stage_ca_f32<DT>(A2, y[u][0], y[u][1], y[u][2], y[u][3], d[u]);
-          scale_pack<DT>(d[u], s_res, z[u]);
+          if constexpr (QT < 0) scale_pack<DT>(d[u], s_res, z[u]);
 #endif
         }
 #pragma unroll
