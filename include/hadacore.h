@@ -14,7 +14,8 @@
  * n is a power of two in [2^7, 2^15] (the paper's range, P:97, P:128 [Sec. 3.2]).
  *
  * Layout: `in` and `out` are row-major m x n matrices of 16-bit floats (IEEE
- * binary16 or bfloat16), contiguous, row pitch = n elements, in DEVICE memory of
+ * binary16 or bfloat16; or binary32 for the HADACORE_F32 debug path), contiguous,
+ * row pitch = n elements, in DEVICE memory of
  * the current CUDA device, 16-byte aligned.  in == out (in-place, P:264-274
  * [App. B]) is allowed and gives bit-identical results to out-of-place.
  *
@@ -53,7 +54,8 @@ typedef struct CUstream_st* hadacore_stream_t;
 
 typedef enum {
   HADACORE_F16 = 0,  /* IEEE 754 binary16 */
-  HADACORE_BF16 = 1  /* bfloat16 */
+  HADACORE_BF16 = 1, /* bfloat16 */
+  HADACORE_F32 = 2   /* IEEE 754 binary32: debug/reference path (fp32 butterflies), not tuned */
 } hadacore_dtype_t;
 
 /* Code formats of the fused quantized output (hadacore_fwht_quant). */
@@ -65,7 +67,7 @@ typedef enum {
 typedef enum {
   HADACORE_OK = 0,
   HADACORE_ERR_INVALID_N = 1,   /* n is not a power of two in [128, 32768] */
-  HADACORE_ERR_INVALID_M = 2,   /* m < 0, or m * n * 2 overflows int64 */
+  HADACORE_ERR_INVALID_M = 2,   /* m < 0, or m * n * element size overflows int64 */
   HADACORE_ERR_NULL = 3,        /* in or out is NULL while m > 0 */
   HADACORE_ERR_MISALIGNED = 4,  /* in or out is not 16-byte aligned */
   HADACORE_ERR_OVERLAP = 5,     /* in != out and the two byte ranges overlap */
@@ -109,7 +111,7 @@ hadacore_status_t hadacore_fwht_host(const void* in_host, void* out_host, int64_
  * row_scale.  out_q: m x n bytes, row-major, 16-byte aligned; row_scale: m floats
  * (fp32).  Neither may overlap `in`.  HBM traffic: 2 B read + 1 B written per element.
  * Same validation, stream and error behaviour as hadacore_fwht; qtype outside the
- * enum returns HADACORE_ERR_DTYPE.
+ * enum, or dtype HADACORE_F32, returns HADACORE_ERR_DTYPE.
  */
 hadacore_status_t hadacore_fwht_quant(const void* in, void* out_q, float* row_scale, int64_t m, int64_t n,
                                       hadacore_dtype_t dtype, hadacore_qtype_t qtype, float scale,

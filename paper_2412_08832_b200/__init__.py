@@ -32,7 +32,7 @@ STATUS = {
     4: "HADACORE_ERR_MISALIGNED", 5: "HADACORE_ERR_OVERLAP", 6: "HADACORE_ERR_DTYPE",
     7: "HADACORE_ERR_SCALE", 8: "HADACORE_ERR_CUDA", 9: "HADACORE_ERR_WORKSPACE",
 }
-_DTYPES = {torch.float16: 0, torch.bfloat16: 1}
+_DTYPES = {torch.float16: 0, torch.bfloat16: 1, torch.float32: 2}  # float32 = debug path
 QTYPES = {"e4m3": (0, torch.float8_e4m3fn), "int8": (1, torch.int8)}
 
 
@@ -86,7 +86,7 @@ def launches_per_call(m: int, n: int) -> int:
 
 def _shape(x: torch.Tensor):
     if x.dtype not in _DTYPES:
-        raise HadacoreError(6, f"dtype {x.dtype} (expected float16 or bfloat16)")
+        raise HadacoreError(6, f"dtype {x.dtype} (expected float16, bfloat16 or float32)")
     if x.dim() < 1:
         raise HadacoreError(1, "need at least one dimension")
     n = x.shape[-1]
@@ -140,7 +140,8 @@ def hadacore_fwht_host(x: torch.Tensor, out: torch.Tensor | None = None, scale: 
         raise HadacoreError(3, "out must be a contiguous CPU tensor with x's shape and dtype")
     dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
     if workspace is None:
-        workspace = torch.empty(min(256 << 20, max(4 * n, 2 * m * n * 2)), dtype=torch.uint8, device=dev)
+        es = x.element_size()
+        workspace = torch.empty(min(256 << 20, max(2 * es * n, 2 * m * n * es)), dtype=torch.uint8, device=dev)
     if scale is None:
         scale = 1.0 / math.sqrt(n) if n > 0 else 1.0
     with torch.cuda.device(workspace.device):
@@ -163,6 +164,8 @@ def hadacore_fwht_quant(x: torch.Tensor, qtype: str = "e4m3", scale: float | Non
     if qtype not in QTYPES:
         raise HadacoreError(6, f"qtype {qtype!r} (expected one of {sorted(QTYPES)})")
     code, qdt = QTYPES[qtype]
+    if x.dtype == torch.float32:
+        raise HadacoreError(6, "the fused quantization takes float16/bfloat16 inputs")
     if not x.is_cuda or not x.is_contiguous():
         raise HadacoreError(8, "x must be a contiguous CUDA tensor")
     if out is None:

@@ -971,4 +971,40 @@ __global__ void __launch_bounds__((NT + 1) * 32, CTAS)
   }
 }
 
+// ------------------------------------------------------------------ fp32 debug path
+// HADACORE_F32 (north_star's "fp32 debug path", tolerance 1e-5): the P:50-64
+// butterflies in fp32 on a shared-memory copy of ROWS rows, one __syncthreads per
+// butterfly stage, scale applied once at the end (R3).  Correctness
+// reference for the 16-bit paths on the GPU, not a performance path.
+template <int N, int ROWS>
+__global__ void __launch_bounds__(512) fwht_f32_kernel(const float* __restrict__ in, float* __restrict__ out,
+                                                        int64_t m, float scale) {
+  extern __shared__ __align__(16) float srow[];
+  for (int64_t r0 = int64_t(blockIdx.x) * ROWS; r0 < m; r0 += int64_t(gridDim.x) * ROWS) {
+    const int rows = (m - r0) < ROWS ? int(m - r0) : ROWS;
+    for (int i = threadIdx.x; i < rows * N / 4; i += blockDim.x)
+      reinterpret_cast<float4*>(srow)[i] = reinterpret_cast<const float4*>(in + r0 * N)[i];
+    __syncthreads();
+    for (int h = 1; h < N; h *= 2) {
+      for (int idx = threadIdx.x; idx < rows * (N / 2); idx += blockDim.x) {
+        const int r = idx / (N / 2), p = idx % (N / 2);
+        const int j = r * N + (p / h) * (2 * h) + (p % h);
+        const float a = srow[j], b = srow[j + h];
+        srow[j] = a + b;
+        srow[j + h] = a - b;
+      }
+      __syncthreads();
+    }
+    for (int i = threadIdx.x; i < rows * N / 4; i += blockDim.x) {
+      float4 v = reinterpret_cast<float4*>(srow)[i];
+      v.x *= scale;
+      v.y *= scale;
+      v.z *= scale;
+      v.w *= scale;
+      reinterpret_cast<float4*>(out + r0 * N)[i] = v;
+    }
+    __syncthreads();
+  }
+}
+
 }  // namespace hadacore

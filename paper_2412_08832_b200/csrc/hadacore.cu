@@ -173,12 +173,45 @@ hadacore_status_t dispatch_n(const void* in, void* out, uint8_t* q, float* rs, i
 
 bool valid_n(int64_t n) { return n >= 128 && n <= 32768 && (n & (n - 1)) == 0; }
 
+size_t elem_size(int dtype) { return dtype == HADACORE_F32 ? 4 : 2; }
+
+template <int N>
+hadacore_status_t launch_f32(const void* in, void* out, int64_t m, float scale, cudaStream_t stream) {
+  constexpr int rows = N >= 4096 ? 1 : 4096 / N;  // >= 16 KiB of rows per CTA iteration
+  constexpr int smem = rows * N * 4;
+  static std::atomic<uint64_t> attr_done{0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return HADACORE_ERR_CUDA;
+  auto kern = fwht_f32_kernel<N, rows>;
+  if (!ensure_smem_attr(kern, smem, attr_done, dev)) return HADACORE_ERR_CUDA;
+  const int64_t groups = (m + rows - 1) / rows;
+  const int64_t cap = int64_t(sm_count(dev)) * 2;
+  kern<<<int(groups < cap ? groups : cap), 512, smem, stream>>>(static_cast<const float*>(in),
+                                                                static_cast<float*>(out), m, scale);
+  return cudaPeekAtLastError() == cudaSuccess ? HADACORE_OK : HADACORE_ERR_CUDA;
+}
+
+hadacore_status_t dispatch_f32(const void* in, void* out, int64_t m, int64_t n, float scale, cudaStream_t st) {
+  switch (n) {
+    case 128: return launch_f32<128>(in, out, m, scale, st);
+    case 256: return launch_f32<256>(in, out, m, scale, st);
+    case 512: return launch_f32<512>(in, out, m, scale, st);
+    case 1024: return launch_f32<1024>(in, out, m, scale, st);
+    case 2048: return launch_f32<2048>(in, out, m, scale, st);
+    case 4096: return launch_f32<4096>(in, out, m, scale, st);
+    case 8192: return launch_f32<8192>(in, out, m, scale, st);
+    case 16384: return launch_f32<16384>(in, out, m, scale, st);
+    case 32768: return launch_f32<32768>(in, out, m, scale, st);
+    default: return HADACORE_ERR_INVALID_N;
+  }
+}
+
 // Shared by both entry points: everything that can be checked without CUDA.
 hadacore_status_t validate(const void* in, const void* out, int64_t m, int64_t n, int dtype, float scale,
                            bool device_buffers) {
-  if (dtype != HADACORE_F16 && dtype != HADACORE_BF16) return HADACORE_ERR_DTYPE;
+  if (dtype != HADACORE_F16 && dtype != HADACORE_BF16 && dtype != HADACORE_F32) return HADACORE_ERR_DTYPE;
   if (!valid_n(n)) return HADACORE_ERR_INVALID_N;
-  if (m < 0 || m > INT64_MAX / (2 * n)) return HADACORE_ERR_INVALID_M;
+  if (m < 0 || m > INT64_MAX / (int64_t(elem_size(dtype)) * n)) return HADACORE_ERR_INVALID_M;
   if (!std::isfinite(scale)) return HADACORE_ERR_SCALE;
   if (m == 0) return HADACORE_OK;
   if (!in || !out) return HADACORE_ERR_NULL;
@@ -186,7 +219,7 @@ hadacore_status_t validate(const void* in, const void* out, int64_t m, int64_t n
     return HADACORE_ERR_MISALIGNED;
   if (in != out) {
     const uintptr_t a = reinterpret_cast<uintptr_t>(in), b = reinterpret_cast<uintptr_t>(out);
-    const uintptr_t bytes = uintptr_t(m) * uintptr_t(n) * 2u;
+    const uintptr_t bytes = uintptr_t(m) * uintptr_t(n) * elem_size(dtype);
     if (a < b + bytes && b < a + bytes) return HADACORE_ERR_OVERLAP;
   }
   return HADACORE_OK;
@@ -194,6 +227,7 @@ hadacore_status_t validate(const void* in, const void* out, int64_t m, int64_t n
 
 hadacore_status_t run(const void* in, void* out, int64_t m, int64_t n, int dtype, float scale,
                       cudaStream_t st) {
+  if (dtype == HADACORE_F32) return dispatch_f32(in, out, m, n, scale, st);
   return dtype == HADACORE_F16 ? dispatch_n<DT_F16, QT_NONE>(in, out, nullptr, nullptr, m, n, scale, st)
                                : dispatch_n<DT_BF16, QT_NONE>(in, out, nullptr, nullptr, m, n, scale, st);
 }
@@ -228,6 +262,7 @@ extern "C" hadacore_status_t hadacore_fwht_quant(const void* in, void* out_q, fl
                                                  int64_t n, hadacore_dtype_t dtype, hadacore_qtype_t qtype,
                                                  float scale, hadacore_stream_t stream) {
   if (qtype != HADACORE_Q_E4M3 && qtype != HADACORE_Q_INT8) return HADACORE_ERR_DTYPE;
+  if (dtype == HADACORE_F32) return HADACORE_ERR_DTYPE;  // the fused path takes 16-bit inputs
   // validate `in` (and m, n, dtype, scale) exactly like hadacore_fwht, with out = in
   const hadacore_status_t v = validate(in, in, m, n, int(dtype), scale, true);
   if (v != HADACORE_OK || m == 0) return v;
@@ -247,7 +282,7 @@ extern "C" hadacore_status_t hadacore_fwht_host(const void* in_host, void* out_h
                                                 size_t workspace_bytes, hadacore_stream_t stream) {
   const hadacore_status_t v = validate(in_host, out_host, m, n, int(dtype), scale, false);
   if (v != HADACORE_OK || m == 0) return v;
-  const size_t row_bytes = size_t(n) * 2;
+  const size_t row_bytes = size_t(n) * elem_size(int(dtype));
   if (!workspace || (reinterpret_cast<uintptr_t>(workspace) & 15u) || workspace_bytes < 2 * row_bytes)
     return HADACORE_ERR_WORKSPACE;
   // Two halves of the workspace, one internal stream each: block b goes through
@@ -303,7 +338,7 @@ extern "C" const char* hadacore_status_string(hadacore_status_t s) {
     case HADACORE_ERR_NULL: return "in/out must be non-NULL when m > 0";
     case HADACORE_ERR_MISALIGNED: return "in/out must be 16-byte aligned";
     case HADACORE_ERR_OVERLAP: return "in and out partially overlap (only in == out is allowed)";
-    case HADACORE_ERR_DTYPE: return "unknown dtype (expected HADACORE_F16 or HADACORE_BF16)";
+    case HADACORE_ERR_DTYPE: return "unsupported dtype / qtype for this entry point";
     case HADACORE_ERR_SCALE: return "scale must be finite";
     case HADACORE_ERR_CUDA: return "CUDA error (see cudaGetLastError)";
     case HADACORE_ERR_WORKSPACE: return "workspace NULL, misaligned or smaller than two rows";

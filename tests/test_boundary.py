@@ -65,7 +65,7 @@ def test_validation_codes(lib):
     assert call(lib, a, b, 4, 0) == INVALID_N
     assert call(lib, a, b, -1, 256) == INVALID_M
     assert call(lib, a, b, 1 << 62, 256) == INVALID_M
-    assert call(lib, a, b, 4, 256, dtype=2) == DTYPE
+    assert call(lib, a, b, 4, 256, dtype=3) == DTYPE
     assert call(lib, a, b, 4, 256, dtype=-1) == DTYPE
     assert call(lib, a, b, 4, 256, scale=float("nan")) == SCALE
     assert call(lib, a, b, 4, 256, scale=float("inf")) == SCALE
@@ -125,7 +125,7 @@ def test_python_binding_rejects_without_fallback():
     with pytest.raises(hc.HadacoreError):
         hc.hadacore_fwht(x)                    # CPU tensor: no CPU fallback
     with pytest.raises(hc.HadacoreError):
-        hc.hadacore_fwht(torch.zeros(4, 256, dtype=torch.float32))
+        hc.hadacore_fwht(torch.zeros(4, 256, dtype=torch.float64))
 
 
 def test_product_path_does_not_import_oracle():

@@ -20,8 +20,9 @@ pytestmark = pytest.mark.gpu
 NS = [1 << k for k in range(7, 16)]
 DTYPES = [torch.float16, torch.bfloat16]
 TOL = {torch.float16: 2e-3, torch.bfloat16: 1.6e-2}
-# rows per pipeline tile in the launch configuration (paper_2412_08832_b200/csrc/hadacore.cu Cfg<N>)
-TILE_ROWS = {128: 128, 256: 64, 512: 32, 1024: 16, 2048: 8, 4096: 4, 8192: 2, 16384: 1, 32768: 1}
+# rows per pipeline tile in the launch configuration (paper_2412_08832_b200/csrc/hadacore.cu Tuned<N>:
+# 16 KiB tiles of whole rows, one 64 KiB row for n = 2^15)
+TILE_ROWS = {128: 64, 256: 32, 512: 16, 1024: 8, 2048: 4, 4096: 2, 8192: 1, 16384: 1, 32768: 1}
 
 
 @pytest.fixture(scope="module")
@@ -205,3 +206,32 @@ def test_full_size_sampled(hc, n, dtype):
         ny = y[r0:r0 + blk].float().norm(dim=1)
         worst = max(worst, ((ny - nx).abs() / nx).max().item())
     assert worst <= TOL[dtype]
+
+
+# ---------------------------------------------------------------- fp32 debug path
+@pytest.mark.parametrize("n", NS)
+def test_fp32_debug_path(hc, n):
+    """HADACORE_F32 (north_star: fp32 debug path, max per-row rel-L2 <= 1e-5)."""
+    m = max(3, (1 << 18) // n) + 1
+    x = synthetic.generate(m, n, torch.float32, 21, dist="D1").cuda()
+    y = hc.hadacore_fwht(x)
+    err = rel_l2_rows(widen(y), oracle.fwht(widen(x)))
+    assert err.max() <= 1e-5, err.max()
+    # identity: +-1 times fp32(1/sqrt n), bitwise
+    rows = min(n, 64)
+    e = torch.zeros(rows, n, device="cuda")
+    e[torch.arange(rows), torch.arange(rows)] = 1.0
+    ye = hc.hadacore_fwht(e)
+    mag = torch.tensor(1.0 / math.sqrt(n), dtype=torch.float32)
+    j = torch.arange(n, dtype=torch.int64)
+    i = torch.arange(rows, dtype=torch.int64)[:, None]
+    a = i & j[None, :]
+    par = torch.zeros_like(a)
+    for b in range(15):
+        par ^= (a >> b) & 1
+    expect = torch.where(par == 1, -mag, mag)
+    assert torch.equal(ye.cpu(), expect)
+    # in place
+    xi = x.clone()
+    hc.hadacore_fwht(xi, out=xi)
+    assert torch.equal(xi, y)
