@@ -80,6 +80,11 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
+// Programmatic dependent launch: let the next kernel be scheduled early, and wait
+// for the previous kernel's completion (and memory flush) before touching memory.
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
@@ -436,9 +441,11 @@ __global__ void __launch_bounds__((NT + 1) * 32, CTAS)
   }
   __syncthreads();
 
+  pdl_launch_dependents();
   if (warp == NT) {
     // ---------------- producer: TMA bulk loads of row tiles into the ring
     if (lane == 0) {
+      pdl_wait();  // the previous kernel on the stream has completed; all our global traffic follows this
       const uint64_t pol = policy_evict_first();
       int it = 0;
       for (int64_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
@@ -709,11 +716,13 @@ __global__ void __launch_bounds__((NT + 1) * 32, CTAS)
   }
   __syncthreads();
 
+  pdl_launch_dependents();
   if (warp == NT) {
     // ---------------- producer: TMA tensor loads and stores of whole row tiles
     if (lane == 0) {
       tma_prefetch(&tm_in);
       tma_prefetch(&tm_out);
+      pdl_wait();  // the previous kernel on the stream has completed; all our global traffic follows this
       const uint64_t pol = policy_evict_first();
       auto load_tile = [&](int st, int64_t tile, auto wait_store_read) {
         mbar_arrive_expect_tx(&full[st], TILE_BYTES);  // full box, OOB rows zero-filled
@@ -980,6 +989,8 @@ template <int N, int ROWS>
 __global__ void __launch_bounds__(512) fwht_f32_kernel(const float* __restrict__ in, float* __restrict__ out,
                                                         int64_t m, float scale) {
   extern __shared__ __align__(16) float srow[];
+  pdl_launch_dependents();
+  pdl_wait();
   for (int64_t r0 = int64_t(blockIdx.x) * ROWS; r0 < m; r0 += int64_t(gridDim.x) * ROWS) {
     const int rows = (m - r0) < ROWS ? int(m - r0) : ROWS;
     for (int i = threadIdx.x; i < rows * N / 4; i += blockDim.x)

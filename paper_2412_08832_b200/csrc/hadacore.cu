@@ -109,6 +109,30 @@ bool encode_rows_map(CUtensorMap* map, const void* base, int64_t m, int n, int b
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// Launch with programmatic dependent launch (PDL): the grid may be scheduled while
+// the previous kernel on the stream drains, runs its prologue (barrier init, TMA
+// descriptor prefetch, constants) and waits in griddepcontrol.wait before its first
+// global-memory access -- so it is safe whatever the previous kernel wrote or read.
+#ifndef HC_NO_PDL
+constexpr bool kPdl = true;
+#else
+constexpr bool kPdl = false;
+#endif
+template <typename Kern, typename... Args>
+cudaError_t launch_pdl(Kern kern, int grid, int block, int smem, cudaStream_t stream, Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = size_t(smem);
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = kPdl ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
 template <typename Kern>
 bool ensure_smem_attr(Kern kern, int smem, std::atomic<uint64_t>& done, int dev) {
   const uint64_t bit = (dev >= 0 && dev < 64) ? (1ull << dev) : 0;
@@ -138,8 +162,9 @@ hadacore_status_t launch(const void* in, void* out, uint8_t* out_q, float* row_s
   if constexpr (N <= 256) {
     auto kern = fwht_kernel<N, DT, C::rows, C::stages, C::nt, C::p, C::u, C::ctas, QT>;
     if (!ensure_smem_attr(kern, smem, attr_done, dev)) return HADACORE_ERR_CUDA;
-    kern<<<grid, (C::nt + 1) * 32, smem, stream>>>(static_cast<const uint16_t*>(in), static_cast<uint16_t*>(out),
-                                                    out_q, row_scale, m, s_res);
+    if (launch_pdl(kern, grid, (C::nt + 1) * 32, smem, stream, static_cast<const uint16_t*>(in),
+                   static_cast<uint16_t*>(out), out_q, row_scale, m, s_res) != cudaSuccess)
+      return HADACORE_ERR_CUDA;
   } else {
     auto kern = fwht_rows_kernel<N, DT, C::rows, C::stages, C::nt, C::p, C::u, C::ctas, QT>;
     if (!ensure_smem_attr(kern, smem, attr_done, dev)) return HADACORE_ERR_CUDA;
@@ -148,8 +173,9 @@ hadacore_status_t launch(const void* in, void* out, uint8_t* out_q, float* row_s
     if (!encode_rows_map(&tin, in, m, N, box_rows, box_segs) ||
         !encode_rows_map(&tout, QT >= 0 ? in : out, m, N, box_rows, box_segs))  // unused when quantizing
       return HADACORE_ERR_CUDA;
-    kern<<<grid, (C::nt + 1) * 32, smem, stream>>>(tin, tout, static_cast<uint16_t*>(out), out_q, row_scale, m,
-                                                    s_res);
+    if (launch_pdl(kern, grid, (C::nt + 1) * 32, smem, stream, tin, tout, static_cast<uint16_t*>(out), out_q,
+                   row_scale, m, s_res) != cudaSuccess)
+      return HADACORE_ERR_CUDA;
   }
   return cudaPeekAtLastError() == cudaSuccess ? HADACORE_OK : HADACORE_ERR_CUDA;
 }
@@ -186,8 +212,9 @@ hadacore_status_t launch_f32(const void* in, void* out, int64_t m, float scale, 
   if (!ensure_smem_attr(kern, smem, attr_done, dev)) return HADACORE_ERR_CUDA;
   const int64_t groups = (m + rows - 1) / rows;
   const int64_t cap = int64_t(sm_count(dev)) * 2;
-  kern<<<int(groups < cap ? groups : cap), 512, smem, stream>>>(static_cast<const float*>(in),
-                                                                static_cast<float*>(out), m, scale);
+  if (launch_pdl(kern, int(groups < cap ? groups : cap), 512, smem, stream, static_cast<const float*>(in),
+                 static_cast<float*>(out), m, scale) != cudaSuccess)
+    return HADACORE_ERR_CUDA;
   return cudaPeekAtLastError() == cudaSuccess ? HADACORE_OK : HADACORE_ERR_CUDA;
 }
 
