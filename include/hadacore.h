@@ -86,9 +86,10 @@ hadacore_status_t hadacore_fwht(const void* in, void* out, int64_t m, int64_t n,
 
 /*
  * End-to-end variant on HOST buffers (the call a host-side user makes): copies row
- * blocks host->device into `workspace`, transforms them in place with the same
- * kernel, and copies them device->host into `out_host`, pipelined over two halves
- * of the workspace so the copies overlap the kernels.  Returns after the last
+ * blocks (<= 16 MiB) host->device into `workspace`, transforms them in place with the
+ * same kernel, and copies them device->host into `out_host`, pipelined over up to
+ * four workspace slots and internal streams so both copy directions overlap the
+ * kernels.  Returns after the last
  * device->host copy has completed (synchronises `stream`).
  *   in_host / out_host: m x n row-major 16-bit matrices in host memory (pinned
  *     memory gives full PCIe bandwidth; pageable works but is slower).  May be equal.

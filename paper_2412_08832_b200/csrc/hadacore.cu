@@ -312,43 +312,51 @@ extern "C" hadacore_status_t hadacore_fwht_host(const void* in_host, void* out_h
   const size_t row_bytes = size_t(n) * elem_size(int(dtype));
   if (!workspace || (reinterpret_cast<uintptr_t>(workspace) & 15u) || workspace_bytes < 2 * row_bytes)
     return HADACORE_ERR_WORKSPACE;
-  // Two halves of the workspace, one internal stream each: block b goes through
-  // H2D -> kernel (in place) -> D2H on stream b&1, so consecutive blocks overlap
-  // their copies (both PCIe directions) with each other's kernels.
-  const int64_t rows_per_half = int64_t((workspace_bytes / 2) / row_bytes);
+  // The workspace is cut into NS slots of at most kBlockBytes, one internal stream
+  // each; block b goes H2D -> kernel (in place) -> D2H on stream b % NS.  Small blocks
+  // and several streams keep both PCIe directions busy (short pipeline fill/drain).
+  constexpr size_t kBlockBytes = size_t(16) << 20;
+  constexpr int kMaxSlots = 4;
+  int slots = int(workspace_bytes / row_bytes >= kMaxSlots ? kMaxSlots : 2);
+  int64_t rows_per_slot = int64_t((workspace_bytes / size_t(slots)) / row_bytes);
+  const int64_t cap_rows = int64_t(kBlockBytes / row_bytes) > 0 ? int64_t(kBlockBytes / row_bytes) : 1;
+  if (rows_per_slot > cap_rows) rows_per_slot = cap_rows;
+  if (rows_per_slot < 1) {
+    slots = 1;
+    rows_per_slot = 1;
+  }
   cudaStream_t user = reinterpret_cast<cudaStream_t>(stream);
-  cudaStream_t st[2] = {nullptr, nullptr};
+  cudaStream_t st[kMaxSlots] = {nullptr, nullptr, nullptr, nullptr};
   cudaEvent_t ev = nullptr;
   hadacore_status_t rc = HADACORE_OK;
-  if (cudaStreamCreateWithFlags(&st[0], cudaStreamNonBlocking) != cudaSuccess ||
-      cudaStreamCreateWithFlags(&st[1], cudaStreamNonBlocking) != cudaSuccess ||
-      cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess) {
+  for (int i = 0; i < slots && rc == HADACORE_OK; ++i)
+    if (cudaStreamCreateWithFlags(&st[i], cudaStreamNonBlocking) != cudaSuccess) rc = HADACORE_ERR_CUDA;
+  if (rc == HADACORE_OK && cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess)
     rc = HADACORE_ERR_CUDA;
-  }
   if (rc == HADACORE_OK) {
     // order after everything already queued on the caller's stream
-    if (cudaEventRecord(ev, user) != cudaSuccess || cudaStreamWaitEvent(st[0], ev, 0) != cudaSuccess ||
-        cudaStreamWaitEvent(st[1], ev, 0) != cudaSuccess)
-      rc = HADACORE_ERR_CUDA;
+    if (cudaEventRecord(ev, user) != cudaSuccess) rc = HADACORE_ERR_CUDA;
+    for (int i = 0; i < slots && rc == HADACORE_OK; ++i)
+      if (cudaStreamWaitEvent(st[i], ev, 0) != cudaSuccess) rc = HADACORE_ERR_CUDA;
   }
   const uint8_t* src = static_cast<const uint8_t*>(in_host);
   uint8_t* dst = static_cast<uint8_t*>(out_host);
   int64_t b = 0;
-  for (int64_t r0 = 0; rc == HADACORE_OK && r0 < m; r0 += rows_per_half, ++b) {
-    const int64_t rows = (m - r0) < rows_per_half ? (m - r0) : rows_per_half;
+  for (int64_t r0 = 0; rc == HADACORE_OK && r0 < m; r0 += rows_per_slot, ++b) {
+    const int64_t rows = (m - r0) < rows_per_slot ? (m - r0) : rows_per_slot;
     const size_t bytes = size_t(rows) * row_bytes;
-    uint8_t* ws = static_cast<uint8_t*>(workspace) + size_t(b & 1) * size_t(rows_per_half) * row_bytes;
-    cudaStream_t s = st[b & 1];
-    if (cudaMemcpyAsync(ws, src + size_t(r0) * row_bytes, bytes, cudaMemcpyHostToDevice, s) != cudaSuccess) {
+    const int k = int(b % slots);
+    uint8_t* ws = static_cast<uint8_t*>(workspace) + size_t(k) * size_t(rows_per_slot) * row_bytes;
+    if (cudaMemcpyAsync(ws, src + size_t(r0) * row_bytes, bytes, cudaMemcpyHostToDevice, st[k]) != cudaSuccess) {
       rc = HADACORE_ERR_CUDA;
       break;
     }
-    rc = run(ws, ws, rows, n, int(dtype), scale, s);
+    rc = run(ws, ws, rows, n, int(dtype), scale, st[k]);
     if (rc != HADACORE_OK) break;
-    if (cudaMemcpyAsync(dst + size_t(r0) * row_bytes, ws, bytes, cudaMemcpyDeviceToHost, s) != cudaSuccess)
+    if (cudaMemcpyAsync(dst + size_t(r0) * row_bytes, ws, bytes, cudaMemcpyDeviceToHost, st[k]) != cudaSuccess)
       rc = HADACORE_ERR_CUDA;
   }
-  for (int i = 0; i < 2; ++i)
+  for (int i = 0; i < slots; ++i)
     if (st[i]) {
       if (cudaStreamSynchronize(st[i]) != cudaSuccess) rc = HADACORE_ERR_CUDA;
       cudaStreamDestroy(st[i]);
