@@ -80,6 +80,22 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
+// HC_TRACE builds (tools/trace_pipeline.py): %globaltimer stamps of pipeline events of
+// the first CTAs, read back with hadacore_trace_read().
+#ifdef HC_TRACE
+constexpr int kTraceCtas = 4, kTraceTiles = 48, kTraceEv = 8;
+__device__ uint64_t g_trace[kTraceCtas][kTraceTiles][kTraceEv];
+__device__ __forceinline__ void trace(int it, int ev) {
+  if (blockIdx.x < kTraceCtas && it < kTraceTiles) {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_trace[blockIdx.x][it][ev] = t;
+  }
+}
+#else
+__device__ __forceinline__ void trace(int, int) {}
+#endif
+
 // Programmatic dependent launch: let the next kernel be scheduled early, and wait
 // for the previous kernel's completion (and memory flush) before touching memory.
 __device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
@@ -744,6 +760,7 @@ __global__ void __launch_bounds__((NT + 1) * 32, CTAS)
       for (int k = 0; k < STAGES; ++k) {
         const int64_t tile = blockIdx.x + int64_t(k) * gridDim.x;
         if (tile >= num_tiles) break;
+        trace(k, 0);
         load_tile(k, tile, no_wait);
       }
       int it = 0;
@@ -753,6 +770,7 @@ __global__ void __launch_bounds__((NT + 1) * 32, CTAS)
 #pragma unroll
         for (int g = 0; g < NSEG; ++g) {
           mbar_wait(&done[s * NSEG + g], ph);
+          if (g == 0) trace(it, 1);
           if constexpr (STG_OUT) continue;
           if constexpr (SEG) {
             tma_store_4d(&tm_out, 0, 0, g % 4, int(tile * TILE_ROWS) + g / 4,
@@ -762,6 +780,7 @@ __global__ void __launch_bounds__((NT + 1) * 32, CTAS)
           }
           bulk_commit();
         }
+        trace(it, 2);
         const int64_t next = tile + int64_t(STAGES) * gridDim.x;
         if (next < num_tiles) {
           if constexpr (STG_OUT) {
@@ -769,6 +788,7 @@ __global__ void __launch_bounds__((NT + 1) * 32, CTAS)
           } else {
             load_tile(s, next, wait_reads);
           }
+          trace(it + STAGES, 0);
         }
       }
       bulk_wait_all();
@@ -812,6 +832,7 @@ __global__ void __launch_bounds__((NT + 1) * 32, CTAS)
   for (int64_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
     const int s = it % STAGES;
     mbar_wait(&full[s], (it / STAGES) & 1);
+    if (warp == 0 && lane == 0) trace(it, 4);
     uint8_t* const tb = smem + s * TILE_BYTES;
 
     // ---- phase 1: H_256 on every 256-chunk, in place
@@ -837,6 +858,7 @@ __global__ void __launch_bounds__((NT + 1) * 32, CTAS)
       for (int u = 0; u < U1; ++u) stg_sh128(p[u], z[u]);
     }
     team_sync();  // P:126 "Sync across the threadblock"
+    if (warp == 0 && lane == 0) trace(it, 5);
 
     // ---- phase 2: H_{n/256} across chunks (residual 2^a factor)
     float amax_r[RPT];  // fused quantization: running max |y| of each of the team's rows
@@ -977,6 +999,7 @@ __global__ void __launch_bounds__((NT + 1) * 32, CTAS)
       __syncwarp();
       if (lane == 0) mbar_arrive(&done[s]);
     }
+    if (warp == 0 && lane == 0) trace(it, 6);
   }
 }
 

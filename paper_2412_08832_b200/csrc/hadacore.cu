@@ -383,6 +383,12 @@ extern "C" const char* hadacore_status_string(hadacore_status_t s) {
 
 extern "C" int hadacore_version(void) { return kVersion; }
 
+#ifdef HC_TRACE
+extern "C" int hadacore_trace_read(void* host, size_t bytes) {
+  return cudaMemcpyFromSymbol(host, g_trace, bytes < sizeof(g_trace) ? bytes : sizeof(g_trace)) == cudaSuccess ? 0 : 1;
+}
+#endif
+
 extern "C" int hadacore_launches_per_call(int64_t m, int64_t n) {
   return (m > 0 && valid_n(n)) ? 1 : 0;
 }

@@ -26,7 +26,8 @@ def build_one(spec):
         name = spec.replace("-", "_")
         extra = (["-DHC_NOCOMPUTE"] if "nocompute" in spec else []) + (["-DHC_SIMT"] if "simt" in spec else []) + \
             (["-DHC_SEG"] if "-seg" in spec else []) + (["-DHC_STG_OUT"] if "stgout" in spec else []) + \
-            (["-DHC_NO_PDL"] if "nopdl" in spec else [])
+            (["-DHC_NO_PDL"] if "nopdl" in spec else []) + \
+            (["-DHC_TRACE"] if "trace" in spec else [])
     else:
         nt, tkb, st, u, ctas = (spec.split(",") + ["1"])[:5]
         name = f"nt{nt}_t{tkb}_s{st}_u{u}_c{ctas}"
