@@ -85,6 +85,12 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 #ifdef HC_TRACE
 constexpr int kTraceCtas = 4, kTraceTiles = 48, kTraceEv = 8;
 __device__ uint64_t g_trace[kTraceCtas][kTraceTiles][kTraceEv];
+__device__ uint64_t g_span[1024][3];  // per CTA: first load issued, last tile done (warp 0), tiles done
+__device__ __forceinline__ uint64_t gtime() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 __device__ __forceinline__ void trace(int it, int ev) {
   if (blockIdx.x < kTraceCtas && it < kTraceTiles) {
     uint64_t t;
@@ -100,6 +106,63 @@ __device__ __forceinline__ void trace(int, int) {}
 // for the previous kernel's completion (and memory flush) before touching memory.
 __device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+// ---- tile scheduling.  Default: Blackwell cluster launch control (CLC).  The grid has
+// one CTA per tile; a running CTA's producer cancels a not-yet-launched CTA with
+// clusterlaunchcontrol.try_cancel and processes its tile instead, so fast SMs take
+// more tiles than slow ones (static round-robin leaves the grid waiting for the
+// slowest SMs: profiles/r01_pipeline_trace_*).  HC_STATIC_SCHED = persistent grid
+// with static round-robin tiles, for A/B.
+#ifdef HC_STATIC_SCHED
+constexpr bool kClc = false;
+#else
+constexpr bool kClc = true;
+#endif
+// Control block at the start of the barrier area: CLC response (16 B), its mbarrier,
+// and the tile id of every ring stage (-1 = no more tiles).
+struct SchedCtl {
+  uint4 clc_resp;
+  uint64_t clc_bar;
+  uint64_t pad;
+  int stage_tile[16];
+};
+static_assert(sizeof(SchedCtl) == 96, "SchedCtl layout");
+
+__device__ __forceinline__ void clc_request(SchedCtl* ctl) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], 16;" ::"r"(smem_addr(&ctl->clc_bar)) : "memory");
+  asm volatile("clusterlaunchcontrol.try_cancel.async.shared::cta.mbarrier::complete_tx::bytes.b128 [%0], [%1];" ::"r"(
+                   smem_addr(&ctl->clc_resp)),
+               "r"(smem_addr(&ctl->clc_bar))
+               : "memory");
+}
+// Waits for the pending request; returns the cancelled CTA's blockIdx.x, or -1 when
+// every remaining CTA is already running (then no further request may be made).
+__device__ __forceinline__ int64_t clc_result(SchedCtl* ctl, uint32_t& phase) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAITC_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAITC_%=;\n}" ::"r"(smem_addr(&ctl->clc_bar)),
+      "r"(phase)
+      : "memory");
+  phase ^= 1u;
+  uint4 r;
+  asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "r"(smem_addr(&ctl->clc_resp))
+               : "memory");
+  uint32_t ok, x;
+  asm volatile(
+      "{\n\t.reg .b128 R;\n\t.reg .pred P;\n\t"
+      "mov.b128 R, {%2, %3};\n\t"
+      "clusterlaunchcontrol.query_cancel.is_canceled.pred.b128 P, R;\n\t"
+      "selp.b32 %0, 1, 0, P;\n\t"
+      "clusterlaunchcontrol.query_cancel.get_first_ctaid::x.b32.b128 %1, R;\n\t}"
+      : "=r"(ok), "=r"(x)
+      : "l"((uint64_t(r.y) << 32) | r.x), "l"((uint64_t(r.w) << 32) | r.z)
+      : "memory");
+  return ok ? int64_t(x) : -1;
+}
 
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -441,12 +504,15 @@ __global__ void __launch_bounds__((NT + 1) * 32, CTAS)
   constexpr int TILE_BYTES = TILE_ROWS * ROW_BYTES;
   static_assert(TILE_BYTES % 16 == 0, "bulk copy granularity");
   extern __shared__ __align__(1024) uint8_t smem[];
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * TILE_BYTES);
+  SchedCtl* ctl = reinterpret_cast<SchedCtl*>(smem + STAGES * TILE_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * TILE_BYTES + sizeof(SchedCtl));
   uint64_t* empty = full + STAGES;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t num_tiles = (m + TILE_ROWS - 1) / TILE_ROWS;
+  static_assert(STAGES <= 16, "SchedCtl holds 16 stages");
 
   if (threadIdx.x == 0) {
+    mbar_init(&ctl->clc_bar, 1);
 #pragma unroll
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
@@ -463,17 +529,30 @@ __global__ void __launch_bounds__((NT + 1) * 32, CTAS)
     if (lane == 0) {
       pdl_wait();  // the previous kernel on the stream has completed; all our global traffic follows this
       const uint64_t pol = policy_evict_first();
-      int it = 0;
-      for (int64_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+      uint32_t clc_phase = 0;
+      int64_t tile = blockIdx.x;
+      for (int it = 0;; ++it) {
         const int s = it % STAGES;
         const uint32_t ph = (it / STAGES) & 1;
         mbar_wait(&empty[s], ph ^ 1);
+        if (tile < 0 || tile >= num_tiles) {  // no more tiles: tell the consumers
+          ctl->stage_tile[s] = -1;
+          mbar_arrive(&full[s]);
+          break;
+        }
+        ctl->stage_tile[s] = int(tile);
+        if constexpr (kClc) clc_request(ctl);  // ask for the next tile while this one loads
         const int64_t row0 = tile * TILE_ROWS;
         const int64_t rem = m - row0;
         const int rows = rem < TILE_ROWS ? int(rem) : TILE_ROWS;
         const uint32_t bytes = uint32_t(rows) * ROW_BYTES;
         mbar_arrive_expect_tx(&full[s], bytes);
         bulk_g2s(smem + s * TILE_BYTES, in + row0 * N, bytes, &full[s], pol);
+        if constexpr (kClc) {
+          tile = clc_result(ctl, clc_phase);
+        } else {
+          tile += gridDim.x;
+        }
       }
     }
     return;
@@ -487,9 +566,11 @@ __global__ void __launch_bounds__((NT + 1) * 32, CTAS)
     make_const_a<DT>(0x7u, A2);  // H_8 over bits {4,5,6} (x) I_2 (bit 1, same row)
     constexpr int FR = TILE_ROWS / 2;  // fragments (row pairs) per tile
     static_assert(FR % (NT * U) == 0, "n=128 work split");
-    for (int64_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+    for (;; ++it) {
       const int s = it % STAGES;
       mbar_wait(&full[s], (it / STAGES) & 1);
+      const int64_t tile = ctl->stage_tile[s];
+      if (tile < 0) break;
       const int64_t row0 = tile * TILE_ROWS;
       const int rows = (m - row0) < TILE_ROWS ? int(m - row0) : TILE_ROWS;
       const uint8_t* tb = smem + s * TILE_BYTES;
@@ -554,9 +635,11 @@ __global__ void __launch_bounds__((NT + 1) * 32, CTAS)
     uint32_t A1[4];
     make_const_a<DT>(0xFu, A1);
     static_assert(TILE_ROWS % (NT * U) == 0, "n=256 work split");
-    for (int64_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+    for (;; ++it) {
       const int s = it % STAGES;
       mbar_wait(&full[s], (it / STAGES) & 1);
+      const int64_t tile = ctl->stage_tile[s];
+      if (tile < 0) break;
       const int64_t row0 = tile * TILE_ROWS;
       const int rows = (m - row0) < TILE_ROWS ? int(m - row0) : TILE_ROWS;
       const uint8_t* tb = smem + s * TILE_BYTES;
@@ -714,13 +797,16 @@ __global__ void __launch_bounds__((NT + 1) * 32, CTAS)
   constexpr int SEG_BYTES = ROW_BYTES / 4;
 
   extern __shared__ __align__(1024) uint8_t smem[];
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * TILE_BYTES);
+  SchedCtl* ctl = reinterpret_cast<SchedCtl*>(smem + STAGES * TILE_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * TILE_BYTES + sizeof(SchedCtl));
   uint64_t* done = full + STAGES;  // [STAGES][NSEG] consumers -> producer: ready to store
-  float* red = reinterpret_cast<float*>(smem + STAGES * TILE_BYTES + 17 * STAGES * 8);  // [NTEAMS][RPT][P] row max
+  float* red = reinterpret_cast<float*>(smem + STAGES * TILE_BYTES + sizeof(SchedCtl) + 17 * STAGES * 8);
+  static_assert(STAGES <= 16, "SchedCtl holds 16 stages");
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t num_tiles = (m + TILE_ROWS - 1) / TILE_ROWS;
 
   if (threadIdx.x == 0) {
+    mbar_init(&ctl->clc_bar, 1);
 #pragma unroll
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
@@ -739,6 +825,9 @@ __global__ void __launch_bounds__((NT + 1) * 32, CTAS)
       tma_prefetch(&tm_in);
       tma_prefetch(&tm_out);
       pdl_wait();  // the previous kernel on the stream has completed; all our global traffic follows this
+#ifdef HC_TRACE
+      g_span[blockIdx.x][0] = gtime();
+#endif
       const uint64_t pol = policy_evict_first();
       auto load_tile = [&](int st, int64_t tile, auto wait_store_read) {
         mbar_arrive_expect_tx(&full[st], TILE_BYTES);  // full box, OOB rows zero-filled
@@ -757,39 +846,64 @@ __global__ void __launch_bounds__((NT + 1) * 32, CTAS)
       // stores to have read the stage
       auto no_wait = [](int) { return std::false_type{}; };
       auto wait_reads = [](int) { return std::true_type{}; };
-      for (int k = 0; k < STAGES; ++k) {
-        const int64_t tile = blockIdx.x + int64_t(k) * gridDim.x;
-        if (tile >= num_tiles) break;
+      uint32_t clc_phase = 0;
+      int64_t tile = blockIdx.x;  // the next tile to load
+      auto advance = [&](int64_t t) -> int64_t {
+        if constexpr (kClc) {
+          return clc_result(ctl, clc_phase);
+        } else {
+          return t + gridDim.x;
+        }
+      };
+      bool ended = false;
+      for (int k = 0; k < STAGES && !ended; ++k) {  // fill the ring
+        if (tile < 0 || tile >= num_tiles) {
+          ctl->stage_tile[k] = -1;
+          mbar_arrive(&full[k]);
+          ended = true;
+          break;
+        }
+        ctl->stage_tile[k] = int(tile);
+        if constexpr (kClc) clc_request(ctl);
         trace(k, 0);
         load_tile(k, tile, no_wait);
+        tile = advance(tile);
       }
-      int it = 0;
-      for (int64_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+      for (int it = 0;; ++it) {
         const int s = it % STAGES;
         const uint32_t ph = (it / STAGES) & 1;
+        const int64_t t = ctl->stage_tile[s];
+        if (t < 0) break;
 #pragma unroll
         for (int g = 0; g < NSEG; ++g) {
           mbar_wait(&done[s * NSEG + g], ph);
           if (g == 0) trace(it, 1);
           if constexpr (STG_OUT) continue;
           if constexpr (SEG) {
-            tma_store_4d(&tm_out, 0, 0, g % 4, int(tile * TILE_ROWS) + g / 4,
+            tma_store_4d(&tm_out, 0, 0, g % 4, int(t * TILE_ROWS) + g / 4,
                          smem + s * TILE_BYTES + (g / 4) * ROW_BYTES + (g % 4) * SEG_BYTES);
           } else {
-            tma_store_4d(&tm_out, 0, 0, 0, int(tile * TILE_ROWS), smem + s * TILE_BYTES);  // OOB rows clipped
+            tma_store_4d(&tm_out, 0, 0, 0, int(t * TILE_ROWS), smem + s * TILE_BYTES);  // OOB rows clipped
           }
           bulk_commit();
         }
         trace(it, 2);
-        const int64_t next = tile + int64_t(STAGES) * gridDim.x;
-        if (next < num_tiles) {
-          if constexpr (STG_OUT) {
-            load_tile(s, next, no_wait);
-          } else {
-            load_tile(s, next, wait_reads);
-          }
-          trace(it + STAGES, 0);
+        if (ended) continue;
+        if (tile < 0 || tile >= num_tiles) {  // no more tiles: tell the consumers
+          ctl->stage_tile[s] = -1;
+          mbar_arrive(&full[s]);
+          ended = true;
+          continue;
         }
+        ctl->stage_tile[s] = int(tile);
+        if constexpr (kClc) clc_request(ctl);
+        if constexpr (STG_OUT) {
+          load_tile(s, tile, no_wait);
+        } else {
+          load_tile(s, tile, wait_reads);
+        }
+        trace(it + STAGES, 0);
+        tile = advance(tile);
       }
       bulk_wait_all();
     }
@@ -829,9 +943,11 @@ __global__ void __launch_bounds__((NT + 1) * 32, CTAS)
   };
 
   int it = 0;
-  for (int64_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+  for (;; ++it) {
     const int s = it % STAGES;
     mbar_wait(&full[s], (it / STAGES) & 1);
+    const int64_t tile = ctl->stage_tile[s];
+    if (tile < 0) break;
     if (warp == 0 && lane == 0) trace(it, 4);
     uint8_t* const tb = smem + s * TILE_BYTES;
 
@@ -1001,6 +1117,12 @@ __global__ void __launch_bounds__((NT + 1) * 32, CTAS)
     }
     if (warp == 0 && lane == 0) trace(it, 6);
   }
+#ifdef HC_TRACE
+  if (warp == 0 && lane == 0) {
+    g_span[blockIdx.x][1] = gtime();
+    g_span[blockIdx.x][2] = it;
+  }
+#endif
 }
 
 // ------------------------------------------------------------------ fp32 debug path

@@ -69,7 +69,7 @@ struct Cfg {
   static constexpr int tile_bytes = rows * 2 * N;
   // more CTAs per SM only if each can still hold a double-buffered ring
   static constexpr int ctas = ((227 * 1024 / K::ctas - 256) / tile_bytes) >= 2 ? K::ctas : 1;
-  static constexpr int max_stages = (227 * 1024 / ctas - 1280) / tile_bytes;
+  static constexpr int max_stages = (227 * 1024 / ctas - 1408) / tile_bytes;
   static constexpr int stages = K::st < max_stages ? K::st : max_stages;
   static constexpr int nteams = N <= 256 ? 1 : (rows < nt ? rows : nt);
   static constexpr int p = N <= 256 ? 1 : nt / nteams;
@@ -149,12 +149,15 @@ hadacore_status_t launch(const void* in, void* out, uint8_t* out_q, float* row_s
   // SEG mode (n >= 8192): each (row, 128-byte-line segment) is its own TMA box
   constexpr int box_segs = seg_mode(N, C::rows) ? 1 : 4;
   // + full[], done[][<=16] and the fused-quantization row-max scratch (one float per warp)
-  constexpr int smem = C::stages * C::tile_bytes + 17 * C::stages * 8 + 4 * C::nt * (N > 256 ? C::rows : 1);
+  constexpr int smem = C::stages * C::tile_bytes + int(sizeof(SchedCtl)) + 17 * C::stages * 8 +
+                       4 * C::nt * (N > 256 ? C::rows : 1);
   static std::atomic<uint64_t> attr_done{0};
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return HADACORE_ERR_CUDA;
+  // CLC scheduling (default): one CTA per tile, resident CTAs steal the rest;
+  // HC_STATIC_SCHED: persistent grid of one CTA per SM with round-robin tiles
   const int64_t tiles = (m + C::rows - 1) / C::rows;
-  const int64_t max_ctas = int64_t(sm_count(dev)) * C::ctas;  // persistent CTAs
+  const int64_t max_ctas = kClc ? int64_t(INT32_MAX) : int64_t(sm_count(dev)) * C::ctas;
   const int grid = int(tiles < max_ctas ? tiles : max_ctas);
   // the per-stage constants multiply by exact powers of two 2^-E; fold the rest of
   // `scale` into the fp32 epilogue of the last stage.
@@ -386,6 +389,9 @@ extern "C" int hadacore_version(void) { return kVersion; }
 #ifdef HC_TRACE
 extern "C" int hadacore_trace_read(void* host, size_t bytes) {
   return cudaMemcpyFromSymbol(host, g_trace, bytes < sizeof(g_trace) ? bytes : sizeof(g_trace)) == cudaSuccess ? 0 : 1;
+}
+extern "C" int hadacore_span_read(void* host, size_t bytes) {
+  return cudaMemcpyFromSymbol(host, g_span, bytes < sizeof(g_span) ? bytes : sizeof(g_span)) == cudaSuccess ? 0 : 1;
 }
 #endif
 

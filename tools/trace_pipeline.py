@@ -31,3 +31,17 @@ for cta in range(2):
     ld = d[:, 0].astype(np.int64)
     print(f"  median: load->full {np.median(full - ld)/1000:.2f} us, full->p1 {np.median(p1 - full)/1000:.2f}, "
           f"p1->p2 {np.median(p2 - p1)/1000:.2f}, tile period {np.median(np.diff(full))/1000:.2f} us")
+
+span = np.zeros((1024, 3), dtype=np.uint64)
+assert lib.hadacore_span_read(span.ctypes.data, span.nbytes) == 0
+grid = int((span[:, 1] > 0).sum())
+t0 = span[:grid, 0].astype(np.int64).min()
+start = (span[:grid, 0].astype(np.int64) - t0) / 1000
+end = (span[:grid, 1].astype(np.int64) - t0) / 1000
+tiles = span[:grid, 2].astype(np.int64)
+per = (end - start) / tiles
+print(f"CTAs {grid}: start max {start.max():.2f} us; end min {end.min():.1f} median {np.median(end):.1f} max {end.max():.1f} us; "
+      f"tiles {tiles.min()}..{tiles.max()}; us/tile min {per.min():.2f} median {np.median(per):.2f} max {per.max():.2f}")
+order = np.argsort(per)
+print("slowest CTAs:", [(int(i), round(float(per[i]), 2)) for i in order[-8:]])
+print("fastest CTAs:", [(int(i), round(float(per[i]), 2)) for i in order[:8]])

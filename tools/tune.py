@@ -27,7 +27,8 @@ def build_one(spec):
         extra = (["-DHC_NOCOMPUTE"] if "nocompute" in spec else []) + (["-DHC_SIMT"] if "simt" in spec else []) + \
             (["-DHC_SEG"] if "-seg" in spec else []) + (["-DHC_STG_OUT"] if "stgout" in spec else []) + \
             (["-DHC_NO_PDL"] if "nopdl" in spec else []) + \
-            (["-DHC_TRACE"] if "trace" in spec else [])
+            (["-DHC_TRACE"] if "trace" in spec else []) + \
+            (["-DHC_STATIC_SCHED"] if "static" in spec else [])
     else:
         nt, tkb, st, u, ctas = (spec.split(",") + ["1"])[:5]
         name = f"nt{nt}_t{tkb}_s{st}_u{u}_c{ctas}"
