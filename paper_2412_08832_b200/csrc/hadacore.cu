@@ -39,8 +39,8 @@ int sm_count(int dev) {
 // ~TILE_KB KiB (whole rows; one 64 KiB row for n = 2^15), rows split into teams of
 // P warps (n > 256) that synchronise with named barriers.  The HC_* macros let
 // tools/tune.py build variants; the defaults are the tuned values.
-// Tuned per n on B200 in bench.py's launch sequence (paired sweeps,
-// profiles/r01_tune_sweep13_bench_sequence.txt): compute warps, tile KiB, ring
+// Tuned per n on B200 in bench.py's launch sequence under CLC scheduling (paired
+// sweeps, profiles/r01_tune_sweep16_clc_retune.txt): compute warps, tile KiB, ring
 // stages, work items per warp in flight, CTAs per SM.
 template <int N> struct Tuned;
 template <> struct Tuned<128>   { static constexpr int nt = 16, tkb = 16, st = 4, u = 1, ctas = 1; };
@@ -50,8 +50,8 @@ template <> struct Tuned<1024>  { static constexpr int nt = 16, tkb = 16, st = 4
 template <> struct Tuned<2048>  { static constexpr int nt = 16, tkb = 16, st = 4, u = 1, ctas = 1; };
 template <> struct Tuned<4096>  { static constexpr int nt = 16, tkb = 16, st = 4, u = 1, ctas = 1; };
 template <> struct Tuned<8192>  { static constexpr int nt = 16, tkb = 16, st = 6, u = 1, ctas = 1; };
-template <> struct Tuned<16384> { static constexpr int nt = 16, tkb = 16, st = 4, u = 1, ctas = 1; };
-template <> struct Tuned<32768> { static constexpr int nt = 8,  tkb = 64, st = 3, u = 1, ctas = 1; };
+template <> struct Tuned<16384> { static constexpr int nt = 16, tkb = 64, st = 3, u = 1, ctas = 1; };
+template <> struct Tuned<32768> { static constexpr int nt = 16, tkb = 64, st = 3, u = 1, ctas = 1; };
 
 #ifdef HC_TUNE  // tools/tune.py: one configuration for every n, from -D macros
 template <int N>
