@@ -48,7 +48,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
-    ap.add_argument("--workload", choices=["fwht", "quant-e4m3", "quant-int8"], default="fwht",
+    ap.add_argument("--workload", choices=["fwht", "quant-e4m3", "quant-int8", "qk-rotate"], default="fwht",
                     help="fwht = the metric's C3 sweep (default); quant-* = the fused FWHT + per-row "
                          "quantization row (NEXT-1) on the same inputs")
     return ap.parse_args()
@@ -227,8 +227,12 @@ def reference_arm(args, rank, world):
 
 
 def config_block(args, world):
-    return {"workload": "C3 size sweep: n=2^7..2^15 x {fp16, bf16}, 2^28 elements per (n, dtype) per GPU, "
-                        "out-of-place, normalized (scale=1/sqrt(n))",
+    wl = ("C3 size sweep: n=2^7..2^15 x {fp16, bf16}, 2^28 elements per (n, dtype) per GPU, "
+          "out-of-place, normalized (scale=1/sqrt(n))")
+    if getattr(args, "workload", "fwht") == "qk-rotate":
+        wl = ("QK rotation: n=2^7..2^15 x {fp16, bf16}; a 2^28-element QKV buffer viewed as [T, 3, H, n], "
+              "H = max(1, 4096/n); the Q and K heads (2/3 of it) transformed in place, normalized")
+    return {"workload": wl,
             "elements_per_launch": args.elems, "ns": NS, "dtypes": ["fp16", "bf16"],
             "launches_per_step": 2 * len(NS), "path": getattr(args, "workload", "fwht"),
             "l2": "no flush: every launch reads a 512 MiB input and writes a 512 MiB output (> 126 MB L2)",
@@ -252,7 +256,6 @@ def main():
     import synthetic
     hc._load()  # fails loudly without the CUDA library
     dev = torch.device("cuda", local)
-    m_of = {n: args.elems // n for n in NS}
     # resident inputs: one 2^28-element matrix per dtype (each (n) is a view), rows
     # [rank*m, (rank+1)*m) of the global seeded matrix (weak scaling)
     xin, xout = {}, {}
@@ -270,7 +273,23 @@ def main():
         qbuf = torch.empty(args.elems, dtype=hc.QTYPES[qtype][1], device=dev)
         sbuf = torch.empty(args.elems // 128, dtype=torch.float32, device=dev)
 
+    rotate = args.workload == "qk-rotate"
+    qk = {}
+    if rotate:
+        # fused QKV activations [T, 3, H, n] (H = max(1, 4096 / n) heads); the Q and K
+        # heads are rotated in place through the strided entry (2 row dims: T x 2H)
+        for dt in xin:
+            for n in NS:
+                h = max(1, 4096 // n)
+                t = args.elems // (3 * h * n)
+                qk[(dt, n)] = xin[dt][: t * 3 * h * n].view(t, 3, h, n)[:, 0:2]
+    elems_of = {(dt, n): (qk[(dt, n)].numel() if rotate else args.elems) for dt, n in pairs}
+
     def launch(dt, n):
+        if rotate:
+            v = qk[(dt, n)]
+            hc.hadacore_fwht_strided(v, out=v, stream=stream)
+            return
         x = xin[dt].view(-1, n)
         if quant:
             hc.hadacore_fwht_quant(x, qtype=qtype, out=qbuf.view(-1, n), row_scale=sbuf[: x.shape[0]],
@@ -325,6 +344,8 @@ def main():
     # scale per row for the fused quantization (per-n average over the sweep)
     bytes_per_launch = 4.0 * args.elems if not quant else \
         sum(3.0 * args.elems + 4.0 * (args.elems // n) for n in NS) / len(NS)
+    if rotate:
+        bytes_per_launch = sum(4.0 * e for e in elems_of.values()) / len(pairs)
     total_bytes = bytes_per_launch * len(pairs) * args.steps * world
     value = total_bytes / (t_max * 1e-3) / 1e9
 
@@ -333,12 +354,12 @@ def main():
     for k, (dt, n) in enumerate(pairs):
         ts = sorted(per[k::len(pairs)])
         med = ts[len(ts) // 2]
-        b_n = 4.0 * args.elems if not quant else 3.0 * args.elems + 4.0 * (args.elems // n)
+        b_n = 4.0 * elems_of[(dt, n)] if not quant else 3.0 * args.elems + 4.0 * (args.elems // n)
         per_n.setdefault("fp16" if dt == torch.float16 else "bf16", {})[str(n)] = round(b_n / (med * 1e-3) / 1e9, 1)
     avg_launch_ms = sum(per) / len(per)
     peak, peak_src = measured_hbm_peak()
     achieved = bytes_per_launch / (avg_launch_ms * 1e-3) / 1e9
-    traffic = ncu_traffic() if not quant else None
+    traffic = ncu_traffic() if args.workload == "fwht" else None
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "peak_source": peak_src,
                 "frac_of_8TBps": round(achieved / NOMINAL_HBM_GBS, 4),
@@ -348,7 +369,7 @@ def main():
 
     # end to end through the public host-buffer C entry (hadacore_fwht_host)
     e2e = None
-    if not args.no_e2e and not quant:
+    if not args.no_e2e and args.workload == "fwht":
         hin = {dt: xin[dt].cpu().pin_memory() for dt in xin}
         hout = torch.empty(args.elems, dtype=torch.float16).pin_memory()
         ws = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
@@ -371,7 +392,7 @@ def main():
         del hin, hout, ws
 
     cpu_baseline = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline and not quant:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and args.workload == "fwht":
         import oracle
         oracle.build()
         threads = oracle.default_threads()
@@ -385,6 +406,9 @@ def main():
     if rank == 0:
         metric = METRIC if not quant else (f"Fused FWHT + per-row {qtype.upper()} quantization HBM GB/s vs "
                                            "n=2^7..2^15 (bf16/fp16 in, 8-bit codes + fp32 row scales out)")
+        if rotate:
+            metric = ("In-place FWHT of the Q and K heads of fused QKV activations [T, 3, H, n] (strided rows) "
+                      "HBM GB/s vs n=2^7..2^15")
         line = {
             "metric": metric, "value": round(value, 1), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(t_max / args.steps, 4), "higher_is_better": True,
@@ -392,7 +416,7 @@ def main():
             "data": "synthetic (counter-based N(0,1), synthetic/)", "config": config_block(args, world),
             "pct_of_8TBps": round(100.0 * value / world / NOMINAL_HBM_GBS, 2),
             "per_n_GBps": per_n, "roofline": roofline, "cpu_baseline": cpu_baseline, "e2e": e2e,
-            "gpu_launches": int(args.steps * sum(hc.launches_per_call(m_of[n], n) for _, n in pairs)),
+            "gpu_launches": int(args.steps * sum(hc.launches_per_call(elems_of[(dt, n)] // n, n) for dt, n in pairs)),
             "clocks": clocks, "remeasured_for_clocks": remeasured,
         }
         print(json.dumps(line), flush=True)

@@ -102,6 +102,25 @@ hadacore_status_t hadacore_fwht_host(const void* in_host, void* out_host, int64_
                                      size_t workspace_bytes, hadacore_stream_t stream);
 
 /*
+ * Strided / multi-head rows: the same transform on the rows
+ * of a 2-level grid, e.g. the Q (or K) heads inside a fused QKV projection
+ * [tokens, 3, H, d] (m_outer = tokens, m_inner = H, stride_outer = 3*H*d,
+ * stride_inner = d, n = d) rotated in place before FP8 attention.
+ *     row (i, j), i < m_outer, j < m_inner:
+ *         in  + i * in_stride_outer  + j * in_stride_inner     (element offsets)
+ *         out + i * out_stride_outer + j * out_stride_inner
+ * Strides are element counts, positive multiples of 8 (16 bytes) below 2^38; rows
+ * may not overlap (stride_inner >= n when m_inner > 1; stride_outer >= (m_inner-1) *
+ * stride_inner + n when m_outer > 1) -- else HADACORE_ERR_INVALID_M.  in == out
+ * requires identical strides; otherwise the two extents may not overlap
+ * (HADACORE_ERR_OVERLAP).  fp16/bf16 only.  Other rules as hadacore_fwht.
+ */
+hadacore_status_t hadacore_fwht_strided(const void* in, void* out, int64_t m_outer, int64_t m_inner,
+                                        int64_t in_stride_outer, int64_t in_stride_inner,
+                                        int64_t out_stride_outer, int64_t out_stride_inner, int64_t n,
+                                        hadacore_dtype_t dtype, float scale, hadacore_stream_t stream);
+
+/*
  * Fused transform + per-row symmetric quantization (the
  * paper's future work "fused Hadamard transform and quantization", P:207 [Sec. 5],
  * for its FP8-attention use, P:180 [Sec. 4.2]):

@@ -20,7 +20,7 @@ import os
 
 import torch
 
-__all__ = ["hadacore_fwht", "hadacore_fwht_host", "hadacore_fwht_quant", "fwht", "HadacoreError", "library_path",
+__all__ = ["hadacore_fwht", "hadacore_fwht_host", "hadacore_fwht_quant", "hadacore_fwht_strided", "fwht", "HadacoreError", "library_path",
            "version", "launches_per_call", "STATUS", "QTYPES"]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -61,6 +61,8 @@ def _load():
     lib.hadacore_fwht_host.restype = ctypes.c_int
     lib.hadacore_fwht_quant.argtypes = [vp, vp, vp, i64, i64, ctypes.c_int, ctypes.c_int, f32, vp]
     lib.hadacore_fwht_quant.restype = ctypes.c_int
+    lib.hadacore_fwht_strided.argtypes = [vp, vp, i64, i64, i64, i64, i64, i64, i64, ctypes.c_int, f32, vp]
+    lib.hadacore_fwht_strided.restype = ctypes.c_int
     lib.hadacore_status_string.argtypes = [ctypes.c_int]
     lib.hadacore_status_string.restype = ctypes.c_char_p
     lib.hadacore_version.argtypes = []
@@ -183,3 +185,50 @@ def hadacore_fwht_quant(x: torch.Tensor, qtype: str = "e4m3", scale: float | Non
         _check(_load().hadacore_fwht_quant(x.data_ptr(), out.data_ptr(), row_scale.data_ptr(), m, n,
                                            _DTYPES[x.dtype], code, float(scale), st.cuda_stream))
     return out, row_scale
+
+
+def hadacore_fwht_strided(x: torch.Tensor, out: torch.Tensor | None = None, scale: float | None = None,
+                          stream: torch.cuda.Stream | None = None) -> torch.Tensor:
+    """Transform the last dimension of a strided view (C: hadacore_fwht_strided).
+
+    ``x`` may be any CUDA view whose last dimension n is contiguous and whose
+    leading dimensions collapse to at most two strided row dimensions, e.g.
+    ``qkv[:, 0]`` of a ``[tokens, 3, H, d]`` projection (rows = tokens x H).
+    ``out=x`` transforms the view in place (the rest of the buffer is untouched);
+    by default the result is a new contiguous tensor.
+    """
+    m, n = _shape(x)
+    if not x.is_cuda or x.stride(-1) != 1:
+        raise HadacoreError(4, "x must be a CUDA view with a contiguous last dimension")
+    if out is None:
+        out = torch.empty(x.shape, dtype=x.dtype, device=x.device)
+    if out.shape != x.shape or out.dtype != x.dtype or out.stride(-1) != 1:
+        raise HadacoreError(3, "out must have x's shape and dtype and a contiguous last dimension")
+
+    def grid(t):
+        # collapse leading dims (dropping size-1 dims) into <= 2 strided row dims
+        dims = [(s, st) for s, st in zip(t.shape[:-1], t.stride()[:-1]) if s != 1]
+        merged = []
+        for size, st in dims:
+            if merged and merged[-1][1] == st * size:
+                merged[-1] = (merged[-1][0] * size, st)
+            else:
+                merged.append((size, st))
+        if len(merged) > 2:
+            raise HadacoreError(2, "more than two non-collapsible row dimensions")
+        while len(merged) < 2:
+            merged.insert(0, (1, n * (merged[0][0] if merged else 1)))
+        (mo, so), (mi, si) = merged
+        return mo, mi, so, si
+
+    mo, mi, so, si = grid(x)
+    mo2, mi2, oso, osi = grid(out)
+    if (mo2, mi2) != (mo, mi):
+        raise HadacoreError(3, "out's row grid differs from x's")
+    if scale is None:
+        scale = 1.0 / math.sqrt(n) if n > 0 else 1.0
+    with torch.cuda.device(x.device):
+        st = stream if stream is not None else torch.cuda.current_stream(x.device)
+        _check(_load().hadacore_fwht_strided(x.data_ptr(), out.data_ptr(), mo, mi, so, si, oso, osi, n,
+                                             _DTYPES[x.dtype], float(scale), st.cuda_stream))
+    return out

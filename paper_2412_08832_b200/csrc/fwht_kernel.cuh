@@ -492,14 +492,104 @@ __host__ __device__ constexpr int total_shift() {
   else return 2 * stage_shift(0xFu) + stage_shift(PlanL<log2_n<N>() - 8>::mask_a);
 }
 
+// ------------------------------------------------------------------ TMA tensor helpers
+__device__ __forceinline__ void tma_prefetch(const void* tmap) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(tmap)) : "memory");
+}
+// 4-D tiled TMA load (SASS UTMALDG) with completion on an mbarrier.
+__device__ __forceinline__ void tma_load_4d(void* dst, const void* tmap, int c0, int c1, int c2, int c3,
+                                            uint64_t* bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3, %4, %5}], [%6], %7;" ::"r"(smem_addr(dst)),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_addr(bar)), "l"(policy)
+      : "memory");
+}
+// 4-D tiled TMA store (SASS UTMASTG), bulk-group completion.
+__device__ __forceinline__ void tma_store_4d(const void* tmap, int c0, int c1, int c2, int c3, const void* src) {
+  asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.tile.bulk_group [%0, {%1, %2, %3, %4}], [%5];" ::"l"(
+                   reinterpret_cast<uint64_t>(tmap)),
+               "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_addr(src))
+               : "memory");
+}
+// 3-D / 5-D tiled TMA loads and 5-D store (the row-grid views of DESIGN.md "Row grids").
+__device__ __forceinline__ void tma_load_3d(void* dst, const void* tmap, int c0, int c1, int c2, uint64_t* bar,
+                                            uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(smem_addr(dst)),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_addr(bar)), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_5d(void* dst, const void* tmap, int c0, int c1, int c2, int c3, int c4,
+                                            uint64_t* bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7], %8;" ::"r"(smem_addr(dst)),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(smem_addr(bar)),
+      "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ void tma_store_5d(const void* tmap, int c0, int c1, int c2, int c3, int c4, const void* src) {
+  asm volatile("cp.async.bulk.tensor.5d.global.shared::cta.tile.bulk_group [%0, {%1, %2, %3, %4, %5}], [%6];" ::"l"(
+                   reinterpret_cast<uint64_t>(tmap)),
+               "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(smem_addr(src))
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read_all() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+template <int PENDING>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(PENDING) : "memory");
+}
+
+// ------------------------------------------------------------------ row grids
+// Rows are a 2-level grid (NEXT-3 "strided / multi-head layouts"): row (i, j), i <
+// m_outer, j < m_inner, lives at base + i*stride_outer + j*stride_inner elements
+// (contiguous m x n: m_outer = m, m_inner = 1).  A pipeline tile is a rectangle of
+// bo outer x bi inner rows (bi a power of two, bi * bo = TILE_ROWS), matching the
+// TMA box, numbered tile = outer_block * nib + inner_block; rows past either edge
+// are zero-filled on load and skipped on store.
+struct RowGrid {
+  int64_t m_outer, m_inner;
+  int64_t out_so, out_si;  // output strides in elements (16-bit outputs)
+  int64_t nib;             // inner blocks = ceil(m_inner / bi)
+  int64_t num_tiles;
+  int32_t lbi, bo;         // log2(bi), bo
+  // non-null when the input rows are one contiguous m x n block (m_inner = 1,
+  // stride_outer = n): fwht_kernel then loads a tile with one 1-D bulk copy of its
+  // valid rows instead of the 3-D tensor box, whose 256-byte box rows (n = 128)
+  // measured 6-9 % slower (profiles/r01_ab_strided.txt)
+  const uint16_t* flat_in;
+};
+struct TileRows {
+  int64_t i0, j0;
+  int lbi;
+  __device__ __forceinline__ TileRows(const RowGrid& g, int64_t tile) : lbi(g.lbi) {
+    const int64_t ob = tile / g.nib, ib = tile - ob * g.nib;
+    i0 = ob * g.bo;
+    j0 = ib << g.lbi;
+  }
+  // tile row r -> (i, j); false if (i, j) is outside the grid
+  __device__ __forceinline__ bool at(const RowGrid& g, int r, int64_t& i, int64_t& j) const {
+    i = i0 + (r >> lbi);
+    j = j0 + (r & ((1 << lbi) - 1));
+    return i < g.m_outer && j < g.m_inner;
+  }
+};
+
 // ------------------------------------------------------------------ kernel
 // Template parameters: N (row length), DT (dtype), TILE_ROWS (rows per pipeline
 // stage), STAGES (ring depth), NT (compute warps), P (warps per row team, n > 256),
 // U (work items per warp processed together, for ILP), CTAS (resident CTAs per SM).
-template <int N, int DT, int TILE_ROWS, int STAGES, int NT, int P, int U, int CTAS, int QT>
+// FLAT: input and output are contiguous m x n (g.flat_in set, out_so = n): the
+// epilogue addresses rows as out + row * n with a 32-bit bound, as before the row
+// grids existed (the general (i, j) addressing costs n = 128 6-9 %).
+template <int N, int DT, int TILE_ROWS, int STAGES, int NT, int P, int U, int CTAS, int QT, bool FLAT>
 __global__ void __launch_bounds__((NT + 1) * 32, CTAS)
-    fwht_kernel(const uint16_t* __restrict__ in, uint16_t* __restrict__ out, uint8_t* __restrict__ out_q,
-                float* __restrict__ row_scale, int64_t m, float s_res) {
+    fwht_kernel(const __grid_constant__ CUtensorMap tm_in, uint16_t* __restrict__ out, uint8_t* __restrict__ out_q,
+                float* __restrict__ row_scale, const RowGrid g, float s_res) {
   constexpr int ROW_BYTES = 2 * N;
   constexpr int TILE_BYTES = TILE_ROWS * ROW_BYTES;
   static_assert(TILE_BYTES % 16 == 0, "bulk copy granularity");
@@ -508,7 +598,7 @@ __global__ void __launch_bounds__((NT + 1) * 32, CTAS)
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * TILE_BYTES + sizeof(SchedCtl));
   uint64_t* empty = full + STAGES;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t num_tiles = (m + TILE_ROWS - 1) / TILE_ROWS;
+  const int64_t num_tiles = g.num_tiles;
   static_assert(STAGES <= 16, "SchedCtl holds 16 stages");
 
   if (threadIdx.x == 0) {
@@ -525,8 +615,9 @@ __global__ void __launch_bounds__((NT + 1) * 32, CTAS)
 
   pdl_launch_dependents();
   if (warp == NT) {
-    // ---------------- producer: TMA bulk loads of row tiles into the ring
+    // ---------------- producer: TMA loads (3-D row-grid box) of row tiles into the ring
     if (lane == 0) {
+      if (!FLAT) tma_prefetch(&tm_in);
       pdl_wait();  // the previous kernel on the stream has completed; all our global traffic follows this
       const uint64_t pol = policy_evict_first();
       uint32_t clc_phase = 0;
@@ -542,12 +633,16 @@ __global__ void __launch_bounds__((NT + 1) * 32, CTAS)
         }
         ctl->stage_tile[s] = int(tile);
         if constexpr (kClc) clc_request(ctl);  // ask for the next tile while this one loads
-        const int64_t row0 = tile * TILE_ROWS;
-        const int64_t rem = m - row0;
-        const int rows = rem < TILE_ROWS ? int(rem) : TILE_ROWS;
-        const uint32_t bytes = uint32_t(rows) * ROW_BYTES;
-        mbar_arrive_expect_tx(&full[s], bytes);
-        bulk_g2s(smem + s * TILE_BYTES, in + row0 * N, bytes, &full[s], pol);
+        const TileRows tr(g, tile);
+        if (FLAT) {
+          const int64_t rem = g.m_outer - tr.i0;
+          const uint32_t bytes = uint32_t(rem < TILE_ROWS ? rem : TILE_ROWS) * ROW_BYTES;
+          mbar_arrive_expect_tx(&full[s], bytes);
+          bulk_g2s(smem + s * TILE_BYTES, g.flat_in + tr.i0 * N, bytes, &full[s], pol);
+        } else {
+          mbar_arrive_expect_tx(&full[s], TILE_BYTES);  // full box; rows outside the grid are zero-filled
+          tma_load_3d(smem + s * TILE_BYTES, &tm_in, 0, int(tr.j0), int(tr.i0), &full[s], pol);
+        }
         if constexpr (kClc) {
           tile = clc_result(ctl, clc_phase);
         } else {
@@ -571,8 +666,9 @@ __global__ void __launch_bounds__((NT + 1) * 32, CTAS)
       mbar_wait(&full[s], (it / STAGES) & 1);
       const int64_t tile = ctl->stage_tile[s];
       if (tile < 0) break;
-      const int64_t row0 = tile * TILE_ROWS;
-      const int rows = (m - row0) < TILE_ROWS ? int(m - row0) : TILE_ROWS;
+      const TileRows tr(g, tile);
+      const int64_t left = g.m_outer - tr.i0;
+      const int rows_left = left < TILE_ROWS ? int(left) : TILE_ROWS;  // FLAT only
       const uint8_t* tb = smem + s * TILE_BYTES;
       for (int f0 = warp; f0 < FR; f0 += NT * U) {
         uint32_t x[U][4], y[U][4], z[U][4];
@@ -613,17 +709,24 @@ __global__ void __launch_bounds__((NT + 1) * 32, CTAS)
               float sc, inv;
               row_scale_of<QT>(warp_absmax(a) * fabsf(s_res), sc, inv);
               const float mul = s_res * inv;
-              const int64_t row = row0 + 2 * f + h;
-              if (2 * f + h < rows) {
+              int64_t i, j;
+              if (FLAT ? 2 * f + h < rows_left : tr.at(g, 2 * f + h, i, j)) {  // codes/scales: contiguous [rows, n]
+                const int64_t row = FLAT ? tr.i0 + 2 * f + h : i * g.m_inner + j;
                 *reinterpret_cast<uint32_t*>(out_q + row * N + lane * 4) =
                     quant4<QT>(d[u][4 * h] * mul, d[u][4 * h + 1] * mul, d[u][4 * h + 2] * mul, d[u][4 * h + 3] * mul);
                 if (lane == 0) row_scale[row] = sc;
               }
             }
           } else {
-            uint16_t* o = out + (row0 + 2 * f) * N + lane * 4;
-            if (2 * f < rows) stg64(o, z[u][0], z[u][1]);
-            if (2 * f + 1 < rows) stg64(o + N, z[u][2], z[u][3]);
+            if constexpr (FLAT) {
+              uint16_t* o = out + (tr.i0 + 2 * f) * N + lane * 4;
+              if (2 * f < rows_left) stg64(o, z[u][0], z[u][1]);
+              if (2 * f + 1 < rows_left) stg64(o + N, z[u][2], z[u][3]);
+            } else {
+              int64_t i, j;
+              if (tr.at(g, 2 * f, i, j)) stg64(out + i * g.out_so + j * g.out_si + lane * 4, z[u][0], z[u][1]);
+              if (tr.at(g, 2 * f + 1, i, j)) stg64(out + i * g.out_so + j * g.out_si + lane * 4, z[u][2], z[u][3]);
+            }
           }
         }
       }
@@ -640,8 +743,9 @@ __global__ void __launch_bounds__((NT + 1) * 32, CTAS)
       mbar_wait(&full[s], (it / STAGES) & 1);
       const int64_t tile = ctl->stage_tile[s];
       if (tile < 0) break;
-      const int64_t row0 = tile * TILE_ROWS;
-      const int rows = (m - row0) < TILE_ROWS ? int(m - row0) : TILE_ROWS;
+      const TileRows tr(g, tile);
+      const int64_t left = g.m_outer - tr.i0;
+      const int rows_left = left < TILE_ROWS ? int(left) : TILE_ROWS;  // FLAT only
       const uint8_t* tb = smem + s * TILE_BYTES;
       for (int r0 = warp; r0 < TILE_ROWS; r0 += NT * U) {
         uint32_t x[U][4], y[U][4], z[U][4];
@@ -670,14 +774,22 @@ __global__ void __launch_bounds__((NT + 1) * 32, CTAS)
             float sc, inv;
             row_scale_of<QT>(warp_absmax(a) * fabsf(s_res), sc, inv);
             const float mul = s_res * inv;
-            if (r < rows) {
-              *reinterpret_cast<uint2*>(out_q + (row0 + r) * N + lane * 8) =
+            int64_t i, j;
+            if (FLAT ? r < rows_left : tr.at(g, r, i, j)) {
+              const int64_t row = FLAT ? tr.i0 + r : i * g.m_inner + j;
+              *reinterpret_cast<uint2*>(out_q + row * N + lane * 8) =
                   make_uint2(quant4<QT>(d[u][0] * mul, d[u][1] * mul, d[u][2] * mul, d[u][3] * mul),
                              quant4<QT>(d[u][4] * mul, d[u][5] * mul, d[u][6] * mul, d[u][7] * mul));
-              if (lane == 0) row_scale[row0 + r] = sc;
+              if (lane == 0) row_scale[row] = sc;
             }
           } else {
-            if (r < rows) stg128(out + (row0 + r) * N + lane * 8, z[u][0], z[u][1], z[u][2], z[u][3]);
+            if constexpr (FLAT) {
+              if (r < rows_left) stg128(out + (tr.i0 + r) * N + lane * 8, z[u][0], z[u][1], z[u][2], z[u][3]);
+            } else {
+              int64_t i, j;
+              if (tr.at(g, r, i, j))
+                stg128(out + i * g.out_so + j * g.out_si + lane * 8, z[u][0], z[u][1], z[u][2], z[u][3]);
+            }
           }
         }
       }
@@ -690,34 +802,6 @@ __global__ void __launch_bounds__((NT + 1) * 32, CTAS)
     (void)out_q;
     (void)row_scale;
   }
-}
-
-// ------------------------------------------------------------------ TMA tensor helpers
-__device__ __forceinline__ void tma_prefetch(const void* tmap) {
-  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(tmap)) : "memory");
-}
-// 4-D tiled TMA load (SASS UTMALDG) with completion on an mbarrier.
-__device__ __forceinline__ void tma_load_4d(void* dst, const void* tmap, int c0, int c1, int c2, int c3,
-                                            uint64_t* bar, uint64_t policy) {
-  asm volatile(
-      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
-      " [%0], [%1, {%2, %3, %4, %5}], [%6], %7;" ::"r"(smem_addr(dst)),
-      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_addr(bar)), "l"(policy)
-      : "memory");
-}
-// 4-D tiled TMA store (SASS UTMASTG), bulk-group completion.
-__device__ __forceinline__ void tma_store_4d(const void* tmap, int c0, int c1, int c2, int c3, const void* src) {
-  asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.tile.bulk_group [%0, {%1, %2, %3, %4}], [%5];" ::"l"(
-                   reinterpret_cast<uint64_t>(tmap)),
-               "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_addr(src))
-               : "memory");
-}
-__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void bulk_wait_read_all() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
-__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
-template <int PENDING>
-__device__ __forceinline__ void bulk_wait_read() {
-  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(PENDING) : "memory");
 }
 
 // Byte offset, inside a row's shared-memory image, of granule g (8 elements) of
@@ -751,14 +835,15 @@ __host__ __device__ constexpr bool seg_mode(int n, int tile_rows) {
 
 // Loads boxes K..NB-1 of a SEG tile (box k = row k/4, segment k%4); with WAIT, box k
 // first waits until the store that read the same bytes (issued k-th of NB) is done.
-template <int K, int NB, int ROW_BYTES, bool WAIT>
-__device__ __forceinline__ void seg_loads(uint8_t* stage, const void* tmap, int row0, uint64_t* bar,
+template <int K, int NB, int ROW_BYTES, bool WAIT, typename TR>
+__device__ __forceinline__ void seg_loads(uint8_t* stage, const void* tmap, const TR& tr, uint64_t* bar,
                                           uint64_t pol) {
   if constexpr (K < NB) {
     if constexpr (WAIT) bulk_wait_read<NB - 1 - K>();
-    tma_load_4d(stage + (K / 4) * ROW_BYTES + (K % 4) * (ROW_BYTES / 4), tmap, 0, 0, K % 4, row0 + K / 4, bar,
-                pol);
-    seg_loads<K + 1, NB, ROW_BYTES, WAIT>(stage, tmap, row0, bar, pol);
+    constexpr int r = K / 4;
+    tma_load_5d(stage + r * ROW_BYTES + (K % 4) * (ROW_BYTES / 4), tmap, 0, 0, K % 4,
+                int(tr.j0 + (r & ((1 << tr.lbi) - 1))), int(tr.i0 + (r >> tr.lbi)), bar, pol);
+    seg_loads<K + 1, NB, ROW_BYTES, WAIT>(stage, tmap, tr, bar, pol);
   }
 }
 
@@ -773,7 +858,7 @@ template <int N, int DT, int TILE_ROWS, int STAGES, int NT, int P, int U, int CT
 __global__ void __launch_bounds__((NT + 1) * 32, CTAS)
     fwht_rows_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ CUtensorMap tm_out,
                      uint16_t* __restrict__ out, uint8_t* __restrict__ out_q, float* __restrict__ row_scale,
-                     int64_t m, float s_res) {
+                     const RowGrid g, float s_res) {
   constexpr int ROW_BYTES = 2 * N;
   constexpr int TILE_BYTES = TILE_ROWS * ROW_BYTES;
   constexpr int Q = log2_n<N>() - 8;
@@ -803,7 +888,7 @@ __global__ void __launch_bounds__((NT + 1) * 32, CTAS)
   float* red = reinterpret_cast<float*>(smem + STAGES * TILE_BYTES + sizeof(SchedCtl) + 17 * STAGES * 8);
   static_assert(STAGES <= 16, "SchedCtl holds 16 stages");
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t num_tiles = (m + TILE_ROWS - 1) / TILE_ROWS;
+  const int64_t num_tiles = g.num_tiles;
 
   if (threadIdx.x == 0) {
     mbar_init(&ctl->clc_bar, 1);
@@ -831,15 +916,16 @@ __global__ void __launch_bounds__((NT + 1) * 32, CTAS)
       const uint64_t pol = policy_evict_first();
       auto load_tile = [&](int st, int64_t tile, auto wait_store_read) {
         mbar_arrive_expect_tx(&full[st], TILE_BYTES);  // full box, OOB rows zero-filled
+        const TileRows tr(g, tile);
         if constexpr (SEG) {
           if constexpr (decltype(wait_store_read(0))::value) {
-            seg_loads<0, NSEG, ROW_BYTES, true>(smem + st * TILE_BYTES, &tm_in, int(tile * TILE_ROWS), &full[st], pol);
+            seg_loads<0, NSEG, ROW_BYTES, true>(smem + st * TILE_BYTES, &tm_in, tr, &full[st], pol);
           } else {
-            seg_loads<0, NSEG, ROW_BYTES, false>(smem + st * TILE_BYTES, &tm_in, int(tile * TILE_ROWS), &full[st], pol);
+            seg_loads<0, NSEG, ROW_BYTES, false>(smem + st * TILE_BYTES, &tm_in, tr, &full[st], pol);
           }
         } else {
           if constexpr (decltype(wait_store_read(0))::value) bulk_wait_read<0>();
-          tma_load_4d(smem + st * TILE_BYTES, &tm_in, 0, 0, 0, int(tile * TILE_ROWS), &full[st], pol);
+          tma_load_5d(smem + st * TILE_BYTES, &tm_in, 0, 0, 0, int(tr.j0), int(tr.i0), &full[st], pol);
         }
       };
       // the tag says whether a refill must first wait for the previous occupant's
@@ -875,15 +961,17 @@ __global__ void __launch_bounds__((NT + 1) * 32, CTAS)
         const int64_t t = ctl->stage_tile[s];
         if (t < 0) break;
 #pragma unroll
-        for (int g = 0; g < NSEG; ++g) {
-          mbar_wait(&done[s * NSEG + g], ph);
-          if (g == 0) trace(it, 1);
+        for (int gs = 0; gs < NSEG; ++gs) {
+          mbar_wait(&done[s * NSEG + gs], ph);
+          if (gs == 0) trace(it, 1);
           if constexpr (STG_OUT) continue;
+          const TileRows tr(g, t);
           if constexpr (SEG) {
-            tma_store_4d(&tm_out, 0, 0, g % 4, int(t * TILE_ROWS) + g / 4,
-                         smem + s * TILE_BYTES + (g / 4) * ROW_BYTES + (g % 4) * SEG_BYTES);
-          } else {
-            tma_store_4d(&tm_out, 0, 0, 0, int(t * TILE_ROWS), smem + s * TILE_BYTES);  // OOB rows clipped
+            const int r = gs / 4;
+            tma_store_5d(&tm_out, 0, 0, gs % 4, int(tr.j0 + (r & ((1 << tr.lbi) - 1))), int(tr.i0 + (r >> tr.lbi)),
+                         smem + s * TILE_BYTES + r * ROW_BYTES + (gs % 4) * SEG_BYTES);
+          } else {  // rows outside the grid are clipped by the TMA unit
+            tma_store_5d(&tm_out, 0, 0, 0, int(tr.j0), int(tr.i0), smem + s * TILE_BYTES);
           }
           bulk_commit();
         }
@@ -1060,15 +1148,15 @@ __global__ void __launch_bounds__((NT + 1) * 32, CTAS)
       }
       team_sync();
       float inv_r[RPT];
-      const int64_t row0 = tile * TILE_ROWS;
+      const TileRows tr(g, tile);
 #pragma unroll
       for (int k = 0; k < RPT; ++k) {
         float a = 0.f;
         for (int w = 0; w < P; ++w) a = absmax_nan(a, red[(team * RPT + k) * P + w]);
         float sc;
         row_scale_of<QT>(a, sc, inv_r[k]);
-        const int r = team + NTEAMS * k;
-        if (wt == 0 && lane == 0 && row0 + r < m) row_scale[row0 + r] = sc;
+        int64_t i, j;
+        if (wt == 0 && lane == 0 && tr.at(g, team + NTEAMS * k, i, j)) row_scale[i * g.m_inner + j] = sc;
       }
       for (int i0 = wt; i0 < ITEMS1; i0 += P * U1) {
         uint32_t z[U1][4];
@@ -1086,8 +1174,9 @@ __global__ void __launch_bounds__((NT + 1) * 32, CTAS)
             if (k == rl) inv = inv_r[k];
           float v[8];
           unpack8<DT>(z[u], v);
-          if (row0 + r < m)
-            *reinterpret_cast<uint2*>(out_q + (row0 + r) * N + c * 256 + lane * 8) =
+          int64_t i, j;
+          if (tr.at(g, r, i, j))
+            *reinterpret_cast<uint2*>(out_q + (i * g.m_inner + j) * N + c * 256 + lane * 8) =
                 make_uint2(quant4<QT>(v[0] * inv, v[1] * inv, v[2] * inv, v[3] * inv),
                            quant4<QT>(v[4] * inv, v[5] * inv, v[6] * inv, v[7] * inv));
         }
@@ -1095,7 +1184,7 @@ __global__ void __launch_bounds__((NT + 1) * 32, CTAS)
       // (red[] is rewritten only after the next tile's phase-1 barrier: no race)
     } else if constexpr (STG_OUT) {
       team_sync();
-      const int64_t row0 = tile * TILE_ROWS;
+      const TileRows tr(g, tile);
       for (int i0 = wt; i0 < ITEMS1; i0 += P * U1) {
         uint32_t z[U1][4];
 #pragma unroll
@@ -1106,7 +1195,9 @@ __global__ void __launch_bounds__((NT + 1) * 32, CTAS)
 #pragma unroll
         for (int u = 0; u < U1; ++u) {
           const int item = i0 + u * P, r = team + NTEAMS * (item / C), c = item % C;
-          if (row0 + r < m) stg128(out + (row0 + r) * N + c * 256 + lane * 8, z[u][0], z[u][1], z[u][2], z[u][3]);
+          int64_t i, j;
+          if (tr.at(g, r, i, j))
+            stg128(out + i * g.out_so + j * g.out_si + c * 256 + lane * 8, z[u][0], z[u][1], z[u][2], z[u][3]);
         }
       }
     }

@@ -92,19 +92,59 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
   return fn;
 }
 
-// 4-D view of an m x n row-major 16-bit matrix for TMA: (64 elements, chunk c of
-// 256 elements [stride 512 B], 128-byte segment s of the chunk [stride 128 B], row
-// [stride 2n B]); box (64, C, 4, rows) with SWIZZLE_128B (DESIGN.md "Shared-memory
-// layout").  Returns false if the driver rejects the descriptor.
-bool encode_rows_map(CUtensorMap* map, const void* base, int64_t m, int n, int box_rows, int box_segs) {
+// Row layout of one call: rows (i, j), i < m_outer, j < m_inner,
+// at base + i*so + j*si elements; contiguous m x n is {m, 1, n, n}.
+struct Layout {
+  int64_t m_outer, m_inner;
+  int64_t in_so, in_si, out_so, out_si;
+};
+
+// Tile shape for TILE_ROWS rows: bi (power of two) inner x bo outer rows.
+RowGrid make_grid(const Layout& L, int tile_rows) {
+  int bi = 1;
+  while (bi * 2 <= tile_rows && bi * 2 <= L.m_inner) bi *= 2;
+  int lbi = 0;
+  while ((1 << lbi) < bi) ++lbi;
+  RowGrid g{};
+  g.m_outer = L.m_outer;
+  g.m_inner = L.m_inner;
+  g.out_so = L.out_so;
+  g.out_si = L.out_si;
+  g.lbi = lbi;
+  g.bo = tile_rows / bi;
+  g.nib = (L.m_inner + bi - 1) / bi;
+  g.num_tiles = ((L.m_outer + g.bo - 1) / g.bo) * g.nib;
+  return g;
+}
+
+// 3-D view (n elements, inner row, outer row) for fwht_kernel (n <= 256), box (n, bi, bo).
+bool encode_small_map(CUtensorMap* map, const void* base, const Layout& L, int64_t so, int64_t si, int n,
+                      const RowGrid& g) {
+  PFN_cuTensorMapEncodeTiled_v12000 enc = tensor_map_encoder();
+  if (!enc) return false;
+  cuuint64_t dims[3] = {cuuint64_t(n), cuuint64_t(L.m_inner), cuuint64_t(L.m_outer)};
+  cuuint64_t strides[2] = {cuuint64_t(2) * cuuint64_t(si), cuuint64_t(2) * cuuint64_t(so)};
+  cuuint32_t box[3] = {cuuint32_t(n), cuuint32_t(1u << g.lbi), cuuint32_t(g.bo)};
+  cuuint32_t estr[3] = {1, 1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT16, 3, const_cast<void*>(base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// 5-D view for fwht_rows_kernel (n >= 512): (64 elements, chunk c of 256 elements
+// [stride 512 B], 128-byte segment s of the chunk [stride 128 B], inner row, outer
+// row); box (64, C, 4, bi, bo) with SWIZZLE_128B,
+// or (64, C, 1, 1, 1) per (row, segment) in SEG mode.
+bool encode_rows_map(CUtensorMap* map, const void* base, const Layout& L, int64_t so, int64_t si, int n,
+                     const RowGrid& g, bool seg) {
   PFN_cuTensorMapEncodeTiled_v12000 enc = tensor_map_encoder();
   if (!enc) return false;
   const int C = n / 256;
-  cuuint64_t dims[4] = {64, cuuint64_t(C), 4, cuuint64_t(m)};
-  cuuint64_t strides[3] = {512, 128, cuuint64_t(2) * cuuint64_t(n)};
-  cuuint32_t box[4] = {64, cuuint32_t(C), cuuint32_t(box_segs), cuuint32_t(box_rows)};
-  cuuint32_t estr[4] = {1, 1, 1, 1};
-  return enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT16, 4, const_cast<void*>(base), dims, strides, box, estr,
+  cuuint64_t dims[5] = {64, cuuint64_t(C), 4, cuuint64_t(L.m_inner), cuuint64_t(L.m_outer)};
+  cuuint64_t strides[4] = {512, 128, cuuint64_t(2) * cuuint64_t(si), cuuint64_t(2) * cuuint64_t(so)};
+  cuuint32_t box[5] = {64, cuuint32_t(C), seg ? 1u : 4u, seg ? 1u : cuuint32_t(1u << g.lbi), seg ? 1u : cuuint32_t(g.bo)};
+  cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT16, 5, const_cast<void*>(base), dims, strides, box, estr,
              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
@@ -143,62 +183,74 @@ bool ensure_smem_attr(Kern kern, int smem, std::atomic<uint64_t>& done, int dev)
 }
 
 template <int N, int DT, int QT>
-hadacore_status_t launch(const void* in, void* out, uint8_t* out_q, float* row_scale, int64_t m, float scale,
+hadacore_status_t launch(const void* in, void* out, uint8_t* out_q, float* row_scale, const Layout& L, float scale,
                          cudaStream_t stream) {
   using C = Cfg<N>;
-  // SEG mode (n >= 8192): each (row, 128-byte-line segment) is its own TMA box
-  constexpr int box_segs = seg_mode(N, C::rows) ? 1 : 4;
+  constexpr bool seg = seg_mode(N, C::rows);
   // + full[], done[][<=16] and the fused-quantization row-max scratch (one float per warp)
   constexpr int smem = C::stages * C::tile_bytes + int(sizeof(SchedCtl)) + 17 * C::stages * 8 +
                        4 * C::nt * (N > 256 ? C::rows : 1);
   static std::atomic<uint64_t> attr_done{0};
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return HADACORE_ERR_CUDA;
+  const RowGrid g = make_grid(L, C::rows);
   // CLC scheduling (default): one CTA per tile, resident CTAs steal the rest;
   // HC_STATIC_SCHED: persistent grid of one CTA per SM with round-robin tiles
-  const int64_t tiles = (m + C::rows - 1) / C::rows;
   const int64_t max_ctas = kClc ? int64_t(INT32_MAX) : int64_t(sm_count(dev)) * C::ctas;
-  const int grid = int(tiles < max_ctas ? tiles : max_ctas);
+  const int grid = int(g.num_tiles < max_ctas ? g.num_tiles : max_ctas);
   // the per-stage constants multiply by exact powers of two 2^-E; fold the rest of
   // `scale` into the fp32 epilogue of the last stage.
   const float s_res = std::ldexp(scale, total_shift<N>());
   if constexpr (N <= 256) {
-    auto kern = fwht_kernel<N, DT, C::rows, C::stages, C::nt, C::p, C::u, C::ctas, QT>;
-    if (!ensure_smem_attr(kern, smem, attr_done, dev)) return HADACORE_ERR_CUDA;
-    if (launch_pdl(kern, grid, (C::nt + 1) * 32, smem, stream, static_cast<const uint16_t*>(in),
-                   static_cast<uint16_t*>(out), out_q, row_scale, m, s_res) != cudaSuccess)
+    // contiguous m x n in and out: 1-D bulk loads and flat epilogue addressing
+    const bool flat = L.m_inner == 1 && L.in_so == N && (QT >= 0 || L.out_so == N);
+    auto kern = flat ? fwht_kernel<N, DT, C::rows, C::stages, C::nt, C::p, C::u, C::ctas, QT, true>
+                     : fwht_kernel<N, DT, C::rows, C::stages, C::nt, C::p, C::u, C::ctas, QT, false>;
+    static std::atomic<uint64_t> attr_done_flat{0};
+    if (!ensure_smem_attr(kern, smem, flat ? attr_done_flat : attr_done, dev)) return HADACORE_ERR_CUDA;
+    RowGrid gs = g;
+    CUtensorMap tin{};
+    if (flat) {
+      gs.flat_in = static_cast<const uint16_t*>(in);
+    } else if (!encode_small_map(&tin, in, L, L.in_so, L.in_si, N, g)) {
+      return HADACORE_ERR_CUDA;
+    }
+    if (launch_pdl(kern, grid, (C::nt + 1) * 32, smem, stream, tin, static_cast<uint16_t*>(out), out_q, row_scale, gs,
+                   s_res) != cudaSuccess)
       return HADACORE_ERR_CUDA;
   } else {
     auto kern = fwht_rows_kernel<N, DT, C::rows, C::stages, C::nt, C::p, C::u, C::ctas, QT>;
     if (!ensure_smem_attr(kern, smem, attr_done, dev)) return HADACORE_ERR_CUDA;
     CUtensorMap tin, tout;
-    constexpr int box_rows = seg_mode(N, C::rows) ? 1 : C::rows;
-    if (!encode_rows_map(&tin, in, m, N, box_rows, box_segs) ||
-        !encode_rows_map(&tout, QT >= 0 ? in : out, m, N, box_rows, box_segs))  // unused when quantizing
+    if (!encode_rows_map(&tin, in, L, L.in_so, L.in_si, N, g, seg) ||
+        !encode_rows_map(&tout, QT >= 0 ? in : out, L, QT >= 0 ? L.in_so : L.out_so, QT >= 0 ? L.in_si : L.out_si, N,
+                         g, seg))  // the output map is unused when quantizing
       return HADACORE_ERR_CUDA;
     if (launch_pdl(kern, grid, (C::nt + 1) * 32, smem, stream, tin, tout, static_cast<uint16_t*>(out), out_q,
-                   row_scale, m, s_res) != cudaSuccess)
+                   row_scale, g, s_res) != cudaSuccess)
       return HADACORE_ERR_CUDA;
   }
   return cudaPeekAtLastError() == cudaSuccess ? HADACORE_OK : HADACORE_ERR_CUDA;
 }
 
 template <int DT, int QT>
-hadacore_status_t dispatch_n(const void* in, void* out, uint8_t* q, float* rs, int64_t m, int64_t n, float scale,
+hadacore_status_t dispatch_n(const void* in, void* out, uint8_t* q, float* rs, const Layout& L, int64_t n, float scale,
                              cudaStream_t st) {
   switch (n) {
-    case 128: return launch<128, DT, QT>(in, out, q, rs, m, scale, st);
-    case 256: return launch<256, DT, QT>(in, out, q, rs, m, scale, st);
-    case 512: return launch<512, DT, QT>(in, out, q, rs, m, scale, st);
-    case 1024: return launch<1024, DT, QT>(in, out, q, rs, m, scale, st);
-    case 2048: return launch<2048, DT, QT>(in, out, q, rs, m, scale, st);
-    case 4096: return launch<4096, DT, QT>(in, out, q, rs, m, scale, st);
-    case 8192: return launch<8192, DT, QT>(in, out, q, rs, m, scale, st);
-    case 16384: return launch<16384, DT, QT>(in, out, q, rs, m, scale, st);
-    case 32768: return launch<32768, DT, QT>(in, out, q, rs, m, scale, st);
+    case 128: return launch<128, DT, QT>(in, out, q, rs, L, scale, st);
+    case 256: return launch<256, DT, QT>(in, out, q, rs, L, scale, st);
+    case 512: return launch<512, DT, QT>(in, out, q, rs, L, scale, st);
+    case 1024: return launch<1024, DT, QT>(in, out, q, rs, L, scale, st);
+    case 2048: return launch<2048, DT, QT>(in, out, q, rs, L, scale, st);
+    case 4096: return launch<4096, DT, QT>(in, out, q, rs, L, scale, st);
+    case 8192: return launch<8192, DT, QT>(in, out, q, rs, L, scale, st);
+    case 16384: return launch<16384, DT, QT>(in, out, q, rs, L, scale, st);
+    case 32768: return launch<32768, DT, QT>(in, out, q, rs, L, scale, st);
     default: return HADACORE_ERR_INVALID_N;
   }
 }
+
+Layout contiguous(int64_t m, int64_t n) { return Layout{m, 1, n, n, n, n}; }
 
 bool valid_n(int64_t n) { return n >= 128 && n <= 32768 && (n & (n - 1)) == 0; }
 
@@ -258,17 +310,25 @@ hadacore_status_t validate(const void* in, const void* out, int64_t m, int64_t n
 hadacore_status_t run(const void* in, void* out, int64_t m, int64_t n, int dtype, float scale,
                       cudaStream_t st) {
   if (dtype == HADACORE_F32) return dispatch_f32(in, out, m, n, scale, st);
-  return dtype == HADACORE_F16 ? dispatch_n<DT_F16, QT_NONE>(in, out, nullptr, nullptr, m, n, scale, st)
-                               : dispatch_n<DT_BF16, QT_NONE>(in, out, nullptr, nullptr, m, n, scale, st);
+  const Layout L = contiguous(m, n);
+  return dtype == HADACORE_F16 ? dispatch_n<DT_F16, QT_NONE>(in, out, nullptr, nullptr, L, n, scale, st)
+                               : dispatch_n<DT_BF16, QT_NONE>(in, out, nullptr, nullptr, L, n, scale, st);
 }
 
 hadacore_status_t run_quant(const void* in, uint8_t* q, float* rs, int64_t m, int64_t n, int dtype, int qtype,
                             float scale, cudaStream_t st) {
+  const Layout L = contiguous(m, n);
   if (dtype == HADACORE_F16)
-    return qtype == HADACORE_Q_E4M3 ? dispatch_n<DT_F16, QT_E4M3>(in, nullptr, q, rs, m, n, scale, st)
-                                    : dispatch_n<DT_F16, QT_INT8>(in, nullptr, q, rs, m, n, scale, st);
-  return qtype == HADACORE_Q_E4M3 ? dispatch_n<DT_BF16, QT_E4M3>(in, nullptr, q, rs, m, n, scale, st)
-                                  : dispatch_n<DT_BF16, QT_INT8>(in, nullptr, q, rs, m, n, scale, st);
+    return qtype == HADACORE_Q_E4M3 ? dispatch_n<DT_F16, QT_E4M3>(in, nullptr, q, rs, L, n, scale, st)
+                                    : dispatch_n<DT_F16, QT_INT8>(in, nullptr, q, rs, L, n, scale, st);
+  return qtype == HADACORE_Q_E4M3 ? dispatch_n<DT_BF16, QT_E4M3>(in, nullptr, q, rs, L, n, scale, st)
+                                  : dispatch_n<DT_BF16, QT_INT8>(in, nullptr, q, rs, L, n, scale, st);
+}
+
+hadacore_status_t run_strided(const void* in, void* out, const Layout& L, int64_t n, int dtype, float scale,
+                              cudaStream_t st) {
+  return dtype == HADACORE_F16 ? dispatch_n<DT_F16, QT_NONE>(in, out, nullptr, nullptr, L, n, scale, st)
+                               : dispatch_n<DT_BF16, QT_NONE>(in, out, nullptr, nullptr, L, n, scale, st);
 }
 
 bool ranges_overlap(const void* a, size_t abytes, const void* b, size_t bbytes) {
@@ -286,6 +346,37 @@ extern "C" hadacore_status_t hadacore_fwht(const void* in, void* out, int64_t m,
   const hadacore_status_t v = validate(in, out, m, n, int(dtype), scale, true);
   if (v != HADACORE_OK || m == 0) return v;
   return run(in, out, m, n, int(dtype), scale, reinterpret_cast<cudaStream_t>(stream));
+}
+
+extern "C" hadacore_status_t hadacore_fwht_strided(const void* in, void* out, int64_t m_outer, int64_t m_inner,
+                                                   int64_t in_stride_outer, int64_t in_stride_inner,
+                                                   int64_t out_stride_outer, int64_t out_stride_inner, int64_t n,
+                                                   hadacore_dtype_t dtype, float scale, hadacore_stream_t stream) {
+  if (dtype != HADACORE_F16 && dtype != HADACORE_BF16) return HADACORE_ERR_DTYPE;
+  if (!valid_n(n)) return HADACORE_ERR_INVALID_N;
+  if (m_outer < 0 || m_inner < 0 || m_outer > (int64_t(1) << 31) || m_inner > (int64_t(1) << 31))
+    return HADACORE_ERR_INVALID_M;
+  if (!std::isfinite(scale)) return HADACORE_ERR_SCALE;
+  if (m_outer == 0 || m_inner == 0) return HADACORE_OK;
+  if (!in || !out) return HADACORE_ERR_NULL;
+  const Layout L{m_outer, m_inner, in_stride_outer, m_inner > 1 ? in_stride_inner : n, out_stride_outer,
+                 m_inner > 1 ? out_stride_inner : n};
+  // strides: multiples of 8 elements (16 B, TMA), rows never overlap, extent fits
+  auto bad_stride = [&](int64_t so, int64_t si) {
+    if (so % 8 || si % 8 || so <= 0 || si <= 0 || so >= (int64_t(1) << 38) || si >= (int64_t(1) << 38)) return true;
+    if (m_inner > 1 && si < n) return true;
+    if (m_outer > 1 && so < (m_inner - 1) * si + n) return true;
+    return false;
+  };
+  if (bad_stride(L.in_so, L.in_si) || bad_stride(L.out_so, L.out_si)) return HADACORE_ERR_INVALID_M;
+  if ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 15u) return HADACORE_ERR_MISALIGNED;
+  auto extent = [&](int64_t so, int64_t si) { return size_t(((m_outer - 1) * so + (m_inner - 1) * si + n) * 2); };
+  if (in == out) {
+    if (L.in_so != L.out_so || L.in_si != L.out_si) return HADACORE_ERR_OVERLAP;
+  } else if (ranges_overlap(in, extent(L.in_so, L.in_si), out, extent(L.out_so, L.out_si))) {
+    return HADACORE_ERR_OVERLAP;
+  }
+  return run_strided(in, out, L, n, int(dtype), scale, reinterpret_cast<cudaStream_t>(stream));
 }
 
 extern "C" hadacore_status_t hadacore_fwht_quant(const void* in, void* out_q, float* row_scale, int64_t m,

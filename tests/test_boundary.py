@@ -30,6 +30,7 @@ def declared_functions():
 
 def test_header_declares_expected_entry_points():
     assert declared_functions() == sorted(["hadacore_fwht", "hadacore_fwht_host", "hadacore_fwht_quant",
+                                           "hadacore_fwht_strided",
                                            "hadacore_status_string", "hadacore_version",
                                            "hadacore_launches_per_call"])
 
@@ -48,8 +49,9 @@ def test_library_targets_sm100a_only(lib):
     assert "sm_100a" in out
     sass = subprocess.run(["cuobjdump", "-sass", hc.library_path()], capture_output=True, text=True).stdout
     assert "HMMA.16816" in sass          # tensor-core contractions
-    assert "UBLKCP.S.G" in sass          # bulk (TMA) global->shared copies (n <= 256)
-    assert "UTMALDG.4D" in sass and "UTMASTG.4D" in sass  # 4-D TMA tensor load/store (n >= 512)
+    assert "UTMALDG.3D" in sass          # 3-D TMA tensor loads of (n, rows, outer) boxes (n <= 256)
+    assert "UTMALDG.5D" in sass and "UTMASTG.5D" in sass  # 5-D TMA tensor load/store, SWIZZLE_128B (n >= 512)
+    assert "UGETNEXTWORKID" in sass      # cluster launch control work stealing
     assert "LDSM.16.MT88.4" in sass and "STSM.16.MT88.4" in sass  # cross-chunk exchange
 
 
@@ -138,3 +140,18 @@ def test_product_path_does_not_import_oracle():
                 text = open(os.path.join(dirpath, f)).read()
                 for bad in ("import oracle", "from oracle", "liboracle", "fwht_oracle", "oracle_fwht"):
                     assert bad not in text, (f, bad)
+
+
+def test_strided_entry_validation(lib):
+    a, b = 0x10000, 0x80000000
+    f = lib.hadacore_fwht_strided
+    # (in, out, m_outer, m_inner, in_so, in_si, out_so, out_si, n, dtype, scale, stream)
+    assert f(a, b, 4, 3, 1004, 128, 384, 128, 128, 0, 1.0, None) == INVALID_M       # stride not multiple of 8
+    assert f(a, b, 4, 3, 384, 64, 384, 128, 128, 0, 1.0, None) == INVALID_M         # inner rows overlap
+    assert f(a, b, 4, 3, 256, 128, 384, 128, 128, 0, 1.0, None) == INVALID_M        # outer rows overlap
+    assert f(a, b, 4, 3, 384, 128, 384, 128, 100, 0, 1.0, None) == INVALID_N
+    assert f(a, b, 4, 3, 384, 128, 384, 128, 128, 2, 1.0, None) == DTYPE            # fp32: contiguous API only
+    assert f(a, a, 4, 3, 384, 128, 768, 128, 128, 0, 1.0, None) == OVERLAP          # in place needs equal strides
+    assert f(a, a + 256, 4, 3, 384, 128, 384, 128, 128, 0, 1.0, None) == OVERLAP    # extents overlap
+    assert f(a + 2, b, 4, 3, 384, 128, 384, 128, 128, 0, 1.0, None) == MISALIGNED
+    assert f(None, None, 0, 3, 384, 128, 384, 128, 128, 0, 1.0, None) == OK

@@ -235,3 +235,60 @@ def test_fp32_debug_path(hc, n):
     xi = x.clone()
     hc.hadacore_fwht(xi, out=xi)
     assert torch.equal(xi, y)
+
+
+# ---------------------------------------------------------------- strided / multi-head rows (NEXT-3)
+@pytest.mark.parametrize("n,heads", [(128, 32), (128, 3), (256, 8), (512, 5), (1024, 12), (4096, 2), (32768, 1)])
+def test_strided_qkv_heads_in_place(hc, n, heads):
+    """Rotate the Q heads of a fused QKV projection [tokens, 3, H, d] in place
+    (hadacore_fwht_strided): Q matches the oracle, K and V are untouched bitwise."""
+    tokens = max(3, (1 << 20) // (3 * heads * n)) + 1
+    qkv = synthetic.generate(tokens * 3 * heads, n, torch.bfloat16, 31, dist="D1").reshape(tokens, 3, heads, n).cuda()
+    before = qkv.clone()
+    q = qkv[:, 0]
+    hc.hadacore_fwht_strided(q, out=q)
+    torch.cuda.synchronize()
+    ref = oracle.fwht(widen(before[:, 0].reshape(-1, n)))
+    err = rel_l2_rows(widen(qkv[:, 0].reshape(-1, n)), ref)
+    assert err.max() <= TOL[torch.bfloat16], err.max()
+    assert torch.equal(qkv[:, 1:].view(torch.int16), before[:, 1:].view(torch.int16))
+    # the same values as the contiguous entry point, bitwise
+    y = hc.hadacore_fwht(before[:, 0].contiguous())
+    assert torch.equal(qkv[:, 0].contiguous().view(torch.int16), y.view(torch.int16))
+
+
+@pytest.mark.parametrize("n", [128, 256, 2048])
+def test_strided_out_of_place_and_padded_rows(hc, n):
+    # rows with a padded pitch (pitch > n) into a contiguous output, and back
+    m, pitch = 777, n + 64
+    base = synthetic.generate(m, pitch, torch.float16, 32).cuda()
+    x = base[:, :n]
+    y = hc.hadacore_fwht_strided(x)
+    assert y.is_contiguous()
+    ref = oracle.fwht(widen(x))
+    assert rel_l2_rows(widen(y), ref).max() <= TOL[torch.float16]
+    out_pad = torch.zeros(m, pitch, dtype=torch.float16, device="cuda")
+    hc.hadacore_fwht_strided(x, out=out_pad[:, :n])
+    assert torch.equal(out_pad[:, :n].view(torch.int16), y.view(torch.int16))
+    assert not out_pad[:, n:].any()
+
+
+def test_torch_custom_ops(hc):
+    import paper_2412_08832_b200.torch_ops  # noqa: F401  (registers torch.ops.hadacore.*)
+    x = synthetic.generate(64, 1024, torch.bfloat16, 41).cuda()
+    y = torch.ops.hadacore.fwht(x, None)
+    assert torch.equal(y.view(torch.int16), hc.hadacore_fwht(x).view(torch.int16))
+    q, s = torch.ops.hadacore.fwht_quant(x, "e4m3", None)
+    q2, s2 = hc.hadacore_fwht_quant(x, "e4m3")
+    assert torch.equal(q.view(torch.uint8), q2.view(torch.uint8)) and torch.equal(s, s2)
+    xi = x.clone()
+    torch.ops.hadacore.fwht_(xi, None)
+    assert torch.equal(xi.view(torch.int16), y.view(torch.int16))
+    # autograd: d/dx sum(w * fwht(x)) = fwht(w) (H symmetric)
+    xr = x.float().to(torch.bfloat16).requires_grad_(True)
+    w = synthetic.generate(64, 1024, torch.bfloat16, 42).cuda()
+    (torch.ops.hadacore.fwht(xr, None).float() * w.float()).sum().backward()
+    assert rel_l2_rows(widen(xr.grad), widen(hc.hadacore_fwht(w))).max() <= TOL[torch.bfloat16]
+    # traceable by torch.compile (fake implementation registered)
+    f = torch.compile(lambda t: torch.ops.hadacore.fwht(t, None) * 2, fullgraph=True)
+    assert torch.equal(f(x).view(torch.int16), (y * 2).view(torch.int16))
