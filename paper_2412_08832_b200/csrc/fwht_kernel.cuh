@@ -436,6 +436,64 @@ __device__ __forceinline__ uint32_t quant4(float a, float b, float c, float d) {
                        0x5410);
   }
 }
+// Fast path of the fused quantization (rows whose max lies in [2^-100, hi]: finite,
+// non-zero, no NaN, no fp32-subnormal reciprocal): packed f32x2 math (FMUL2 / FFMA2)
+// and, for INT8, round-to-nearest-even by the 1.5 * 2^23 trick -- one FFMA2 rounds
+// the exact product v * m to an integer held in the low mantissa bits, so no F2I.
+// |v * m| <= Q (1 + 2^-8)(1 + 2^-22) < 127.5 for the 16-bit image (RNE of y, which is
+// <= amax (1 + 2^-8)) and the fp32 accumulators alike, so no clamp is needed.
+__device__ __forceinline__ void mul2(float& a, float& b, float m) {
+  asm("{.reg .b64 t, s;\n mov.b64 t, {%0,%1};\n mov.b64 s, {%2,%2};\n mul.rn.f32x2 t, t, s;\n mov.b64 {%0,%1}, t;}"
+      : "+f"(a), "+f"(b)
+      : "f"(m));
+}
+__device__ __forceinline__ void fma2(float& a, float& b, float m, float c) {
+  asm("{.reg .b64 t, s, u;\n mov.b64 t, {%0,%1};\n mov.b64 s, {%2,%2};\n mov.b64 u, {%3,%3};\n"
+      " fma.rn.f32x2 t, t, s, u;\n mov.b64 {%0,%1}, t;}"
+      : "+f"(a), "+f"(b)
+      : "f"(m), "f"(c));
+}
+__device__ __forceinline__ float rcp_ftz(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ bool quant_fast_range(float amax, float hi) {
+  return amax >= 0x1p-100f && amax <= hi;  // false for 0, NaN, Inf
+}
+template <int QT>
+__device__ __forceinline__ uint32_t quant4_fast(float a, float b, float c, float d, float m) {
+  if constexpr (QT == QT_E4M3) {
+    mul2(a, b, m);
+    mul2(c, d, m);
+    uint16_t lo, hi;
+    asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(lo) : "f"(b), "f"(a));
+    asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(hi) : "f"(d), "f"(c));
+    return uint32_t(lo) | (uint32_t(hi) << 16);
+  } else {
+    fma2(a, b, m, 12582912.f);  // 1.5 * 2^23
+    fma2(c, d, m, 12582912.f);
+    return __byte_perm(__byte_perm(__float_as_uint(a), __float_as_uint(b), 0x0040),
+                       __byte_perm(__float_as_uint(c), __float_as_uint(d), 0x0040), 0x5410);
+  }
+}
+// predicated global stores (no divergent branch around the epilogue)
+__device__ __forceinline__ void stg32_if(void* p, uint32_t v, bool pred) {
+  asm volatile("{.reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q st.global.b32 [%0], %1;}" ::"l"(p), "r"(v),
+               "r"(int(pred))
+               : "memory");
+}
+__device__ __forceinline__ void stg64_if(void* p, uint32_t a, uint32_t b, bool pred) {
+  asm volatile("{.reg .pred q;\n setp.ne.b32 q, %3, 0;\n @q st.global.v2.b32 [%0], {%1, %2};}" ::"l"(p), "r"(a),
+               "r"(b), "r"(int(pred))
+               : "memory");
+}
+__device__ __forceinline__ void stf32_if(float* p, float v, bool pred) {
+  asm volatile("{.reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q st.global.f32 [%0], %1;}" ::"l"(p), "f"(v),
+               "r"(int(pred))
+               : "memory");
+}
+
 // row scale s = amax / Q and the code multiplier Q / amax (amax = max |y| >= 0, Inf or NaN)
 template <int QT>
 __device__ __forceinline__ void row_scale_of(float amax, float& scale, float& inv) {
@@ -655,6 +713,12 @@ __global__ void __launch_bounds__((NT + 1) * 32, CTAS)
 
   // ---------------- consumers
   int it = 0;
+  // fused quantization fast path, in the accumulator domain (y = d * s_res):
+  // scale = max|d| |s_res| / Q, code multiplier = sign(s_res) Q / max|d|
+  const float q_qs = copysignf(qmax_of<QT == QT_NONE ? QT_E4M3 : QT>(), s_res);
+  const float q_ss = fabsf(s_res) / qmax_of<QT == QT_NONE ? QT_E4M3 : QT>();
+  (void)q_qs;
+  (void)q_ss;
   if constexpr (N == 128) {
     uint32_t A1[4], A2[4];
     make_const_a<DT>(0xFu, A1);  // H_16 over element bits {0,1,2,3}
@@ -701,21 +765,33 @@ __global__ void __launch_bounds__((NT + 1) * 32, CTAS)
         for (int u = 0; u < U; ++u) {
           const int f = f0 + u * NT;
           if constexpr (QT >= 0) {  // rows A (d[0..3] = elements 4l..4l+3) and B (d[4..7])
+            float am[2];
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
               float a = 0.f;
 #pragma unroll
               for (int e = 0; e < 4; ++e) a = absmax_nan(a, d[u][4 * h + e]);
-              float sc, inv;
-              row_scale_of<QT>(warp_absmax(a) * fabsf(s_res), sc, inv);
-              const float mul = s_res * inv;
-              int64_t i, j;
-              if (FLAT ? 2 * f + h < rows_left : tr.at(g, 2 * f + h, i, j)) {  // codes/scales: contiguous [rows, n]
-                const int64_t row = FLAT ? tr.i0 + 2 * f + h : i * g.m_inner + j;
-                *reinterpret_cast<uint32_t*>(out_q + row * N + lane * 4) =
-                    quant4<QT>(d[u][4 * h] * mul, d[u][4 * h + 1] * mul, d[u][4 * h + 2] * mul, d[u][4 * h + 3] * mul);
-                if (lane == 0) row_scale[row] = sc;
+              am[h] = warp_absmax(a);  // max |d| of the row; |y| = |d| |s_res|
+            }
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const float* v = &d[u][4 * h];
+              float sc;
+              uint32_t code;
+              if (quant_fast_range(am[h], 0x1p100f)) {
+                sc = am[h] * q_ss;
+                code = quant4_fast<QT>(v[0], v[1], v[2], v[3], q_qs * rcp_ftz(am[h]));
+              } else {
+                float inv;
+                row_scale_of<QT>(am[h] * fabsf(s_res), sc, inv);
+                const float mul = s_res * inv;
+                code = quant4<QT>(v[0] * mul, v[1] * mul, v[2] * mul, v[3] * mul);
               }
+              int64_t i = 0, j = 0;
+              const bool ok = FLAT ? 2 * f + h < rows_left : tr.at(g, 2 * f + h, i, j);
+              const int64_t row = FLAT ? tr.i0 + 2 * f + h : i * g.m_inner + j;  // codes/scales: contiguous [rows, n]
+              stg32_if(out_q + row * N + lane * 4, code, ok);
+              stf32_if(row_scale + row, sc, ok && lane == 0);
             }
           } else {
             if constexpr (FLAT) {
@@ -771,17 +847,27 @@ __global__ void __launch_bounds__((NT + 1) * 32, CTAS)
             float a = 0.f;
 #pragma unroll
             for (int e = 0; e < 8; ++e) a = absmax_nan(a, d[u][e]);
-            float sc, inv;
-            row_scale_of<QT>(warp_absmax(a) * fabsf(s_res), sc, inv);
-            const float mul = s_res * inv;
-            int64_t i, j;
-            if (FLAT ? r < rows_left : tr.at(g, r, i, j)) {
-              const int64_t row = FLAT ? tr.i0 + r : i * g.m_inner + j;
-              *reinterpret_cast<uint2*>(out_q + row * N + lane * 8) =
-                  make_uint2(quant4<QT>(d[u][0] * mul, d[u][1] * mul, d[u][2] * mul, d[u][3] * mul),
-                             quant4<QT>(d[u][4] * mul, d[u][5] * mul, d[u][6] * mul, d[u][7] * mul));
-              if (lane == 0) row_scale[row] = sc;
+            const float am = warp_absmax(a);  // max |d| of the row; |y| = |d| |s_res|
+            const float* v = d[u];
+            float sc;
+            uint32_t c0, c1;
+            if (quant_fast_range(am, 0x1p100f)) {
+              sc = am * q_ss;
+              const float mul = q_qs * rcp_ftz(am);
+              c0 = quant4_fast<QT>(v[0], v[1], v[2], v[3], mul);
+              c1 = quant4_fast<QT>(v[4], v[5], v[6], v[7], mul);
+            } else {
+              float inv;
+              row_scale_of<QT>(am * fabsf(s_res), sc, inv);
+              const float mul = s_res * inv;
+              c0 = quant4<QT>(v[0] * mul, v[1] * mul, v[2] * mul, v[3] * mul);
+              c1 = quant4<QT>(v[4] * mul, v[5] * mul, v[6] * mul, v[7] * mul);
             }
+            int64_t i = 0, j = 0;
+            const bool ok = FLAT ? r < rows_left : tr.at(g, r, i, j);
+            const int64_t row = FLAT ? tr.i0 + r : i * g.m_inner + j;
+            stg64_if(out_q + row * N + lane * 8, c0, c1, ok);
+            stf32_if(row_scale + row, sc, ok && lane == 0);
           } else {
             if constexpr (FLAT) {
               if (r < rows_left) stg128(out + (tr.i0 + r) * N + lane * 8, z[u][0], z[u][1], z[u][2], z[u][3]);
@@ -1148,15 +1234,29 @@ __global__ void __launch_bounds__((NT + 1) * 32, CTAS)
       }
       team_sync();
       float inv_r[RPT];
+      uint32_t fast_r = 0;  // bit k: row k takes the fast path
+      uint8_t* q_r[RPT];    // code row pointers (valid rows only)
+      uint32_t ok_r = 0;
       const TileRows tr(g, tile);
+      // image-domain fast range: the fp16 image holds Inf where y overflowed fp16
+      constexpr float kHi = DT == DT_F16 ? 65504.f : 0x1p100f;
 #pragma unroll
       for (int k = 0; k < RPT; ++k) {
         float a = 0.f;
         for (int w = 0; w < P; ++w) a = absmax_nan(a, red[(team * RPT + k) * P + w]);
         float sc;
-        row_scale_of<QT>(a, sc, inv_r[k]);
-        int64_t i, j;
-        if (wt == 0 && lane == 0 && tr.at(g, team + NTEAMS * k, i, j)) row_scale[i * g.m_inner + j] = sc;
+        if (quant_fast_range(a, kHi)) {
+          sc = a * (1.f / qmax_of<QT>());
+          inv_r[k] = qmax_of<QT>() * rcp_ftz(a);
+          fast_r |= 1u << k;
+        } else {
+          row_scale_of<QT>(a, sc, inv_r[k]);
+        }
+        int64_t i = 0, j = 0;
+        const bool ok = tr.at(g, team + NTEAMS * k, i, j);
+        ok_r |= uint32_t(ok) << k;
+        q_r[k] = out_q + (i * g.m_inner + j) * N + lane * 8;
+        stf32_if(row_scale + (i * g.m_inner + j), sc, ok && wt == 0 && lane == 0);
       }
       for (int i0 = wt; i0 < ITEMS1; i0 += P * U1) {
         uint32_t z[U1][4];
@@ -1167,18 +1267,26 @@ __global__ void __launch_bounds__((NT + 1) * 32, CTAS)
         }
 #pragma unroll
         for (int u = 0; u < U1; ++u) {
-          const int item = i0 + u * P, rl = item / C, r = team + NTEAMS * rl, c = item % C;
+          const int item = i0 + u * P, rl = item / C, c = item % C;
           float inv = 0.f;
+          uint8_t* qp = nullptr;
 #pragma unroll
           for (int k = 0; k < RPT; ++k)
-            if (k == rl) inv = inv_r[k];
+            if (k == rl) {
+              inv = inv_r[k];
+              qp = q_r[k];
+            }
           float v[8];
           unpack8<DT>(z[u], v);
-          int64_t i, j;
-          if (tr.at(g, r, i, j))
-            *reinterpret_cast<uint2*>(out_q + (i * g.m_inner + j) * N + c * 256 + lane * 8) =
-                make_uint2(quant4<QT>(v[0] * inv, v[1] * inv, v[2] * inv, v[3] * inv),
-                           quant4<QT>(v[4] * inv, v[5] * inv, v[6] * inv, v[7] * inv));
+          uint32_t c0, c1;
+          if ((fast_r >> rl) & 1u) {
+            c0 = quant4_fast<QT>(v[0], v[1], v[2], v[3], inv);
+            c1 = quant4_fast<QT>(v[4], v[5], v[6], v[7], inv);
+          } else {
+            c0 = quant4<QT>(v[0] * inv, v[1] * inv, v[2] * inv, v[3] * inv);
+            c1 = quant4<QT>(v[4] * inv, v[5] * inv, v[6] * inv, v[7] * inv);
+          }
+          stg64_if(qp + c * 256, c0, c1, (ok_r >> rl) & 1u);
         }
       }
       // (red[] is rewritten only after the next tile's phase-1 barrier: no race)

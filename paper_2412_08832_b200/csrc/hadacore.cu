@@ -13,6 +13,8 @@
 #include <cstring>
 #include <mutex>
 
+#include <type_traits>
+
 #include "../../include/hadacore.h"
 #include "fwht_kernel.cuh"
 
@@ -53,17 +55,24 @@ template <> struct Tuned<8192>  { static constexpr int nt = 16, tkb = 16, st = 6
 template <> struct Tuned<16384> { static constexpr int nt = 16, tkb = 64, st = 3, u = 1, ctas = 1; };
 template <> struct Tuned<32768> { static constexpr int nt = 16, tkb = 64, st = 3, u = 1, ctas = 1; };
 
+// Fused quantization (QT >= 0): its epilogue (row max, team barrier, code pass) makes
+// a tile's critical path longer, so more independent pipelines per SM win: 3 CTAs of
+// 8 consumer warps with 32 KiB tiles in a 2-stage ring (paired sweeps,
+// profiles/r01_quant_sweep*.txt: +20-60 % over the transform's table at n = 2^10..2^14).
+template <int N> struct TunedQ      { static constexpr int nt = 8, tkb = 32, st = 2, u = 1, ctas = 3; };
+template <> struct TunedQ<32768>    { static constexpr int nt = 16, tkb = 64, st = 3, u = 1, ctas = 1; };
+
 #ifdef HC_TUNE  // tools/tune.py: one configuration for every n, from -D macros
-template <int N>
+template <int N, int QT>
 struct Knobs { static constexpr int nt = HC_NT, tkb = HC_TILE_KB, st = HC_STAGES, u = HC_U, ctas = HC_CTAS; };
 #else
-template <int N>
-struct Knobs : Tuned<N> {};
+template <int N, int QT>
+struct Knobs : std::conditional_t<(QT >= 0), TunedQ<N>, Tuned<N>> {};
 #endif
 
-template <int N>
+template <int N, int QT = -1>
 struct Cfg {
-  using K = Knobs<N>;
+  using K = Knobs<N, QT>;
   static constexpr int nt = K::nt;
   static constexpr int rows = (K::tkb * 1024) / (2 * N) > 0 ? (K::tkb * 1024) / (2 * N) : 1;
   static constexpr int tile_bytes = rows * 2 * N;
@@ -185,7 +194,7 @@ bool ensure_smem_attr(Kern kern, int smem, std::atomic<uint64_t>& done, int dev)
 template <int N, int DT, int QT>
 hadacore_status_t launch(const void* in, void* out, uint8_t* out_q, float* row_scale, const Layout& L, float scale,
                          cudaStream_t stream) {
-  using C = Cfg<N>;
+  using C = Cfg<N, QT>;
   constexpr bool seg = seg_mode(N, C::rows);
   // + full[], done[][<=16] and the fused-quantization row-max scratch (one float per warp)
   constexpr int smem = C::stages * C::tile_bytes + int(sizeof(SchedCtl)) + 17 * C::stages * 8 +

@@ -68,12 +68,24 @@ def run(reps=15, ns=None, repeats=3):
         b.synchronize()
         return a.elapsed_time(b) / reps
 
+    # TUNE_QT=e4m3|int8: time the fused quantization entry instead (3 B/element + 4 B/row)
+    qt = {"": None, "e4m3": 0, "int8": 1}[os.environ.get("TUNE_QT", "")]
+    qbuf = torch.empty(elems, dtype=torch.uint8, device="cuda") if qt is not None else None
+    sbuf = torch.empty(elems // 128, dtype=torch.float32, device="cuda") if qt is not None else None
     fns = {}
     for path in libs:
         lib = ctypes.CDLL(path)
-        f = lib.hadacore_fwht
-        f.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int,
-                      ctypes.c_float, ctypes.c_void_p]
+        if qt is None:
+            f = lib.hadacore_fwht
+            f.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int,
+                          ctypes.c_float, ctypes.c_void_p]
+        else:
+            fq = lib.hadacore_fwht_quant
+            fq.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64,
+                           ctypes.c_int, ctypes.c_int, ctypes.c_float, ctypes.c_void_p]
+
+            def f(i, o, m, n, dt, sc, stream, fq=fq):  # o is ignored: codes/scales go to qbuf/sbuf
+                return fq(i, qbuf.data_ptr() if o == dst.data_ptr() else o, sbuf.data_ptr(), m, n, dt, qt, sc, stream)
         fns[os.path.basename(path)[6:-3]] = f
     samples = {}
     mem = []
@@ -92,8 +104,9 @@ def run(reps=15, ns=None, repeats=3):
                     b.record()
                 torch.cuda.synchronize()
             for (dt, n), (a, b) in zip(pairs, evs):
+                nbytes = 4.0 * elems if qt is None else 3.0 * elems + 4.0 * elems / n
                 samples.setdefault(name, {}).setdefault(f"{'f16' if dt == 0 else 'bf16'}_{n}", []).append(
-                    4.0 * elems / (a.elapsed_time(b) * 1e-3) / 1e9)
+                    nbytes / (a.elapsed_time(b) * 1e-3) / 1e9)
     base = sorted(fns)[0] if "tuned" not in fns else "tuned"
     for name in fns:
         rel = {k: statistics.median([a / b for a, b in zip(v, samples[base][k])]) for k, v in samples[name].items()}
@@ -107,7 +120,7 @@ def run(reps=15, ns=None, repeats=3):
     import paper_2412_08832_b200 as hc
     small = torch.randn(1 << 20, device="cuda")
     for name, f in fns.items():
-        if "nocompute" in name:
+        if "nocompute" in name or qt is not None:
             continue
         worst = 0.0
         for dt, tdt in ((0, torch.float16), (1, torch.bfloat16)):
@@ -120,6 +133,17 @@ def run(reps=15, ns=None, repeats=3):
                 err = ((o.float() - ref).norm(dim=1) / ref.norm(dim=1)).max().item()
                 worst = max(worst, err)
         print(f"agreement {name}: max rel-L2 vs default library {worst:.2e}")
+    if qt is not None:
+        x = small.to(torch.bfloat16)
+        for name, f in fns.items():
+            bad = 0
+            for n in (ns or NS):
+                xv = x.view(-1, n)
+                q_ref, s_ref = hc.hadacore_fwht_quant(xv, qtype=["e4m3", "int8"][qt])
+                o = torch.empty(xv.numel(), dtype=torch.uint8, device="cuda")
+                assert f(xv.data_ptr(), o.data_ptr(), xv.shape[0], n, 1, 1.0 / n ** 0.5, st) == 0
+                bad += int((o.view(-1, n) != q_ref.view(torch.uint8)).sum())
+            print(f"agreement {name}: quant codes differing from the default library: {bad}")
     results = {nm: {k: round(statistics.median(v)) for k, v in d.items()} for nm, d in samples.items()}
     spread = {nm: {k: round(max(v) - min(v)) for k, v in d.items()} for nm, d in samples.items()}
     for nm, res in results.items():
