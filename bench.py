@@ -33,6 +33,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "FWHT HBM GB/s vs n=2^7..2^15 (bf16/fp16) at 1/2/4/8 B200; % of 8 TB/s"
 NS = [1 << k for k in range(7, 16)]
+SMALL_NS = [1 << k for k in range(1, 7)]  # NEXT-2: rows shorter than the paper's 2^7 floor
 ELEMS = 1 << 28
 NOMINAL_HBM_GBS = 8000.0
 FALLBACK_HBM_GBS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback
@@ -48,9 +49,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
-    ap.add_argument("--workload", choices=["fwht", "quant-e4m3", "quant-int8", "qk-rotate"], default="fwht",
+    ap.add_argument("--workload", choices=["fwht", "quant-e4m3", "quant-int8", "qk-rotate", "small"], default="fwht",
                     help="fwht = the metric's C3 sweep (default); quant-* = the fused FWHT + per-row "
-                         "quantization row (NEXT-1) on the same inputs")
+                         "quantization row (NEXT-1) on the same inputs; small = n=2^1..2^6 (NEXT-2)")
     return ap.parse_args()
 
 
@@ -229,12 +230,16 @@ def reference_arm(args, rank, world):
 def config_block(args, world):
     wl = ("C3 size sweep: n=2^7..2^15 x {fp16, bf16}, 2^28 elements per (n, dtype) per GPU, "
           "out-of-place, normalized (scale=1/sqrt(n))")
+    ns = SMALL_NS if getattr(args, "workload", "fwht") == "small" else NS
+    if getattr(args, "workload", "fwht") == "small":
+        wl = ("NEXT-2 small sizes: n=2^1..2^6 x {fp16, bf16}, 2^28 elements per (n, dtype) per GPU, "
+              "out-of-place, normalized (scale=1/sqrt(n))")
     if getattr(args, "workload", "fwht") == "qk-rotate":
         wl = ("QK rotation: n=2^7..2^15 x {fp16, bf16}; a 2^28-element QKV buffer viewed as [T, 3, H, n], "
               "H = max(1, 4096/n); the Q and K heads (2/3 of it) transformed in place, normalized")
     return {"workload": wl,
-            "elements_per_launch": args.elems, "ns": NS, "dtypes": ["fp16", "bf16"],
-            "launches_per_step": 2 * len(NS), "path": getattr(args, "workload", "fwht"),
+            "elements_per_launch": args.elems, "ns": ns, "dtypes": ["fp16", "bf16"],
+            "launches_per_step": 2 * len(ns), "path": getattr(args, "workload", "fwht"),
             "l2": "no flush: every launch reads a 512 MiB input and writes a 512 MiB output (> 126 MB L2)",
             "parallelism": f"row-sharded x{world}, no collective on the hot path" if world > 1 else "single GPU"}
 
@@ -266,7 +271,8 @@ def main():
         xin[dt] = buf
     obuf = torch.empty(args.elems, dtype=torch.float16, device=dev)
     stream = torch.cuda.current_stream(dev)
-    pairs = [(dt, n) for dt in (torch.float16, torch.bfloat16) for n in NS]
+    ns = SMALL_NS if args.workload == "small" else NS
+    pairs = [(dt, n) for dt in (torch.float16, torch.bfloat16) for n in ns]
     quant = args.workload.startswith("quant")
     qtype = args.workload.split("-")[1] if quant else None
     if quant:
@@ -431,6 +437,8 @@ def main():
     if rank == 0:
         metric = METRIC if not quant else (f"Fused FWHT + per-row {qtype.upper()} quantization HBM GB/s vs "
                                            "n=2^7..2^15 (bf16/fp16 in, 8-bit codes + fp32 row scales out)")
+        if args.workload == "small":
+            metric = "FWHT HBM GB/s vs n=2^1..2^6 (bf16/fp16), rows shorter than the paper's 2^7 (NEXT-2)"
         if rotate:
             metric = ("In-place FWHT of the Q and K heads of fused QKV activations [T, 3, H, n] (strided rows) "
                       "HBM GB/s vs n=2^7..2^15")

@@ -11,7 +11,10 @@
  * [Sec. 2.2]).  H_n is symmetric, so this equals the right multiply in * H_n.
  * `scale` is the WHOLE multiplier on the +-1 matrix: pass 1/sqrt(n) for the
  * normalized (orthonormal) transform of P:41 ("+-1/sqrt(d) ... when normalized").
- * n is a power of two in [2^7, 2^15] (the paper's range, P:97, P:128 [Sec. 3.2]).
+ * n is a power of two in [2^7, 2^15] (the paper's range, P:97, P:128 [Sec. 3.2]) or,
+ * for hadacore_fwht / hadacore_fwht_host only, in [2, 2^6] (
+ * SPEC S:49's domain 2 <= d; fp32 register butterflies, DESIGN.md "Rows shorter
+ * than 128").
  *
  * Layout: `in` and `out` are row-major m x n matrices of 16-bit floats (IEEE
  * binary16 or bfloat16; or binary32 for the HADACORE_F32 debug path), contiguous,
@@ -66,7 +69,8 @@ typedef enum {
 
 typedef enum {
   HADACORE_OK = 0,
-  HADACORE_ERR_INVALID_N = 1,   /* n is not a power of two in [128, 32768] */
+  HADACORE_ERR_INVALID_N = 1,   /* n is not a power of two in [2, 32768] ([128, 32768] for the
+                                   strided and quantizing entry points) */
   HADACORE_ERR_INVALID_M = 2,   /* m < 0, or m * n * element size overflows int64 */
   HADACORE_ERR_NULL = 3,        /* in or out is NULL while m > 0 */
   HADACORE_ERR_MISALIGNED = 4,  /* in or out is not 16-byte aligned */
@@ -79,7 +83,9 @@ typedef enum {
 
 /*
  * out[i, :] = scale * H_n * in[i, :] for i in [0, m), on `stream` (device buffers).
- * m == 0 returns HADACORE_OK without launching anything.
+ * n = 2..2^15.  m == 0 returns HADACORE_OK without launching anything.  Only the
+ * buffer start must be 16-byte aligned: for n < 8 the total m * n * 2 bytes need
+ * not be a multiple of 16 (bytes past the last row are never touched).
  */
 hadacore_status_t hadacore_fwht(const void* in, void* out, int64_t m, int64_t n,
                                 hadacore_dtype_t dtype, float scale, hadacore_stream_t stream);
@@ -94,7 +100,8 @@ hadacore_status_t hadacore_fwht(const void* in, void* out, int64_t m, int64_t n,
  *   in_host / out_host: m x n row-major 16-bit matrices in host memory (pinned
  *     memory gives full PCIe bandwidth; pageable works but is slower).  May be equal.
  *   workspace: device buffer of workspace_bytes >= 2 * 2 * n bytes (two rows),
- *     16-byte aligned; larger workspaces mean larger copy blocks.
+ *     16-byte aligned; larger workspaces mean larger copy blocks (for n < 8 the
+ *     blocks hold multiples of 16 / (2 n) rows so that they stay 16-byte aligned).
  * Same validation and errors as hadacore_fwht, plus HADACORE_ERR_WORKSPACE.
  */
 hadacore_status_t hadacore_fwht_host(const void* in_host, void* out_host, int64_t m, int64_t n,
@@ -113,7 +120,7 @@ hadacore_status_t hadacore_fwht_host(const void* in_host, void* out_host, int64_
  * may not overlap (stride_inner >= n when m_inner > 1; stride_outer >= (m_inner-1) *
  * stride_inner + n when m_outer > 1) -- else HADACORE_ERR_INVALID_M.  in == out
  * requires identical strides; otherwise the two extents may not overlap
- * (HADACORE_ERR_OVERLAP).  fp16/bf16 only.  Other rules as hadacore_fwht.
+ * (HADACORE_ERR_OVERLAP).  fp16/bf16 and n = 2^7..2^15 only.  Other rules as hadacore_fwht.
  */
 hadacore_status_t hadacore_fwht_strided(const void* in, void* out, int64_t m_outer, int64_t m_inner,
                                         int64_t in_stride_outer, int64_t in_stride_inner,
@@ -129,7 +136,8 @@ hadacore_status_t hadacore_fwht_strided(const void* in, void* out, int64_t m_out
  *     out_q[i, j]  = round(y_j / row_scale[i])   (E4M3 saturating / INT8 clamped)
  * so out_q[i, j] * row_scale[i] ~= y_j.  A row containing Inf/NaN gets a non-finite
  * row_scale.  out_q: m x n bytes, row-major, 16-byte aligned; row_scale: m floats
- * (fp32).  Neither may overlap `in`.  HBM traffic: 2 B read + 1 B written per element.
+ * (fp32).  Neither may overlap `in`.  n = 2^7..2^15.  HBM traffic: 2 B read + 1 B
+ * written per element.
  * Same validation, stream and error behaviour as hadacore_fwht; qtype outside the
  * enum, or dtype HADACORE_F32, returns HADACORE_ERR_DTYPE.
  */

@@ -1337,8 +1337,13 @@ __global__ void __launch_bounds__(512) fwht_f32_kernel(const float* __restrict__
   pdl_wait();
   for (int64_t r0 = int64_t(blockIdx.x) * ROWS; r0 < m; r0 += int64_t(gridDim.x) * ROWS) {
     const int rows = (m - r0) < ROWS ? int(m - r0) : ROWS;
-    for (int i = threadIdx.x; i < rows * N / 4; i += blockDim.x)
-      reinterpret_cast<float4*>(srow)[i] = reinterpret_cast<const float4*>(in + r0 * N)[i];
+    const int cnt = rows * N;  // a multiple of 4 unless n < 4 (then copied by element)
+    if (cnt % 4 == 0) {
+      for (int i = threadIdx.x; i < cnt / 4; i += blockDim.x)
+        reinterpret_cast<float4*>(srow)[i] = reinterpret_cast<const float4*>(in + r0 * N)[i];
+    } else {
+      for (int i = threadIdx.x; i < cnt; i += blockDim.x) srow[i] = in[r0 * N + i];
+    }
     __syncthreads();
     for (int h = 1; h < N; h *= 2) {
       for (int idx = threadIdx.x; idx < rows * (N / 2); idx += blockDim.x) {
@@ -1350,13 +1355,17 @@ __global__ void __launch_bounds__(512) fwht_f32_kernel(const float* __restrict__
       }
       __syncthreads();
     }
-    for (int i = threadIdx.x; i < rows * N / 4; i += blockDim.x) {
-      float4 v = reinterpret_cast<float4*>(srow)[i];
-      v.x *= scale;
-      v.y *= scale;
-      v.z *= scale;
-      v.w *= scale;
-      reinterpret_cast<float4*>(out + r0 * N)[i] = v;
+    if (cnt % 4 == 0) {
+      for (int i = threadIdx.x; i < cnt / 4; i += blockDim.x) {
+        float4 v = reinterpret_cast<float4*>(srow)[i];
+        v.x *= scale;
+        v.y *= scale;
+        v.z *= scale;
+        v.w *= scale;
+        reinterpret_cast<float4*>(out + r0 * N)[i] = v;
+      }
+    } else {
+      for (int i = threadIdx.x; i < cnt; i += blockDim.x) out[r0 * N + i] = srow[i] * scale;
     }
     __syncthreads();
   }

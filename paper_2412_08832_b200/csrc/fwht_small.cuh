@@ -1,0 +1,247 @@
+// fwht_small.cuh -- sm_100a kernel for rows shorter than 128 elements (n = 2..64),
+// SURVEY.md 8(f) NEXT-2 ("size breadth: n = 2..64", SPEC S:49's domain 2 <= d).
+// "P:NN" = /root/reference/PAPER.md line NN.
+//
+// Why not the tensor cores here: a 256-element mma fragment would hold 256/n rows,
+// and with two m16n8k16 stages every fragment bit but one is contracted by one of
+// them, so a row bit would be contracted with a
+// structural-zero I_2 factor -- 0 * Inf = NaN would leak a non-finite row into its
+// neighbours (reading R13).  With k = log2 n <= 6 butterfly stages the work is
+// ~k + 3 fp32 instructions per element, far below the issue rate that the HBM
+// stream needs, so the P:50-64 listing runs as fp32 register
+// butterflies.
+//
+// Layout of the work: the producer warp streams contiguous 1-D byte ranges
+// HBM -> shared memory (cp.async.bulk, UBLKCP) into a STAGES-deep ring and writes
+// finished stages back with 1-D bulk stores (shared -> global), like
+// fwht_rows_kernel.  A consumer lane owns one ITEM: for n <= 8 one 16-byte granule
+// (8 elements = 8/n whole rows), for n >= 16 one whole row of G = n/8 granules.
+// Bank conflicts of the per-lane row reads (row stride 2n bytes) are avoided by
+// reading granule j ^ c (c a lane constant, so 8 consecutive lanes touch 8
+// different 16-byte bank groups); the granule-bit butterflies then use the sign
+// trick of DESIGN.md (a butterfly with its second operand negated is the butterfly
+// followed by a swap across that bit), so the result for granule j ^ c lands in
+// register slot j up to a known sign, which is folded into the final scale; slot
+// j is written back to the address it was read from.
+#pragma once
+#include "fwht_kernel.cuh"
+
+namespace hadacore {
+
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_addr(src)),
+               "r"(bytes)
+               : "memory");
+}
+
+template <int DT>
+__device__ __forceinline__ void unpack2(uint32_t w, float& lo, float& hi) {
+  if constexpr (DT == DT_F16) {
+    const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w));
+    lo = f.x;
+    hi = f.y;
+  } else {
+    lo = __uint_as_float(w << 16);
+    hi = __uint_as_float(w & 0xffff0000u);
+  }
+}
+
+// Rows of N = 2..64 elements; TILE_BYTES per ring stage, NT consumer warps, U items
+// per lane in flight.
+template <int N, int DT, int TILE_BYTES, int STAGES, int NT, int U>
+__global__ void __launch_bounds__((NT + 1) * 32, 1)
+    fwht_small_kernel(const uint16_t* __restrict__ in, uint16_t* __restrict__ out, int64_t total_bytes,
+                      int64_t num_tiles, float scale) {
+  constexpr int K = log2_n<N>();
+  constexpr int G = N >= 8 ? N / 8 : 1;            // granules per item
+  constexpr int ITEM_BYTES = 16 * G;
+  constexpr int ITEMS = TILE_BYTES / ITEM_BYTES;   // items per full tile
+  constexpr int KG = N >= 16 ? K - 3 : 0;          // granule bits of an item
+  constexpr int KE = K < 3 ? K : 3;                // element bits inside a granule
+  static_assert(TILE_BYTES % ITEM_BYTES == 0 && STAGES <= 16, "tile layout");
+
+  extern __shared__ __align__(1024) uint8_t smem[];
+  SchedCtl* ctl = reinterpret_cast<SchedCtl*>(smem + STAGES * TILE_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * TILE_BYTES + sizeof(SchedCtl));
+  uint64_t* done = full + STAGES;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    mbar_init(&ctl->clc_bar, 1);
+#pragma unroll
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&done[s], NT);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    fence_proxy_async_smem();
+  }
+  __syncthreads();
+
+  // bytes of tile t, and its 16-byte-multiple prefix moved by the bulk engine (the
+  // rest, < 16 bytes, exists only for n <= 4 and is handled by one consumer lane)
+  auto tile_bytes = [&](int64_t t) -> int {
+    const int64_t left = total_bytes - t * TILE_BYTES;
+    return int(left < TILE_BYTES ? left : TILE_BYTES);
+  };
+
+  pdl_launch_dependents();
+  if (warp == NT) {
+    // ---------------- producer: 1-D bulk loads into the ring, 1-D bulk stores out of it
+    if (lane == 0) {
+      pdl_wait();  // the previous kernel on the stream has completed
+      const uint64_t pol = policy_evict_first();
+      uint32_t clc_phase = 0;
+      int64_t tile = blockIdx.x;
+      auto advance = [&](int64_t t) -> int64_t {
+        if constexpr (kClc) {
+          return clc_result(ctl, clc_phase);
+        } else {
+          return t + gridDim.x;
+        }
+      };
+      auto load = [&](int st, int64_t t) {
+        const uint32_t b16 = uint32_t(tile_bytes(t)) & ~15u;
+        mbar_arrive_expect_tx(&full[st], b16);
+        if (b16) bulk_g2s(smem + st * TILE_BYTES, reinterpret_cast<const uint8_t*>(in) + t * TILE_BYTES, b16, &full[st], pol);
+      };
+      bool ended = false;
+      for (int k = 0; k < STAGES; ++k) {  // fill the ring
+        if (tile < 0 || tile >= num_tiles) {
+          ctl->stage_tile[k] = -1;
+          mbar_arrive(&full[k]);
+          ended = true;
+          break;
+        }
+        ctl->stage_tile[k] = int(tile);
+        if constexpr (kClc) clc_request(ctl);
+        load(k, tile);
+        tile = advance(tile);
+      }
+      for (int it = 0;; ++it) {
+        const int s = it % STAGES;
+        const int64_t t = ctl->stage_tile[s];
+        if (t < 0) break;
+        mbar_wait(&done[s], (it / STAGES) & 1);
+        const uint32_t b16 = uint32_t(tile_bytes(t)) & ~15u;
+        if (b16) bulk_s2g(reinterpret_cast<uint8_t*>(out) + t * TILE_BYTES, smem + s * TILE_BYTES, b16);
+        bulk_commit();
+        if (ended) continue;
+        if (tile < 0 || tile >= num_tiles) {
+          ctl->stage_tile[s] = -1;
+          mbar_arrive(&full[s]);
+          ended = true;
+          continue;
+        }
+        ctl->stage_tile[s] = int(tile);
+        if constexpr (kClc) clc_request(ctl);
+        bulk_wait_read<0>();  // the store just issued (and older ones) has read the stage
+        load(s, tile);
+        tile = advance(tile);
+      }
+      bulk_wait_all();
+    }
+    return;
+  }
+
+  // ---------------- consumers
+  // granule XOR of this lane: 8 consecutive lanes read 8 distinct bank groups
+  constexpr int LG = KG;  // log2 G
+  const uint32_t c = G > 1 ? (uint32_t(lane) >> (3 - LG)) & uint32_t(G - 1) : 0u;
+  // per-slot scale: scale * (-1)^popcount((j ^ c) & c) (sign left by the swapped butterflies)
+  float sc[G];
+#pragma unroll
+  for (int j = 0; j < G; ++j) sc[j] = (__popc((uint32_t(j) ^ c) & c) & 1) ? -scale : scale;
+  float sg[KG > 0 ? KG : 1];  // sign of the second operand of the granule-bit butterflies
+#pragma unroll
+  for (int b = 0; b < KG; ++b) sg[b] = ((c >> b) & 1u) ? -1.f : 1.f;
+
+  for (int it = 0;; ++it) {
+    const int s = it % STAGES;
+    mbar_wait(&full[s], (it / STAGES) & 1);
+    const int64_t tile = ctl->stage_tile[s];
+    if (tile < 0) break;
+    uint8_t* const tb = smem + s * TILE_BYTES;
+    const int bytes = tile_bytes(tile);
+    const int b16 = bytes & ~15;
+    const int items = (bytes + ITEM_BYTES - 1) / ITEM_BYTES;
+    for (int i0 = warp * 32 + lane; i0 < items; i0 += NT * 32 * U) {
+      float v[U][8 * G];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int item = i0 + u * NT * 32;
+        if (item >= items) continue;
+        const uint8_t* p = tb + item * ITEM_BYTES;
+#pragma unroll
+        for (int j = 0; j < G; ++j) {
+          uint32_t w[4];
+          if (N <= 4 && item * 16 + 16 > b16) {
+            // partial last granule (n <= 4, total bytes not a multiple of 16): whole rows
+            // of 4 or 8 bytes straight from global memory (after the producer's pdl_wait
+            // via the full barrier), zero-filled
+            const uint32_t* gsrc =
+                reinterpret_cast<const uint32_t*>(reinterpret_cast<const uint8_t*>(in) + tile * TILE_BYTES + item * 16);
+            const int nw = (bytes - item * 16) / 4;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) w[q] = q < nw ? gsrc[q] : 0u;
+          } else {
+            lds128(p + 16 * (uint32_t(j) ^ c), w[0], w[1], w[2], w[3]);
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q) unpack2<DT>(w[q], v[u][8 * j + 2 * q], v[u][8 * j + 2 * q + 1]);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        // element bits (inside a granule; for n <= 8 each row of n elements is
+        // contiguous in the granule, so bits 0..k-1 never cross rows): P:50-64 butterflies
+#pragma unroll
+        for (int b = 0; b < KE; ++b)
+#pragma unroll
+          for (int e = 0; e < 8 * G; ++e)
+            if (!(e & (1 << b))) {
+              const float p0 = v[u][e], p1 = v[u][e | (1 << b)];
+              v[u][e] = p0 + p1;
+              v[u][e | (1 << b)] = p0 - p1;
+            }
+        // granule bits: butterflies with the second operand times sg[b] (= the plain
+        // butterfly followed by a swap across bit b when c has bit b set)
+#pragma unroll
+        for (int b = 0; b < KG; ++b)
+#pragma unroll
+          for (int e = 0; e < 8 * G; ++e)
+            if (!(e & (8 << b))) {
+              const float p0 = v[u][e], p1 = v[u][e | (8 << b)];
+              v[u][e] = fmaf(p1, sg[b], p0);
+              v[u][e | (8 << b)] = fmaf(p1, -sg[b], p0);
+            }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int item = i0 + u * NT * 32;
+        if (item >= items) continue;
+        uint8_t* p = tb + item * ITEM_BYTES;
+#pragma unroll
+        for (int j = 0; j < G; ++j) {
+          uint32_t w[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) w[q] = pack2<DT>(v[u][8 * j + 2 * q] * sc[j], v[u][8 * j + 2 * q + 1] * sc[j]);
+          if (N <= 4 && item * 16 + 16 > b16) {
+            uint32_t* gdst = reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(out) + tile * TILE_BYTES + item * 16);
+            const int nw = (bytes - item * 16) / 4;
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              if (q < nw) gdst[q] = w[q];
+          } else {
+            stg_sh128(p + 16 * (uint32_t(j) ^ c), w);
+          }
+        }
+      }
+    }
+    fence_proxy_async_smem();  // this warp's smem writes -> visible to the bulk store
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&done[s]);
+  }
+}
+
+}  // namespace hadacore

@@ -17,6 +17,7 @@
 
 #include "../../include/hadacore.h"
 #include "fwht_kernel.cuh"
+#include "fwht_small.cuh"
 
 namespace hadacore {
 namespace {
@@ -61,6 +62,13 @@ template <> struct Tuned<32768> { static constexpr int nt = 16, tkb = 64, st = 3
 // profiles/r01_quant_sweep*.txt: +20-60 % over the transform's table at n = 2^10..2^14).
 template <int N> struct TunedQ      { static constexpr int nt = 8, tkb = 32, st = 2, u = 1, ctas = 3; };
 template <> struct TunedQ<32768>    { static constexpr int nt = 16, tkb = 64, st = 3, u = 1, ctas = 1; };
+
+// Rows shorter than 128 (NEXT-2, fwht_small_kernel): 8 consumer warps, 32 KiB tiles,
+// 4-stage ring; U items per lane in flight (an item is 8 elements for n <= 8, a row
+// of n elements otherwise).
+template <int N> struct TunedS {
+  static constexpr int nt = 8, tkb = 32, st = 4, u = N <= 8 ? 4 : (N == 16 ? 2 : 1);
+};
 
 #ifdef HC_TUNE  // tools/tune.py: one configuration for every n, from -D macros
 template <int N, int QT>
@@ -242,6 +250,39 @@ hadacore_status_t launch(const void* in, void* out, uint8_t* out_q, float* row_s
   return cudaPeekAtLastError() == cudaSuccess ? HADACORE_OK : HADACORE_ERR_CUDA;
 }
 
+template <int N, int DT>
+hadacore_status_t launch_small(const void* in, void* out, int64_t m, float scale, cudaStream_t stream) {
+  using T = TunedS<N>;
+  constexpr int tile = T::tkb * 1024;
+  constexpr int smem = T::st * tile + int(sizeof(SchedCtl)) + 2 * T::st * 8;
+  static std::atomic<uint64_t> attr_done{0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return HADACORE_ERR_CUDA;
+  auto kern = fwht_small_kernel<N, DT, tile, T::st, T::nt, T::u>;
+  if (!ensure_smem_attr(kern, smem, attr_done, dev)) return HADACORE_ERR_CUDA;
+  const int64_t total = m * N * 2;
+  const int64_t tiles = (total + tile - 1) / tile;
+  const int64_t max_ctas = kClc ? int64_t(INT32_MAX) : int64_t(sm_count(dev));
+  const int grid = int(tiles < max_ctas ? tiles : max_ctas);
+  if (launch_pdl(kern, grid, (T::nt + 1) * 32, smem, stream, static_cast<const uint16_t*>(in),
+                 static_cast<uint16_t*>(out), total, tiles, scale) != cudaSuccess)
+    return HADACORE_ERR_CUDA;
+  return cudaPeekAtLastError() == cudaSuccess ? HADACORE_OK : HADACORE_ERR_CUDA;
+}
+
+template <int DT>
+hadacore_status_t dispatch_small(const void* in, void* out, int64_t m, int64_t n, float scale, cudaStream_t st) {
+  switch (n) {
+    case 2: return launch_small<2, DT>(in, out, m, scale, st);
+    case 4: return launch_small<4, DT>(in, out, m, scale, st);
+    case 8: return launch_small<8, DT>(in, out, m, scale, st);
+    case 16: return launch_small<16, DT>(in, out, m, scale, st);
+    case 32: return launch_small<32, DT>(in, out, m, scale, st);
+    case 64: return launch_small<64, DT>(in, out, m, scale, st);
+    default: return HADACORE_ERR_INVALID_N;
+  }
+}
+
 template <int DT, int QT>
 hadacore_status_t dispatch_n(const void* in, void* out, uint8_t* q, float* rs, const Layout& L, int64_t n, float scale,
                              cudaStream_t st) {
@@ -261,7 +302,10 @@ hadacore_status_t dispatch_n(const void* in, void* out, uint8_t* q, float* rs, c
 
 Layout contiguous(int64_t m, int64_t n) { return Layout{m, 1, n, n, n, n}; }
 
-bool valid_n(int64_t n) { return n >= 128 && n <= 32768 && (n & (n - 1)) == 0; }
+// hadacore_fwht / hadacore_fwht_host: n = 2..2^15 (n < 128: NEXT-2, fwht_small_kernel);
+// the strided and fused-quantization entry points: the paper's range 2^7..2^15.
+bool valid_n(int64_t n) { return n >= 2 && n <= 32768 && (n & (n - 1)) == 0; }
+bool valid_n_paper(int64_t n) { return n >= 128 && n <= 32768 && (n & (n - 1)) == 0; }
 
 size_t elem_size(int dtype) { return dtype == HADACORE_F32 ? 4 : 2; }
 
@@ -284,6 +328,12 @@ hadacore_status_t launch_f32(const void* in, void* out, int64_t m, float scale, 
 
 hadacore_status_t dispatch_f32(const void* in, void* out, int64_t m, int64_t n, float scale, cudaStream_t st) {
   switch (n) {
+    case 2: return launch_f32<2>(in, out, m, scale, st);
+    case 4: return launch_f32<4>(in, out, m, scale, st);
+    case 8: return launch_f32<8>(in, out, m, scale, st);
+    case 16: return launch_f32<16>(in, out, m, scale, st);
+    case 32: return launch_f32<32>(in, out, m, scale, st);
+    case 64: return launch_f32<64>(in, out, m, scale, st);
     case 128: return launch_f32<128>(in, out, m, scale, st);
     case 256: return launch_f32<256>(in, out, m, scale, st);
     case 512: return launch_f32<512>(in, out, m, scale, st);
@@ -319,6 +369,9 @@ hadacore_status_t validate(const void* in, const void* out, int64_t m, int64_t n
 hadacore_status_t run(const void* in, void* out, int64_t m, int64_t n, int dtype, float scale,
                       cudaStream_t st) {
   if (dtype == HADACORE_F32) return dispatch_f32(in, out, m, n, scale, st);
+  if (n < 128)
+    return dtype == HADACORE_F16 ? dispatch_small<DT_F16>(in, out, m, n, scale, st)
+                                 : dispatch_small<DT_BF16>(in, out, m, n, scale, st);
   const Layout L = contiguous(m, n);
   return dtype == HADACORE_F16 ? dispatch_n<DT_F16, QT_NONE>(in, out, nullptr, nullptr, L, n, scale, st)
                                : dispatch_n<DT_BF16, QT_NONE>(in, out, nullptr, nullptr, L, n, scale, st);
@@ -362,7 +415,7 @@ extern "C" hadacore_status_t hadacore_fwht_strided(const void* in, void* out, in
                                                    int64_t out_stride_outer, int64_t out_stride_inner, int64_t n,
                                                    hadacore_dtype_t dtype, float scale, hadacore_stream_t stream) {
   if (dtype != HADACORE_F16 && dtype != HADACORE_BF16) return HADACORE_ERR_DTYPE;
-  if (!valid_n(n)) return HADACORE_ERR_INVALID_N;
+  if (!valid_n_paper(n)) return HADACORE_ERR_INVALID_N;
   if (m_outer < 0 || m_inner < 0 || m_outer > (int64_t(1) << 31) || m_inner > (int64_t(1) << 31))
     return HADACORE_ERR_INVALID_M;
   if (!std::isfinite(scale)) return HADACORE_ERR_SCALE;
@@ -393,6 +446,7 @@ extern "C" hadacore_status_t hadacore_fwht_quant(const void* in, void* out_q, fl
                                                  float scale, hadacore_stream_t stream) {
   if (qtype != HADACORE_Q_E4M3 && qtype != HADACORE_Q_INT8) return HADACORE_ERR_DTYPE;
   if (dtype == HADACORE_F32) return HADACORE_ERR_DTYPE;  // the fused path takes 16-bit inputs
+  if (!valid_n_paper(n)) return HADACORE_ERR_INVALID_N;
   // validate `in` (and m, n, dtype, scale) exactly like hadacore_fwht, with out = in
   const hadacore_status_t v = validate(in, in, m, n, int(dtype), scale, true);
   if (v != HADACORE_OK || m == 0) return v;
@@ -420,13 +474,17 @@ extern "C" hadacore_status_t hadacore_fwht_host(const void* in_host, void* out_h
   // and several streams keep both PCIe directions busy (short pipeline fill/drain).
   constexpr size_t kBlockBytes = size_t(16) << 20;
   constexpr int kMaxSlots = 4;
-  int slots = int(workspace_bytes / row_bytes >= kMaxSlots ? kMaxSlots : 2);
+  // slot offsets stay 16-byte aligned: rows of < 16 bytes (n < 8) go in groups of
+  // 16 / row_bytes rows
+  const int64_t align_rows = row_bytes >= 16 ? 1 : int64_t(16 / row_bytes);
+  int slots = int(workspace_bytes / row_bytes >= size_t(kMaxSlots * align_rows) ? kMaxSlots : 2);
   int64_t rows_per_slot = int64_t((workspace_bytes / size_t(slots)) / row_bytes);
   const int64_t cap_rows = int64_t(kBlockBytes / row_bytes) > 0 ? int64_t(kBlockBytes / row_bytes) : 1;
   if (rows_per_slot > cap_rows) rows_per_slot = cap_rows;
-  if (rows_per_slot < 1) {
+  rows_per_slot -= rows_per_slot % align_rows;
+  if (rows_per_slot < align_rows) {
     slots = 1;
-    rows_per_slot = 1;
+    rows_per_slot = workspace_bytes / row_bytes >= size_t(align_rows) ? align_rows : 1;
   }
   cudaStream_t user = reinterpret_cast<cudaStream_t>(stream);
   cudaStream_t st[kMaxSlots] = {nullptr, nullptr, nullptr, nullptr};
@@ -471,7 +529,8 @@ extern "C" hadacore_status_t hadacore_fwht_host(const void* in_host, void* out_h
 extern "C" const char* hadacore_status_string(hadacore_status_t s) {
   switch (s) {
     case HADACORE_OK: return "ok";
-    case HADACORE_ERR_INVALID_N: return "n must be a power of two in [128, 32768]";
+    case HADACORE_ERR_INVALID_N:
+      return "n must be a power of two in [2, 32768] ([128, 32768] for the strided and quantizing entry points)";
     case HADACORE_ERR_INVALID_M: return "m must be >= 0 and m*n*2 must fit in int64";
     case HADACORE_ERR_NULL: return "in/out must be non-NULL when m > 0";
     case HADACORE_ERR_MISALIGNED: return "in/out must be 16-byte aligned";

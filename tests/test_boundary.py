@@ -62,9 +62,16 @@ def call(lib, in_ptr, out_ptr, m, n, dtype=0, scale=1.0):
 def test_validation_codes(lib):
     a, b = 0x10000, 0x8000000
     assert call(lib, a, b, 4, 100) == INVALID_N
-    assert call(lib, a, b, 4, 64) == INVALID_N
+    assert call(lib, a, b, 4, 1) == INVALID_N       # n = 2..2^15 (NEXT-2 widened the paper's 2^7 floor)
+    assert call(lib, a, b, 4, 3) == INVALID_N
+    assert call(lib, a, b, 4, 96) == INVALID_N
     assert call(lib, a, b, 4, 65536) == INVALID_N
     assert call(lib, a, b, 4, 0) == INVALID_N
+    assert call(lib, a, b, 4, -128) == INVALID_N
+    for n in (2, 4, 8, 16, 32, 64):                 # accepted: m == 0 is a no-op without a GPU
+        assert call(lib, None, None, 0, n) == OK
+        assert call(lib, a + 8, b, 4, n) == MISALIGNED
+        assert call(lib, a, a + 16, 64, n) == OVERLAP
     assert call(lib, a, b, -1, 256) == INVALID_M
     assert call(lib, a, b, 1 << 62, 256) == INVALID_M
     assert call(lib, a, b, 4, 256, dtype=3) == DTYPE
@@ -99,6 +106,7 @@ def test_quant_entry_validation(lib):
     assert f(a, q, rs, 4, 256, 0, 2, 1.0, None) == DTYPE          # unknown qtype
     assert f(a, q, rs, 4, 256, 3, 0, 1.0, None) == DTYPE          # unknown dtype
     assert f(a, q, rs, 4, 100, 0, 0, 1.0, None) == INVALID_N
+    assert f(a, q, rs, 4, 64, 0, 0, 1.0, None) == INVALID_N      # fused quantization: the paper's 2^7..2^15
     assert f(a, q, rs, 4, 256, 0, 1, float("nan"), None) == SCALE
     assert f(a, None, rs, 4, 256, 0, 0, 1.0, None) == NULL
     assert f(a, q, None, 4, 256, 0, 0, 1.0, None) == NULL
@@ -119,6 +127,7 @@ def test_status_strings_and_version(lib):
     assert lib.hadacore_launches_per_call(0, 256) == 0
     assert lib.hadacore_launches_per_call(10, 256) == 1
     assert lib.hadacore_launches_per_call(10, 100) == 0
+    assert lib.hadacore_launches_per_call(10, 2) == 1
 
 
 def test_python_binding_rejects_without_fallback():
@@ -150,6 +159,7 @@ def test_strided_entry_validation(lib):
     assert f(a, b, 4, 3, 384, 64, 384, 128, 128, 0, 1.0, None) == INVALID_M         # inner rows overlap
     assert f(a, b, 4, 3, 256, 128, 384, 128, 128, 0, 1.0, None) == INVALID_M        # outer rows overlap
     assert f(a, b, 4, 3, 384, 128, 384, 128, 100, 0, 1.0, None) == INVALID_N
+    assert f(a, b, 4, 3, 384, 128, 384, 128, 64, 0, 1.0, None) == INVALID_N   # row grids: 2^7..2^15
     assert f(a, b, 4, 3, 384, 128, 384, 128, 128, 2, 1.0, None) == DTYPE            # fp32: contiguous API only
     assert f(a, a, 4, 3, 384, 128, 768, 128, 128, 0, 1.0, None) == OVERLAP          # in place needs equal strides
     assert f(a, a + 256, 4, 3, 384, 128, 384, 128, 128, 0, 1.0, None) == OVERLAP    # extents overlap
