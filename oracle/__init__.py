@@ -15,6 +15,10 @@ and follows /root/reference/PAPER.md:
 * ``dense_entry`` -- the definition y_l = scale * sum_j (-1)^popcount(j&l) x_j,
                      P:41 [Sec. 2.1] + Sylvester's construction P:45 [Sec. 2.2].
 * ``dense``       -- the definition for a whole (small) matrix.
+* ``quantize`` / ``fake_quant`` / ``lab_trial`` -- symmetric quantization and the
+                     rotated-vs-plain quantization-error trial of SPEC's quant_lab
+                     (the paper's motivation P:24 [Sec. 1], P:180
+                     [Sec. 4.2]), in fp64.
 
 Parity status: pinned (see tests/test_oracle.py and DESIGN.md "Oracle pins").
 """
@@ -60,6 +64,9 @@ def _load():
         lib.oracle_quantize_rows_f64.argtypes = [dp, ctypes.POINTER(ctypes.c_uint8), dp, ctypes.c_int64,
                                                  ctypes.c_int64, ctypes.c_int]
         lib.oracle_quantize_rows_f64.restype = ctypes.c_int
+        lib.oracle_quantize_f64.argtypes = [dp, ctypes.POINTER(ctypes.c_uint8), dp, ctypes.c_int64,
+                                            ctypes.c_int64, ctypes.c_int, ctypes.c_int]
+        lib.oracle_quantize_f64.restype = ctypes.c_int
         _lib = lib
     return _lib
 
@@ -119,7 +126,8 @@ def dense_entry(row, l: int, scale: float | None = None) -> float:
     return float(_load().oracle_dense_entry_f64(_ptr(a), n, int(l), float(scale)))
 
 
-QTYPES = {"e4m3": 0, "int8": 1}
+QTYPES = {"e4m3": 0, "int8": 1, "int4": 2}
+QMAX = {"e4m3": 448.0, "int8": 127.0, "int4": 7.0}
 
 
 def e4m3_value(code: int) -> float:
@@ -149,10 +157,46 @@ def quantize_rows(y, qtype: str):
     return codes, scales
 
 
+def quantize(y, qtype: str, per_tensor: bool = False):
+    """Symmetric quantization, SPEC quant_lab S:419-427: scale = max_abs / Q (Q = 448,
+    127, 7 for e4m3, int8, int4), codes = round(y / scale) (ties to even; e4m3 by
+    enumeration, saturating; integers clamped to +-Q); max_abs per row or over the
+    whole matrix (per_tensor, the scale then repeated per row); all-zero -> scale 1.
+    Returns (codes uint8 (m, n), scales float64 (m,))."""
+    a = _as_f64_2d(y)
+    m, n = a.shape
+    codes = np.empty((m, n), dtype=np.uint8)
+    scales = np.empty(m, dtype=np.float64)
+    rc = _load().oracle_quantize_f64(_ptr(a), codes.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8)),
+                                     _ptr(scales), m, n, QTYPES[qtype], int(bool(per_tensor)))
+    if rc != 0:
+        raise ValueError("oracle_quantize_f64 rejected its arguments")
+    return codes, scales
+
+
+def fake_quant(x, qtype: str, per_tensor: bool = False) -> np.ndarray:
+    """quantize -> dequantize (SPEC S:419 'dequantize multiplies back'), fp64."""
+    codes, scales = quantize(x, qtype, per_tensor)
+    return dequantize_rows(codes, scales, qtype)
+
+
+def lab_trial(x, qtype: str, per_tensor: bool = False) -> dict:
+    """One trial of SPEC's run_experiment, in fp64 on the original x:
+    (a) plain: fake-quantize x -> mse_plain; (b) rotated: y = H x (normalized,
+    P:41), fake-quantize y, inverse-rotate with H again (involution) -> mse_rotated;
+    max_abs of x and of y."""
+    a = _as_f64_2d(x)
+    y = fwht(a)
+    back = fwht(fake_quant(y, qtype, per_tensor))
+    plain = fake_quant(a, qtype, per_tensor)
+    return {"mse_plain": float(np.mean((plain - a) ** 2)), "mse_rotated": float(np.mean((back - a) ** 2)),
+            "max_abs_plain": float(np.abs(a).max()), "max_abs_rotated": float(np.abs(y).max())}
+
+
 def dequantize_rows(codes, scales, qtype: str) -> np.ndarray:
     """codes (m, n) uint8 and per-row scales -> fp64 values."""
     codes = np.asarray(codes, dtype=np.uint8)
-    if qtype == "int8":
+    if qtype in ("int8", "int4"):
         v = codes.view(np.int8).astype(np.float64)
     else:
         table = np.array([e4m3_value(c) for c in range(256)])

@@ -161,27 +161,42 @@ int oracle_e4m3_encode(double x) {
   return (neg ? 0x80 : 0) | best; /* |x| > 448 lands on 0x7E (448): saturation */
 }
 
-/* y: m x n fp64 (already transformed); codes: m x n bytes; scales: m doubles. */
-int oracle_quantize_rows_f64(const double* y, uint8_t* codes, double* scales, int64_t m, int64_t n, int qtype) {
-  if (m < 0 || n < 1 || (qtype != 0 && qtype != 1)) return -1;
-  const double qmax = qtype == 0 ? 448.0 : 127.0;
+/* qtype 2 = INT4 (SPEC quant_lab S:422 "Q = 7 (INT4)"): round-half-to-even of
+ * x/scale, clamped to [-7, 7], one code per byte (two's complement). */
+static double qmax_of(int qtype) { return qtype == 0 ? 448.0 : (qtype == 1 ? 127.0 : 7.0); }
+
+static uint8_t encode(double v, int qtype) {
+  if (qtype == 0) return (uint8_t)oracle_e4m3_encode(v);
+  const double lim = qmax_of(qtype);
+  double q = nearbyint(v); /* default rounding mode: to nearest, ties to even */
+  if (q > lim) q = lim;
+  if (q < -lim) q = -lim;
+  return (uint8_t)(int8_t)q;
+}
+
+/* y: m x n fp64 (already transformed); codes: m x n bytes; scales: m doubles.
+ * per_tensor = 0: one scale per row (SPEC "PerRow"); 1: one scale for the whole
+ * matrix, max_abs over all m*n entries (SPEC "PerTensor"), repeated in
+ * every scales[r]. */
+int oracle_quantize_f64(const double* y, uint8_t* codes, double* scales, int64_t m, int64_t n, int qtype,
+                        int per_tensor) {
+  if (m < 0 || n < 1 || qtype < 0 || qtype > 2) return -1;
+  const double qmax = qmax_of(qtype);
+  double tmax = 0.0;
+  if (per_tensor)
+    for (int64_t i = 0; i < m * n; ++i) tmax = fmax(tmax, fabs(y[i]));
   for (int64_t r = 0; r < m; ++r) {
     const double* row = y + r * n;
-    double amax = 0.0;
-    for (int64_t j = 0; j < n; ++j) amax = fmax(amax, fabs(row[j]));
+    double amax = tmax;
+    if (!per_tensor)
+      for (int64_t j = 0; j < n; ++j) amax = fmax(amax, fabs(row[j]));
     const double s = amax > 0.0 ? amax / qmax : 1.0;
     scales[r] = s;
-    for (int64_t j = 0; j < n; ++j) {
-      const double v = amax > 0.0 ? row[j] / s : 0.0;
-      if (qtype == 0) {
-        codes[r * n + j] = (uint8_t)oracle_e4m3_encode(v);
-      } else {
-        double q = nearbyint(v); /* default rounding mode: to nearest, ties to even */
-        if (q > 127.0) q = 127.0;
-        if (q < -127.0) q = -127.0;
-        codes[r * n + j] = (uint8_t)(int8_t)q;
-      }
-    }
+    for (int64_t j = 0; j < n; ++j) codes[r * n + j] = encode(amax > 0.0 ? row[j] / s : 0.0, qtype);
   }
   return 0;
+}
+
+int oracle_quantize_rows_f64(const double* y, uint8_t* codes, double* scales, int64_t m, int64_t n, int qtype) {
+  return oracle_quantize_f64(y, codes, scales, m, n, qtype, 0);
 }

@@ -62,7 +62,8 @@ def _uniform_pair(idx: torch.Tensor, seed: int):
 
 
 def normal_block(row0: int, m: int, n: int, seed: int, dist: str = "D0",
-                 device="cpu") -> torch.Tensor:
+                 device="cpu", outlier_rate: float = OUTLIER_RATE, outlier_value: float = OUTLIER_VALUE
+                 ) -> torch.Tensor:
     """fp32 (m, n) block of rows [row0, row0+m) of the global seeded matrix."""
     rows = torch.arange(row0, row0 + m, device=device, dtype=torch.int64)
     cols = torch.arange(n, device=device, dtype=torch.int64)
@@ -71,9 +72,9 @@ def normal_block(row0: int, m: int, n: int, seed: int, dist: str = "D0",
     v = torch.sqrt(-2.0 * torch.log(u1)) * torch.cos((2.0 * torch.pi) * u2)
     if dist == "D1":
         h = splitmix64(idx ^ _wrap64(_SALT + seed))
-        pick = (_lsr(h, 11).to(torch.float64) * (1.0 / 9007199254740992.0)) < OUTLIER_RATE
+        pick = (_lsr(h, 11).to(torch.float64) * (1.0 / 9007199254740992.0)) < outlier_rate
         sign = torch.where((h & 1) == 1, -1.0, 1.0).to(torch.float32)
-        v = torch.where(pick, sign * OUTLIER_VALUE, v)
+        v = torch.where(pick, sign * float(outlier_value), v)
     elif dist != "D0":
         raise ValueError(f"unknown distribution {dist!r}")
     return v
@@ -115,3 +116,14 @@ def special_rows(n: int, dtype: torch.dtype) -> tuple[torch.Tensor, list[str]]:
     tiny = torch.finfo(dtype).tiny  # smallest normal
     add("subnormal", g * (tiny / 8.0))
     return torch.stack(rows).to(dtype), names
+
+
+def outlier_matrix(m: int, n: int, seed: int, base_std: float = 1.0, outlier_rate: float = OUTLIER_RATE,
+                   outlier_scale: float = OUTLIER_VALUE, device="cpu") -> torch.Tensor:
+    """SPEC quant_lab OutlierSpec: fp32 (m, n) Gaussian(0, base_std) entries
+    with an outlier_rate fraction resampled at +-outlier_scale * base_std (the D1 draw
+    with parameters); deterministic per seed."""
+    if not (0.0 <= outlier_rate <= 1.0) or outlier_scale < 1.0 or base_std <= 0.0:
+        raise ValueError("BadSpec: need 0 <= outlier_rate <= 1, outlier_scale >= 1, base_std > 0")
+    v = normal_block(0, m, n, seed, "D1", device=device, outlier_rate=outlier_rate, outlier_value=outlier_scale)
+    return v * float(base_std)

@@ -25,6 +25,7 @@ import pytest
 import scipy.linalg
 
 import oracle
+import synthetic
 
 GOLDEN = os.path.join(os.path.dirname(__file__), "golden", "spec_examples.json")
 
@@ -233,3 +234,88 @@ def test_quantization_error_bounds_on_random_rows():
         else:  # relative 2^-4 in the normal range, half the subnormal spacing below it
             assert np.all(err <= np.abs(y) * 2.0 ** -4 + s[:, None] * 2.0 ** -10 + 1e-12)
         assert np.allclose(np.abs(deq).max(axis=1), np.abs(y).max(axis=1))   # the max is exact
+
+
+# ---------------------------------------------------------------- quant_lab oracle (NEXT-4)
+# Pins for oracle.quantize (INT4, per-tensor) and oracle.lab_trial: SPEC quant_lab
+# S:397-440 worked examples, closed forms and invariants.
+
+def test_quantize_int4_closed_forms_and_ties():
+    # scale 1 via a 7 anchor: ties to even, clamp never needed below max_abs
+    codes, s = oracle.quantize(np.array([[7.0, 2.5, 3.5, -2.5, 0.5, 1.5, -7.0]]), "int4")
+    assert s[0] == 1.0 and list(codes[0].view(np.int8)) == [7, 2, 4, -2, 0, 2, -7]
+    # S:427 single outlier 100 among unit-scale values, INT4: scale 100/7 ~ 14.3, the
+    # bulk collapses to 0 after the round trip, the outlier survives
+    row = np.concatenate([[100.0], np.linspace(-1.0, 1.0, 63)])[None, :]
+    codes, s = oracle.quantize(row, "int4")
+    assert s[0] == 100.0 / 7.0
+    deq = oracle.fake_quant(row, "int4")
+    assert np.all(deq[0, 1:] == 0.0) and abs(deq[0, 0] - 100.0) <= 1e-12
+
+
+def test_quantize_per_tensor():
+    # max_abs = 127 somewhere in the matrix, INT8 PerTensor -> scale 1.0 for every
+    # row and integers round-trip exactly (per row they would not: row 1's max is 5)
+    x = np.array([[127.0, -3.0, 0.0, 64.0], [5.0, -5.0, 1.0, 2.0]])
+    codes, s = oracle.quantize(x, "int8", per_tensor=True)
+    assert np.all(s == 1.0)
+    assert np.array_equal(oracle.fake_quant(x, "int8", per_tensor=True), x)
+    _, s_row = oracle.quantize(x, "int8")
+    assert s_row[1] == 5.0 / 127.0
+    # one row: per-tensor == per-row; brute-force tensor max on a random matrix
+    rng = np.random.default_rng(5)
+    r = rng.standard_normal((1, 256))
+    for q in ("e4m3", "int8", "int4"):
+        assert np.array_equal(oracle.fake_quant(r, q, True), oracle.fake_quant(r, q, False))
+    big = rng.standard_normal((7, 64)) * np.arange(1, 8)[:, None]
+    _, st = oracle.quantize(big, "int4", per_tensor=True)
+    assert np.all(st == max(abs(v) for v in big.ravel()) / 7.0)
+
+
+def test_fake_quant_error_bounds_all_targets():
+    rng = np.random.default_rng(9)
+    x = rng.standard_normal((16, 512)) * np.exp(rng.standard_normal((16, 1)))
+    for per_tensor in (False, True):
+        for q in ("int8", "int4"):
+            codes, s = oracle.quantize(x, q, per_tensor)
+            deq = oracle.dequantize_rows(codes, s, q)
+            assert np.all(np.abs(deq - x) <= s[:, None] / 2 * (1 + 1e-12))   # S:421 "scale/2 per entry"
+            assert np.all(np.abs(codes.view(np.int8)) <= oracle.QMAX[q])
+        deq = oracle.fake_quant(x, "e4m3", per_tensor)
+        _, s = oracle.quantize(x, "e4m3", per_tensor)
+        assert np.all(np.abs(deq - x) <= np.abs(x) * 2.0 ** -4 + s[:, None] * 2.0 ** -10 + 1e-12)
+
+
+def test_lab_trial_closed_forms():
+    # x = c e0 (one row): the rotated row is constant c/sqrt(d) -> max_abs exactly that,
+    # and every rotated entry is exactly representable after scaling: no rotated error
+    for d in (16, 256, 4096):
+        c = 3.0
+        x = np.zeros((1, d)); x[0, 0] = c
+        t = oracle.lab_trial(x, "int4")
+        assert abs(t["max_abs_rotated"] - c / np.sqrt(d)) <= 1e-15 * c
+        assert t["max_abs_plain"] == c and t["mse_plain"] == 0.0
+        assert t["mse_rotated"] <= 1e-28
+    # rotation alone (no quantization) is reproduced to 1e-10 by the inverse rotation
+    x = synthetic.outlier_matrix(8, 1024, 3).double().numpy()
+    assert np.max(np.abs(oracle.fwht(oracle.fwht(x)) - x)) <= 1e-10
+
+
+def test_lab_trial_parseval_and_direction():
+    # the inverse-rotated error equals the rotated-domain error (H orthogonal): an
+    # independent check of the inverse-rotation step
+    x = synthetic.outlier_matrix(16, 1024, 11).double().numpy()
+    for q in ("int4", "int8", "e4m3"):
+        t = oracle.lab_trial(x, q)
+        y = oracle.fwht(x)
+        rot_dom = float(np.mean((oracle.fake_quant(y, q) - y) ** 2))
+        assert abs(t["mse_rotated"] - rot_dom) <= 1e-9 * rot_dom
+    # S:438 (DERIVED; direction fixed by P:24 Sec. 1's outlier argument): outlier_rate 1e-3,
+    # outlier_scale 100, INT4 per row -> rotated error below plain in >= 95 % of 100 trials
+    wins = 0
+    for trial in range(100):
+        xt = synthetic.outlier_matrix(64, 1024, 1000 + trial).double().numpy()
+        t = oracle.lab_trial(xt, "int4")
+        wins += t["mse_rotated"] < t["mse_plain"]
+        assert t["max_abs_rotated"] <= t["max_abs_plain"]
+    assert wins >= 95
