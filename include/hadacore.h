@@ -64,7 +64,8 @@ typedef enum {
 /* Code formats of the fused quantized output (hadacore_fwht_quant). */
 typedef enum {
   HADACORE_Q_E4M3 = 0, /* FP8 E4M3 ("e4m3fn": no infinities, max finite 448), RNE, saturating */
-  HADACORE_Q_INT8 = 1  /* signed 8-bit integer, RNE, clamped to [-127, 127] */
+  HADACORE_Q_INT8 = 1, /* signed 8-bit integer, RNE, clamped to [-127, 127] */
+  HADACORE_Q_INT4 = 2  /* signed 4-bit integer, RNE, clamped to [-7, 7]: hadacore_fake_quant only */
 } hadacore_qtype_t;
 
 typedef enum {
@@ -144,6 +145,30 @@ hadacore_status_t hadacore_fwht_strided(const void* in, void* out, int64_t m_out
 hadacore_status_t hadacore_fwht_quant(const void* in, void* out_q, float* row_scale, int64_t m, int64_t n,
                                       hadacore_dtype_t dtype, hadacore_qtype_t qtype, float scale,
                                       hadacore_stream_t stream);
+
+/*
+ * Quantization-error lab (SPEC quant_lab S:397-440, the
+ * paper's motivation P:24 [Sec. 1]: rotations "reduce the magnitude of outliers"):
+ * the harness of the rotated-vs-plain experiment, whose rotations are
+ * hadacore_fwht calls on fp32 rows.
+ *
+ * hadacore_fake_quant: symmetric quantize -> dequantize of fp32 rows,
+ *     row_amax[i] = max_j |in[i, j]|          (per_tensor != 0: the max over the whole
+ *                                             matrix, written to every row_amax[i])
+ *     s_i = row_amax[i] / Q                   (Q = 448 E4M3, 127 INT8, 7 INT4; 1 if 0)
+ *     out[i, j] = code(in[i, j] / s_i) * s_i  (E4M3 RNE satfinite; integers RNE, clamp +-Q)
+ * in, out: m x n fp32 row-major device buffers (in == out allowed), row_amax: m
+ * fp32; all 16-byte aligned; n a power of two in [2, 32768]; finite inputs (SPEC
+ * S:420 "pre: finite input").  Asynchronous on `stream`; errors as hadacore_fwht,
+ * HADACORE_ERR_DTYPE for a qtype outside the enum.
+ *
+ * hadacore_row_sq_error: out[i] = sum_j (a[i, j] - b[i, j])^2 accumulated in fp64,
+ * for m x n fp32 row-major device buffers (4-byte aligned; out 8-byte aligned).
+ */
+hadacore_status_t hadacore_fake_quant(const float* in, float* out, float* row_amax, int64_t m, int64_t n,
+                                      hadacore_qtype_t qtype, int per_tensor, hadacore_stream_t stream);
+hadacore_status_t hadacore_row_sq_error(const float* a, const float* b, double* out, int64_t m, int64_t n,
+                                        hadacore_stream_t stream);
 
 /* Static, human-readable description of a status code (never NULL). */
 const char* hadacore_status_string(hadacore_status_t status);

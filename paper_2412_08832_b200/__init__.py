@@ -22,8 +22,8 @@ import os
 
 import torch
 
-__all__ = ["hadacore_fwht", "hadacore_fwht_host", "hadacore_fwht_quant", "hadacore_fwht_strided", "fwht", "HadacoreError", "library_path",
-           "version", "launches_per_call", "STATUS", "QTYPES"]
+__all__ = ["hadacore_fwht", "hadacore_fwht_host", "hadacore_fwht_quant", "hadacore_fwht_strided", "fwht", "HadacoreError",
+           "library_path", "version", "launches_per_call", "STATUS", "QTYPES", "fake_quant", "row_sq_error"]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_HERE, "libhadacore.so")
@@ -36,6 +36,7 @@ STATUS = {
 }
 _DTYPES = {torch.float16: 0, torch.bfloat16: 1, torch.float32: 2}  # float32 = debug path
 QTYPES = {"e4m3": (0, torch.float8_e4m3fn), "int8": (1, torch.int8)}
+LAB_QTYPES = {"e4m3": 0, "int8": 1, "int4": 2}  # hadacore_fake_quant (quant lab, NEXT-4)
 
 
 class HadacoreError(RuntimeError):
@@ -65,6 +66,10 @@ def _load():
     lib.hadacore_fwht_quant.restype = ctypes.c_int
     lib.hadacore_fwht_strided.argtypes = [vp, vp, i64, i64, i64, i64, i64, i64, i64, ctypes.c_int, f32, vp]
     lib.hadacore_fwht_strided.restype = ctypes.c_int
+    lib.hadacore_fake_quant.argtypes = [vp, vp, vp, i64, i64, ctypes.c_int, ctypes.c_int, vp]
+    lib.hadacore_fake_quant.restype = ctypes.c_int
+    lib.hadacore_row_sq_error.argtypes = [vp, vp, vp, i64, i64, vp]
+    lib.hadacore_row_sq_error.restype = ctypes.c_int
     lib.hadacore_status_string.argtypes = [ctypes.c_int]
     lib.hadacore_status_string.restype = ctypes.c_char_p
     lib.hadacore_version.argtypes = []
@@ -234,3 +239,38 @@ def hadacore_fwht_strided(x: torch.Tensor, out: torch.Tensor | None = None, scal
         _check(_load().hadacore_fwht_strided(x.data_ptr(), out.data_ptr(), mo, mi, so, si, oso, osi, n,
                                              _DTYPES[x.dtype], float(scale), st.cuda_stream))
     return out
+
+
+def fake_quant(x: torch.Tensor, qtype: str = "int4", per_tensor: bool = False, out: torch.Tensor | None = None,
+               stream: torch.cuda.Stream | None = None):
+    """Symmetric quantize -> dequantize of fp32 rows (C: hadacore_fake_quant; quant lab).
+
+    Returns ``(out, row_amax)``: ``out`` fp32 like ``x``; ``row_amax`` the per-row max
+    |x| (per_tensor: the matrix max in every entry); the scale used is row_amax / Q.
+    """
+    m, n = _shape(x)
+    if qtype not in LAB_QTYPES:
+        raise HadacoreError(6, f"qtype {qtype!r} (expected one of {sorted(LAB_QTYPES)})")
+    if x.dtype != torch.float32 or not x.is_cuda or not x.is_contiguous():
+        raise HadacoreError(6, "x must be a contiguous float32 CUDA tensor")
+    if out is None:
+        out = torch.empty_like(x)
+    amax = torch.empty(max(m, 1), dtype=torch.float32, device=x.device)
+    with torch.cuda.device(x.device):
+        st = stream if stream is not None else torch.cuda.current_stream(x.device)
+        _check(_load().hadacore_fake_quant(x.data_ptr(), out.data_ptr(), amax.data_ptr(), m, n, LAB_QTYPES[qtype],
+                                           int(bool(per_tensor)), st.cuda_stream))
+    return out, amax[:m]
+
+
+def row_sq_error(a: torch.Tensor, b: torch.Tensor, stream: torch.cuda.Stream | None = None) -> torch.Tensor:
+    """Per-row sum of squared differences of two fp32 CUDA matrices, fp64 (C: hadacore_row_sq_error)."""
+    m, n = _shape(a)
+    if a.shape != b.shape or a.dtype != torch.float32 or b.dtype != torch.float32 or not (a.is_cuda and b.is_cuda) \
+            or not (a.is_contiguous() and b.is_contiguous()):
+        raise HadacoreError(3, "a, b must be contiguous float32 CUDA tensors of one shape")
+    out = torch.empty(max(m, 1), dtype=torch.float64, device=a.device)
+    with torch.cuda.device(a.device):
+        st = stream if stream is not None else torch.cuda.current_stream(a.device)
+        _check(_load().hadacore_row_sq_error(a.data_ptr(), b.data_ptr(), out.data_ptr(), m, n, st.cuda_stream))
+    return out[:m]

@@ -55,7 +55,6 @@ __global__ void __launch_bounds__((NT + 1) * 32, 1)
   constexpr int K = log2_n<N>();
   constexpr int G = N >= 8 ? N / 8 : 1;            // granules per item
   constexpr int ITEM_BYTES = 16 * G;
-  constexpr int ITEMS = TILE_BYTES / ITEM_BYTES;   // items per full tile
   constexpr int KG = N >= 16 ? K - 3 : 0;          // granule bits of an item
   constexpr int KE = K < 3 ? K : 3;                // element bits inside a granule
   static_assert(TILE_BYTES % ITEM_BYTES == 0 && STAGES <= 16, "tile layout");

@@ -18,6 +18,7 @@
 #include "../../include/hadacore.h"
 #include "fwht_kernel.cuh"
 #include "fwht_small.cuh"
+#include "quant_lab.cuh"
 
 namespace hadacore {
 namespace {
@@ -524,6 +525,60 @@ extern "C" hadacore_status_t hadacore_fwht_host(const void* in_host, void* out_h
     }
   if (ev) cudaEventDestroy(ev);
   return rc;
+}
+
+// ---------------------------------------------------------------- quant lab (NEXT-4)
+namespace hadacore {
+namespace {
+int log2_pow2(int64_t n) {
+  int k = 0;
+  while ((int64_t(1) << k) < n) ++k;
+  return k;
+}
+int lab_grid(int64_t work_items, int per_block) {
+  const int64_t b = (work_items + per_block - 1) / per_block;
+  const int64_t cap = int64_t(sm_count(0)) * 16;
+  return int(b < 1 ? 1 : (b < cap ? b : cap));
+}
+}  // namespace
+}  // namespace hadacore
+
+extern "C" hadacore_status_t hadacore_fake_quant(const float* in, float* out, float* row_amax, int64_t m, int64_t n,
+                                                 hadacore_qtype_t qtype, int per_tensor, hadacore_stream_t stream) {
+  if (qtype != HADACORE_Q_E4M3 && qtype != HADACORE_Q_INT8 && qtype != HADACORE_Q_INT4) return HADACORE_ERR_DTYPE;
+  if (!valid_n(n)) return HADACORE_ERR_INVALID_N;
+  if (m < 0 || m > INT64_MAX / (4 * n)) return HADACORE_ERR_INVALID_M;
+  if (m == 0) return HADACORE_OK;
+  if (!in || !out || !row_amax) return HADACORE_ERR_NULL;
+  if ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out) | reinterpret_cast<uintptr_t>(row_amax)) & 15u)
+    return HADACORE_ERR_MISALIGNED;
+  const size_t bytes = size_t(m) * size_t(n) * 4;
+  if ((in != out && ranges_overlap(in, bytes, out, bytes)) || ranges_overlap(in, bytes, row_amax, size_t(m) * 4) ||
+      ranges_overlap(out, bytes, row_amax, size_t(m) * 4))
+    return HADACORE_ERR_OVERLAP;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  lab::row_amax_kernel<<<lab_grid(m, 8), 256, 0, st>>>(in, row_amax, m, n);
+  if (per_tensor) lab::tensor_amax_kernel<<<1, 1024, 0, st>>>(row_amax, m);
+  const int64_t total = m * n;
+  const int g = lab_grid(total, 256 * 8), k = log2_pow2(n);
+  if (qtype == HADACORE_Q_E4M3) lab::fake_quant_kernel<lab::LQ_E4M3><<<g, 256, 0, st>>>(in, out, row_amax, total, k);
+  else if (qtype == HADACORE_Q_INT8) lab::fake_quant_kernel<lab::LQ_INT8><<<g, 256, 0, st>>>(in, out, row_amax, total, k);
+  else lab::fake_quant_kernel<lab::LQ_INT4><<<g, 256, 0, st>>>(in, out, row_amax, total, k);
+  return cudaPeekAtLastError() == cudaSuccess ? HADACORE_OK : HADACORE_ERR_CUDA;
+}
+
+extern "C" hadacore_status_t hadacore_row_sq_error(const float* a, const float* b, double* out, int64_t m, int64_t n,
+                                                   hadacore_stream_t stream) {
+  if (n < 1) return HADACORE_ERR_INVALID_N;
+  if (m < 0 || m > INT64_MAX / (4 * n)) return HADACORE_ERR_INVALID_M;
+  if (m == 0) return HADACORE_OK;
+  if (!a || !b || !out) return HADACORE_ERR_NULL;
+  if ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b)) & 3u ||
+      reinterpret_cast<uintptr_t>(out) & 7u)
+    return HADACORE_ERR_MISALIGNED;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  lab::row_sq_error_kernel<<<lab_grid(m, 8), 256, 0, st>>>(a, b, out, m, n);
+  return cudaPeekAtLastError() == cudaSuccess ? HADACORE_OK : HADACORE_ERR_CUDA;
 }
 
 extern "C" const char* hadacore_status_string(hadacore_status_t s) {

@@ -30,7 +30,7 @@ def declared_functions():
 
 def test_header_declares_expected_entry_points():
     assert declared_functions() == sorted(["hadacore_fwht", "hadacore_fwht_host", "hadacore_fwht_quant",
-                                           "hadacore_fwht_strided",
+                                           "hadacore_fwht_strided", "hadacore_fake_quant", "hadacore_row_sq_error",
                                            "hadacore_status_string", "hadacore_version",
                                            "hadacore_launches_per_call"])
 
@@ -165,3 +165,25 @@ def test_strided_entry_validation(lib):
     assert f(a, a + 256, 4, 3, 384, 128, 384, 128, 128, 0, 1.0, None) == OVERLAP    # extents overlap
     assert f(a + 2, b, 4, 3, 384, 128, 384, 128, 128, 0, 1.0, None) == MISALIGNED
     assert f(None, None, 0, 3, 384, 128, 384, 128, 128, 0, 1.0, None) == OK
+
+
+def test_lab_entry_validation(lib):
+    a, b, s = 0x10000, 0x8000000, 0x20000000
+    f = lib.hadacore_fake_quant
+    f.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int,
+                  ctypes.c_int, ctypes.c_void_p]
+    assert f(a, b, s, 4, 256, 3, 0, None) == DTYPE            # qtype outside {E4M3, INT8, INT4}
+    assert f(a, b, s, 4, 100, 2, 0, None) == INVALID_N
+    assert f(a, b, s, -1, 256, 2, 0, None) == INVALID_M
+    assert f(None, b, s, 4, 256, 2, 0, None) == NULL
+    assert f(a, b, None, 4, 256, 2, 0, None) == NULL
+    assert f(a + 4, b, s, 4, 256, 2, 0, None) == MISALIGNED
+    assert f(a, a + 16, s, 4, 256, 2, 0, None) == OVERLAP
+    assert f(a, b, a + 16, 4, 256, 2, 1, None) == OVERLAP
+    assert f(None, None, None, 0, 256, 2, 0, None) == OK
+    g = lib.hadacore_row_sq_error
+    g.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p]
+    assert g(a, b, s, 4, 0, None) == INVALID_N
+    assert g(a, b, s + 4, 4, 16, None) == MISALIGNED
+    assert g(None, b, s, 4, 16, None) == NULL
+    assert g(None, None, None, 0, 16, None) == OK
