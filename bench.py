@@ -49,9 +49,10 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
-    ap.add_argument("--workload", choices=["fwht", "quant-e4m3", "quant-int8", "qk-rotate", "small"], default="fwht",
+    ap.add_argument("--workload", choices=["fwht", "quant-e4m3", "quant-int8", "qk-rotate", "small", "f32"], default="fwht",
                     help="fwht = the metric's C3 sweep (default); quant-* = the fused FWHT + per-row "
-                         "quantization row (NEXT-1) on the same inputs; small = n=2^1..2^6 (NEXT-2)")
+                         "quantization row (NEXT-1) on the same inputs; small = n=2^1..2^6 (NEXT-2); "
+                         "f32 = the fp32 path over n=2^1..2^15 (NEXT-2)")
     return ap.parse_args()
 
 
@@ -231,6 +232,10 @@ def config_block(args, world):
     wl = ("C3 size sweep: n=2^7..2^15 x {fp16, bf16}, 2^28 elements per (n, dtype) per GPU, "
           "out-of-place, normalized (scale=1/sqrt(n))")
     ns = SMALL_NS if getattr(args, "workload", "fwht") == "small" else NS
+    if getattr(args, "workload", "fwht") == "f32":
+        ns = SMALL_NS + NS
+        wl = ("NEXT-2 fp32 path: n=2^1..2^15 fp32, 2^28 elements (1 GiB in, 1 GiB out) per n per GPU, "
+              "out-of-place, normalized (scale=1/sqrt(n))")
     if getattr(args, "workload", "fwht") == "small":
         wl = ("NEXT-2 small sizes: n=2^1..2^6 x {fp16, bf16}, 2^28 elements per (n, dtype) per GPU, "
               "out-of-place, normalized (scale=1/sqrt(n))")
@@ -238,8 +243,9 @@ def config_block(args, world):
         wl = ("QK rotation: n=2^7..2^15 x {fp16, bf16}; a 2^28-element QKV buffer viewed as [T, 3, H, n], "
               "H = max(1, 4096/n); the Q and K heads (2/3 of it) transformed in place, normalized")
     return {"workload": wl,
-            "elements_per_launch": args.elems, "ns": ns, "dtypes": ["fp16", "bf16"],
-            "launches_per_step": 2 * len(ns), "path": getattr(args, "workload", "fwht"),
+            "elements_per_launch": args.elems, "ns": ns,
+            "dtypes": ["fp32"] if getattr(args, "workload", "fwht") == "f32" else ["fp16", "bf16"],
+            "launches_per_step": (1 if getattr(args, "workload", "fwht") == "f32" else 2) * len(ns), "path": getattr(args, "workload", "fwht"),
             "l2": "no flush: every launch reads a 512 MiB input and writes a 512 MiB output (> 126 MB L2)",
             "parallelism": f"row-sharded x{world}, no collective on the hot path" if world > 1 else "single GPU"}
 
@@ -272,7 +278,14 @@ def main():
     obuf = torch.empty(args.elems, dtype=torch.float16, device=dev)
     stream = torch.cuda.current_stream(dev)
     ns = SMALL_NS if args.workload == "small" else NS
-    pairs = [(dt, n) for dt in (torch.float16, torch.bfloat16) for n in ns]
+    f32 = args.workload == "f32"
+    if f32:
+        ns = SMALL_NS + NS
+        xin = {torch.float32: torch.empty(args.elems, dtype=torch.float32, device=dev)}
+        synthetic.generate(args.elems // 256, 256, torch.float32, synthetic.seed_for(2, torch.float32),
+                           row0=rank * (args.elems // 256), out=xin[torch.float32].view(-1, 256))
+        obuf = torch.empty(args.elems, dtype=torch.float32, device=dev)
+    pairs = [(dt, n) for dt in ((torch.float32,) if f32 else (torch.float16, torch.bfloat16)) for n in ns]
     quant = args.workload.startswith("quant")
     qtype = args.workload.split("-")[1] if quant else None
     if quant:
@@ -301,7 +314,7 @@ def main():
             hc.hadacore_fwht_quant(x, qtype=qtype, out=qbuf.view(-1, n), row_scale=sbuf[: x.shape[0]],
                                    stream=stream)
             return
-        o = obuf.view(torch.int16).view(dt).view(-1, n)
+        o = obuf.view(-1, n) if f32 else obuf.view(torch.int16).view(dt).view(-1, n)
         hc.hadacore_fwht(x, out=o, stream=stream)
 
     # warm-up
@@ -358,7 +371,8 @@ def main():
     t_max = max_over_ranks(total_ms, dist, torch)
     # algorithmic bytes: 2 B read + 2 B written per element (fwht); 2 + 1 B plus one fp32
     # scale per row for the fused quantization (per-n average over the sweep)
-    bytes_per_launch = 4.0 * args.elems if not quant else \
+    esize = 4 if f32 else 2
+    bytes_per_launch = 2.0 * esize * args.elems if not quant else \
         sum(3.0 * args.elems + 4.0 * (args.elems // n) for n in NS) / len(NS)
     if rotate:
         bytes_per_launch = sum(4.0 * e for e in elems_of.values()) / len(pairs)
@@ -370,8 +384,8 @@ def main():
     for k, (dt, n) in enumerate(pairs):
         ts = sorted(per[k::len(pairs)])
         med = ts[len(ts) // 2]
-        b_n = 4.0 * elems_of[(dt, n)] if not quant else 3.0 * args.elems + 4.0 * (args.elems // n)
-        per_n.setdefault("fp16" if dt == torch.float16 else "bf16", {})[str(n)] = round(b_n / (med * 1e-3) / 1e9, 1)
+        b_n = 2.0 * esize * elems_of[(dt, n)] if not quant else 3.0 * args.elems + 4.0 * (args.elems // n)
+        per_n.setdefault({torch.float16: "fp16", torch.bfloat16: "bf16", torch.float32: "fp32"}[dt], {})[str(n)] = round(b_n / (med * 1e-3) / 1e9, 1)
     # roofline over the timed region: every launch of the step is the same transform
     # (one per (dtype, n)), so the kernel's average launch duration is the region time
     # over the launches in it (per-(dtype, n) values: per_n_GBps)
@@ -437,6 +451,8 @@ def main():
     if rank == 0:
         metric = METRIC if not quant else (f"Fused FWHT + per-row {qtype.upper()} quantization HBM GB/s vs "
                                            "n=2^7..2^15 (bf16/fp16 in, 8-bit codes + fp32 row scales out)")
+        if f32:
+            metric = "FWHT HBM GB/s vs n=2^1..2^15, fp32 path (NEXT-2; north_star's fp32 path, tolerance 1e-5)"
         if args.workload == "small":
             metric = "FWHT HBM GB/s vs n=2^1..2^6 (bf16/fp16), rows shorter than the paper's 2^7 (NEXT-2)"
         if rotate:
@@ -445,11 +461,12 @@ def main():
         line = {
             "metric": metric, "value": round(value, 1), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(t_max / args.steps, 4), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "fp16+bf16 (fp32 last-stage accumulate)",
+            "scaling": "weak", "vs_baseline": None,
+            "dtype": "fp32" if f32 else "fp16+bf16 (fp32 last-stage accumulate)",
             "data": "synthetic (counter-based N(0,1), synthetic/)", "config": config_block(args, world),
             "pct_of_8TBps": round(100.0 * value / world / NOMINAL_HBM_GBS, 2),
             "per_n_GBps": per_n, "roofline": roofline, "cpu_baseline": cpu_baseline, "e2e": e2e,
-            "gpu_launches": int(args.steps * sum(hc.launches_per_call(elems_of[(dt, n)] // n, n) for dt, n in pairs)),
+            "gpu_launches": int(args.steps * sum(hc.launches_per_call(elems_of[(dt, n)] // n, n, dt) for dt, n in pairs)),
             "clocks": clocks, "remeasured_for_clocks": remeasured,
         }
         print(json.dumps(line), flush=True)

@@ -58,7 +58,7 @@ typedef struct CUstream_st* hadacore_stream_t;
 typedef enum {
   HADACORE_F16 = 0,  /* IEEE 754 binary16 */
   HADACORE_BF16 = 1, /* bfloat16 */
-  HADACORE_F32 = 2   /* IEEE 754 binary32: debug/reference path (fp32 butterflies), not tuned */
+  HADACORE_F32 = 2   /* IEEE 754 binary32: fp32 register butterflies (north_star's fp32 path, 1e-5) */
 } hadacore_dtype_t;
 
 /* Code formats of the fused quantized output (hadacore_fwht_quant). */
@@ -181,6 +181,10 @@ int hadacore_version(void);
  * (0 when m == 0, else 1), for launch accounting in benchmarks.
  */
 int hadacore_launches_per_call(int64_t m, int64_t n);
+
+/* The same for a given dtype: the fp32 path takes two launches at n = 2^15 (its
+ * rows of 128 KiB are transformed as two halves, then combined). */
+int hadacore_launches_per_call_dtype(int64_t m, int64_t n, hadacore_dtype_t dtype);
 
 #ifdef __cplusplus
 }

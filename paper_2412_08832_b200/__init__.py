@@ -34,7 +34,7 @@ STATUS = {
     4: "HADACORE_ERR_MISALIGNED", 5: "HADACORE_ERR_OVERLAP", 6: "HADACORE_ERR_DTYPE",
     7: "HADACORE_ERR_SCALE", 8: "HADACORE_ERR_CUDA", 9: "HADACORE_ERR_WORKSPACE",
 }
-_DTYPES = {torch.float16: 0, torch.bfloat16: 1, torch.float32: 2}  # float32 = debug path
+_DTYPES = {torch.float16: 0, torch.bfloat16: 1, torch.float32: 2}
 QTYPES = {"e4m3": (0, torch.float8_e4m3fn), "int8": (1, torch.int8)}
 LAB_QTYPES = {"e4m3": 0, "int8": 1, "int4": 2}  # hadacore_fake_quant (quant lab, NEXT-4)
 
@@ -76,6 +76,8 @@ def _load():
     lib.hadacore_version.restype = ctypes.c_int
     lib.hadacore_launches_per_call.argtypes = [i64, i64]
     lib.hadacore_launches_per_call.restype = ctypes.c_int
+    lib.hadacore_launches_per_call_dtype.argtypes = [i64, i64, ctypes.c_int]
+    lib.hadacore_launches_per_call_dtype.restype = ctypes.c_int
     _lib = lib
     return lib
 
@@ -89,8 +91,10 @@ def version() -> int:
     return _load().hadacore_version()
 
 
-def launches_per_call(m: int, n: int) -> int:
-    return _load().hadacore_launches_per_call(int(m), int(n))
+def launches_per_call(m: int, n: int, dtype: torch.dtype | None = None) -> int:
+    if dtype is None:
+        return _load().hadacore_launches_per_call(int(m), int(n))
+    return _load().hadacore_launches_per_call_dtype(int(m), int(n), _DTYPES[dtype])
 
 
 def _shape(x: torch.Tensor):

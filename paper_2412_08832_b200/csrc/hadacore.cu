@@ -18,6 +18,7 @@
 #include "../../include/hadacore.h"
 #include "fwht_kernel.cuh"
 #include "fwht_small.cuh"
+#include "fwht_f32.cuh"
 #include "quant_lab.cuh"
 
 namespace hadacore {
@@ -327,7 +328,68 @@ hadacore_status_t launch_f32(const void* in, void* out, int64_t m, float scale, 
   return cudaPeekAtLastError() == cudaSuccess ? HADACORE_OK : HADACORE_ERR_CUDA;
 }
 
+// Full-speed fp32 path (NEXT-2, fwht_f32_fast_kernel): 8 consumer warps, 32 KiB
+// tiles in a 4-stage ring (64 KiB x 3 for n = 2^14); n = 2^15 = two 2^14 halves +
+// f32_half_butterfly_kernel.
+template <int N> struct TunedF { static constexpr int nt = 8, tkb = N >= 16384 ? 64 : 32, st = N >= 16384 ? 3 : 4; };
+
+template <int N>
+hadacore_status_t launch_f32_fast(const void* in, void* out, int64_t m, float scale, cudaStream_t stream) {
+  using T = TunedF<N>;
+  constexpr int tile = T::tkb * 1024;
+  constexpr int smem = T::st * tile + int(sizeof(SchedCtl)) + 2 * T::st * 8;
+  static std::atomic<uint64_t> attr_done{0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return HADACORE_ERR_CUDA;
+  auto kern = fwht_f32_fast_kernel<N, tile, T::st, T::nt>;
+  if (!ensure_smem_attr(kern, smem, attr_done, dev)) return HADACORE_ERR_CUDA;
+  const int64_t total = m * N * 4;
+  const int64_t tiles = (total + tile - 1) / tile;
+  const int64_t max_ctas = kClc ? int64_t(INT32_MAX) : int64_t(sm_count(dev));
+  const int grid = int(tiles < max_ctas ? tiles : max_ctas);
+  if (launch_pdl(kern, grid, (T::nt + 1) * 32, smem, stream, static_cast<const float*>(in), static_cast<float*>(out),
+                 total, tiles, scale) != cudaSuccess)
+    return HADACORE_ERR_CUDA;
+  return cudaPeekAtLastError() == cudaSuccess ? HADACORE_OK : HADACORE_ERR_CUDA;
+}
+
+hadacore_status_t launch_f32_32k(const void* in, void* out, int64_t m, float scale, cudaStream_t stream) {
+  // pass 1: I_2 (x) H_2^14 on the two halves of every row (unnormalized), into `out`
+  hadacore_status_t rc = launch_f32_fast<16384>(in, out, 2 * m, 1.f, stream);
+  if (rc != HADACORE_OK) return rc;
+  // pass 2: H_2 (x) I_2^14 across the halves, times scale, in place in `out`
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return HADACORE_ERR_CUDA;
+  const int64_t work = m * 4096, cap = int64_t(sm_count(dev)) * 8;
+  const int64_t blocks = (work + 255) / 256;
+  if (launch_pdl(f32_half_butterfly_kernel, int(blocks < cap ? blocks : cap), 256, 0, stream,
+                 static_cast<const float*>(out), static_cast<float*>(out), m, scale) != cudaSuccess)
+    return HADACORE_ERR_CUDA;
+  return cudaPeekAtLastError() == cudaSuccess ? HADACORE_OK : HADACORE_ERR_CUDA;
+}
+
 hadacore_status_t dispatch_f32(const void* in, void* out, int64_t m, int64_t n, float scale, cudaStream_t st) {
+#ifndef HC_F32_SIMPLE
+  switch (n) {
+    case 2: return launch_f32_fast<2>(in, out, m, scale, st);
+    case 4: return launch_f32_fast<4>(in, out, m, scale, st);
+    case 8: return launch_f32_fast<8>(in, out, m, scale, st);
+    case 16: return launch_f32_fast<16>(in, out, m, scale, st);
+    case 32: return launch_f32_fast<32>(in, out, m, scale, st);
+    case 64: return launch_f32_fast<64>(in, out, m, scale, st);
+    case 128: return launch_f32_fast<128>(in, out, m, scale, st);
+    case 256: return launch_f32_fast<256>(in, out, m, scale, st);
+    case 512: return launch_f32_fast<512>(in, out, m, scale, st);
+    case 1024: return launch_f32_fast<1024>(in, out, m, scale, st);
+    case 2048: return launch_f32_fast<2048>(in, out, m, scale, st);
+    case 4096: return launch_f32_fast<4096>(in, out, m, scale, st);
+    case 8192: return launch_f32_fast<8192>(in, out, m, scale, st);
+    case 16384: return launch_f32_fast<16384>(in, out, m, scale, st);
+    case 32768: return launch_f32_32k(in, out, m, scale, st);
+    default: return HADACORE_ERR_INVALID_N;
+  }
+#endif
+  // HC_F32_SIMPLE builds: the plain shared-memory debug kernel (one barrier per stage)
   switch (n) {
     case 2: return launch_f32<2>(in, out, m, scale, st);
     case 4: return launch_f32<4>(in, out, m, scale, st);
@@ -611,4 +673,11 @@ extern "C" int hadacore_span_read(void* host, size_t bytes) {
 
 extern "C" int hadacore_launches_per_call(int64_t m, int64_t n) {
   return (m > 0 && valid_n(n)) ? 1 : 0;
+}
+
+extern "C" int hadacore_launches_per_call_dtype(int64_t m, int64_t n, hadacore_dtype_t dtype) {
+#ifndef HC_F32_SIMPLE
+  if (dtype == HADACORE_F32 && m > 0 && n == 32768) return 2;  // two passes (fwht_f32.cuh)
+#endif
+  return hadacore_launches_per_call(m, n);
 }

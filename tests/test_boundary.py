@@ -32,7 +32,7 @@ def test_header_declares_expected_entry_points():
     assert declared_functions() == sorted(["hadacore_fwht", "hadacore_fwht_host", "hadacore_fwht_quant",
                                            "hadacore_fwht_strided", "hadacore_fake_quant", "hadacore_row_sq_error",
                                            "hadacore_status_string", "hadacore_version",
-                                           "hadacore_launches_per_call"])
+                                           "hadacore_launches_per_call", "hadacore_launches_per_call_dtype"])
 
 
 def test_library_exports_every_declared_symbol(lib):
@@ -128,6 +128,9 @@ def test_status_strings_and_version(lib):
     assert lib.hadacore_launches_per_call(10, 256) == 1
     assert lib.hadacore_launches_per_call(10, 100) == 0
     assert lib.hadacore_launches_per_call(10, 2) == 1
+    assert lib.hadacore_launches_per_call_dtype(10, 32768, 2) == 2     # fp32 n = 2^15: two passes
+    assert lib.hadacore_launches_per_call_dtype(10, 32768, 1) == 1
+    assert lib.hadacore_launches_per_call_dtype(0, 32768, 2) == 0
 
 
 def test_python_binding_rejects_without_fallback():
