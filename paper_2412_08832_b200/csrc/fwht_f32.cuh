@@ -16,9 +16,10 @@
 //             consecutive lanes take consecutive columns, so every LDS.32/STS.32 of
 //             a warp touches 32 consecutive words (conflict-free).
 // A named barrier over the consumer warps separates phases; the last phase applies
-// `scale`.  Rows of n = 2^15 (128 KiB of fp32) do not fit a double-buffered ring:
-// they are transformed as two rows of 2^14 by this kernel and finished by
-// f32_half_butterfly_kernel (H_2 (x) I across the halves).
+// `scale`.  Rows of n = 2^15 (128 KiB of fp32) do not fit a double-buffered ring in
+// one CTA: fwht_f32_pair_kernel splits each over a 2-CTA cluster (below); the
+// two-pass variant (2^14 halves + f32_half_butterfly_kernel) is the HC_F32_TWO_PASS
+// build, kept for A/B.
 #pragma once
 #include "fwht_small.cuh"
 
@@ -247,6 +248,209 @@ __global__ void __launch_bounds__((NT + 1) * 32, 1)
     __syncwarp();
     if (lane == 0) mbar_arrive(&done[s]);
   }
+}
+
+// ---------------------------------------------------------------- n = 2^15, 2-CTA clusters
+// A 128 KiB fp32 row does not fit a double-buffered ring in one CTA, so a CLUSTER of two
+// CTAs owns a row: CTA rank h holds half h (64 KiB) in its own ring and applies
+// H_2^14 to it (phases 0-2 of fwht_f32_fast_kernel); the last factor, H_2 over the top
+// index bit, needs both halves: every consumer thread reads the partner's elements
+// at half of the positions through distributed shared memory (mapa +
+// ld.shared::cluster; 32 KiB per CTA and tile) and computes both scale * (a + b) and
+// scale * (a - b) there; each CTA stores its two 32 KiB output pieces.  Two mbarriers
+// per stage order the exchange: ready[s] (the partner's half is final; one remote
+// release.cluster arrival per partner consumer thread) and consumed[s] (the partner
+// has read this CTA's half, so it may be overwritten).  Rows are scheduled
+// statically (row = cluster id + k * clusters), identically in both CTAs.  The
+// consumer warps form G groups that take alternate tiles, so one group's exchange
+// (two cross-SM handshakes and the DSMEM reads) overlaps the other's butterflies.
+__device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {  // non-.aligned: callable from diverged warps
+  asm volatile("barrier.cluster.arrive.release;\n\tbarrier.cluster.wait.acquire;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAITCL_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAITCL_%=;\n}" ::"r"(smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ float4 ld_cluster_f4(uint32_t cluster_addr) {
+  float4 v;
+  asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(cluster_addr)
+               : "memory");
+  return v;
+}
+
+template <int STAGES, int NT, int G>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((NT + 1) * 32, 1)
+    fwht_f32_pair_kernel(const float* __restrict__ in, float* __restrict__ out, int64_t m, float scale) {
+  constexpr int NH = 16384;                 // elements per half row (per CTA)
+  constexpr int TILE_BYTES = NH * 4;        // 64 KiB
+  constexpr int K = 14;
+  constexpr int NTG = NT / G;               // consumer warps per group; group g takes tiles it = g mod G
+  constexpr int PER_THREAD = NH / 8 / (NTG * 32);  // float4 positions of the final factor per consumer thread
+  // G <= STAGES: a group never waits on a stage barrier two phases ahead of its
+  // current phase (parity waits cannot tell those apart)
+  static_assert(NT % G == 0 && G <= STAGES, "groups");
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * TILE_BYTES);
+  uint64_t* done = full + STAGES;
+  uint64_t* ready = done + STAGES;
+  uint64_t* consumed = ready + STAGES;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank(), peer = rank ^ 1u;
+  const int64_t cid = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
+
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&done[s], NTG);
+      mbar_init(&ready[s], NTG * 32);
+      mbar_init(&consumed[s], NTG * 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    fence_proxy_async_smem();
+  }
+  cluster_sync_all();  // both CTAs' barriers exist before any remote arrival
+  pdl_launch_dependents();
+
+  if (warp == NT) {
+    if (lane == 0) {
+      pdl_wait();
+      const uint64_t pol = policy_evict_first();
+      auto src = [&](int64_t r) { return reinterpret_cast<const uint8_t*>(in + r * 2 * NH + rank * NH); };
+      int64_t r_load = cid;
+      for (int k = 0; k < STAGES && r_load < m; ++k, r_load += nclusters) {
+        mbar_arrive_expect_tx(&full[k], TILE_BYTES);
+        bulk_g2s(smem + k * TILE_BYTES, src(r_load), TILE_BYTES, &full[k], pol);
+      }
+      int it = 0;
+      for (int64_t r = cid; r < m; r += nclusters, ++it) {
+        const int s = it % STAGES;
+        mbar_wait(&done[s], (it / STAGES) & 1);
+        // smem [0, NH/2) = y_lo at this CTA's positions, [NH/2, NH) = y_hi at them
+        bulk_s2g(out + r * 2 * NH + rank * (NH / 2), smem + s * TILE_BYTES, TILE_BYTES / 2);
+        bulk_s2g(out + r * 2 * NH + NH + rank * (NH / 2), smem + s * TILE_BYTES + TILE_BYTES / 2, TILE_BYTES / 2);
+        bulk_commit();
+        if (r_load < m) {
+          bulk_wait_read<0>();
+          mbar_arrive_expect_tx(&full[s], TILE_BYTES);
+          bulk_g2s(smem + s * TILE_BYTES, src(r_load), TILE_BYTES, &full[s], pol);
+          r_load += nclusters;
+        }
+      }
+      bulk_wait_all();
+    }
+  } else {
+    const int grp = warp / NTG, tid = threadIdx.x - grp * NTG * 32;
+    const uint32_t c = uint32_t(lane) & 7u;
+    float al[3];
+#pragma unroll
+    for (int b = 0; b < 3; ++b) al[b] = ((c >> b) & 1u) ? -1.f : 1.f;
+    for (int it = grp;; it += G) {
+      const int64_t r = cid + int64_t(it) * nclusters;
+      if (r >= m) break;
+      const int s = it % STAGES;
+      const uint32_t ph = (it / STAGES) & 1;
+      mbar_wait(&full[s], ph);
+      float* const tb = reinterpret_cast<float*>(smem + s * TILE_BYTES);
+      // phase 0: bits 0..4, 32 contiguous floats per lane (sign-folded granule butterflies)
+      for (int item = tid; item < NH / 32; item += NTG * 32) {
+        float v[32];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float4 w = *reinterpret_cast<const float4*>(tb + 4 * (item * 8 + int(uint32_t(j) ^ c)));
+          v[4 * j] = w.x;
+          v[4 * j + 1] = w.y;
+          v[4 * j + 2] = w.z;
+          v[4 * j + 3] = w.w;
+        }
+#pragma unroll
+        for (int b = 0; b < 2; ++b)
+#pragma unroll
+          for (int e = 0; e < 32; ++e)
+            if (!(e & (1 << b))) {
+              const float p0 = v[e], p1 = v[e | (1 << b)];
+              v[e] = p0 + p1;
+              v[e | (1 << b)] = p0 - p1;
+            }
+#pragma unroll
+        for (int b = 0; b < 3; ++b)
+#pragma unroll
+          for (int e = 0; e < 32; ++e)
+            if (!(e & (4 << b))) {
+              const float p0 = v[e], p1 = v[e | (4 << b)];
+              v[e] = fmaf(p0, al[b], p1);
+              v[e | (4 << b)] = fmaf(p1, -al[b], p0);
+            }
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          *reinterpret_cast<float4*>(tb + 4 * (item * 8 + int(uint32_t(j) ^ c))) =
+              make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+      }
+      named_bar_sync(1 + grp, NTG * 32);
+      f32_phase<NH, 1, NTG>(tb, 1, tid, 1.f);
+      named_bar_sync(1 + grp, NTG * 32);
+      f32_phase<NH, 2, NTG>(tb, 1, tid, 1.f);  // the last in-CTA phase (scale applied below)
+      static_assert(K == 14, "half rows of 2^14");
+      // this thread's half is final: tell the partner (release at cluster scope)
+      const uint32_t tb_addr = smem_addr(tb);
+      mbar_arrive_remote(mapa_shared(smem_addr(&ready[s]), peer));
+      mbar_wait_cluster(&ready[s], ph);  // the partner's half is final
+      named_bar_sync(1 + grp, NTG * 32);  // ... and so is every thread's part of ours
+      // positions [rank * NH/2, (rank+1) * NH/2) of both halves are this CTA's: it reads
+      // the partner's half only there (32 KiB over DSMEM), and produces both outputs
+      // y_lo = a + b and y_hi = a - b for them
+      float4 own[PER_THREAD], pb[PER_THREAD];
+      const uint32_t peer_tb = mapa_shared(tb_addr, peer);
+      const int q0 = int(rank) * (NH / 8);  // first float4 of this CTA's positions
+#pragma unroll
+      for (int k2 = 0; k2 < PER_THREAD; ++k2)
+#ifdef HC_PAIR_NODSMEM  // diagnostic (wrong results): local reads instead of the partner's
+        pb[k2] = *reinterpret_cast<const float4*>(tb + 4 * (q0 + tid + k2 * NTG * 32) + 1);
+#else
+        pb[k2] = ld_cluster_f4(peer_tb + 16u * uint32_t(q0 + tid + k2 * NTG * 32));
+#endif
+#pragma unroll
+      for (int k2 = 0; k2 < PER_THREAD; ++k2) own[k2] = *reinterpret_cast<const float4*>(tb + 4 * (q0 + tid + k2 * NTG * 32));
+      mbar_arrive_remote(mapa_shared(smem_addr(&consumed[s]), peer));  // done reading the partner
+      mbar_wait_cluster(&consumed[s], ph);  // the partner is done reading ours
+#pragma unroll
+      for (int k2 = 0; k2 < PER_THREAD; ++k2) {
+        // rank 0 holds the low half (own = a, partner = b); rank 1 the high half (own = b)
+        const float4 a = rank == 0 ? own[k2] : pb[k2];
+        const float4 b = rank == 0 ? pb[k2] : own[k2];
+        const int e4 = tid + k2 * NTG * 32;
+        *reinterpret_cast<float4*>(tb + 4 * e4) =
+            make_float4((a.x + b.x) * scale, (a.y + b.y) * scale, (a.z + b.z) * scale, (a.w + b.w) * scale);
+        *reinterpret_cast<float4*>(tb + 4 * (NH / 8 + e4)) =
+            make_float4((a.x - b.x) * scale, (a.y - b.y) * scale, (a.z - b.z) * scale, (a.w - b.w) * scale);
+      }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&done[s]);
+    }
+  }
+  __syncwarp();
+  cluster_sync_all();  // no CTA leaves while its partner may still touch its shared memory
 }
 
 // n = 2^15 in fp32, second pass: rows are [a | b] with a, b = H_2^14-transformed halves;

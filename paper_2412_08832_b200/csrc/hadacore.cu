@@ -354,6 +354,42 @@ hadacore_status_t launch_f32_fast(const void* in, void* out, int64_t m, float sc
 }
 
 hadacore_status_t launch_f32_32k(const void* in, void* out, int64_t m, float scale, cudaStream_t stream) {
+#ifndef HC_F32_TWO_PASS
+  // one launch of 2-CTA clusters, a row per cluster (fwht_f32_pair_kernel)
+#ifndef HC_PAIR_NT
+#define HC_PAIR_NT 16
+#endif
+#ifndef HC_PAIR_G
+#define HC_PAIR_G 2
+#endif
+  constexpr int st = 3, nt = HC_PAIR_NT, groups = HC_PAIR_G;
+  constexpr int smem = st * 65536 + 4 * st * 8;
+  static std::atomic<uint64_t> attr_done{0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return HADACORE_ERR_CUDA;
+  auto kern = fwht_f32_pair_kernel<st, nt, groups>;
+  if (!ensure_smem_attr(kern, smem, attr_done, dev)) return HADACORE_ERR_CUDA;
+  // co-resident clusters: a cluster's CTAs share a GPC, so not every SM pairs up --
+  // a grid with more clusters than fit at once would run a second wave
+  static std::atomic<int> max_clusters[kMaxDevices];
+  int cap = (dev >= 0 && dev < kMaxDevices) ? max_clusters[dev].load(std::memory_order_relaxed) : 0;
+  if (cap <= 0) {
+    cudaLaunchConfig_t q{};
+    q.gridDim = dim3(2 * (sm_count(dev) / 2));
+    q.blockDim = dim3((nt + 1) * 32);
+    q.dynamicSmemBytes = size_t(smem);
+    if (cudaOccupancyMaxActiveClusters(&cap, kern, &q) != cudaSuccess || cap <= 0) {
+      cudaGetLastError();
+      cap = sm_count(dev) / 2;
+    }
+    if (dev >= 0 && dev < kMaxDevices) max_clusters[dev].store(cap, std::memory_order_relaxed);
+  }
+  const int64_t clusters = m < cap ? m : int64_t(cap);
+  if (launch_pdl(kern, int(2 * clusters), (nt + 1) * 32, smem, stream, static_cast<const float*>(in),
+                 static_cast<float*>(out), m, scale) != cudaSuccess)
+    return HADACORE_ERR_CUDA;
+  return cudaPeekAtLastError() == cudaSuccess ? HADACORE_OK : HADACORE_ERR_CUDA;
+#else
   // pass 1: I_2 (x) H_2^14 on the two halves of every row (unnormalized), into `out`
   hadacore_status_t rc = launch_f32_fast<16384>(in, out, 2 * m, 1.f, stream);
   if (rc != HADACORE_OK) return rc;
@@ -366,6 +402,7 @@ hadacore_status_t launch_f32_32k(const void* in, void* out, int64_t m, float sca
                  static_cast<const float*>(out), static_cast<float*>(out), m, scale) != cudaSuccess)
     return HADACORE_ERR_CUDA;
   return cudaPeekAtLastError() == cudaSuccess ? HADACORE_OK : HADACORE_ERR_CUDA;
+#endif
 }
 
 hadacore_status_t dispatch_f32(const void* in, void* out, int64_t m, int64_t n, float scale, cudaStream_t st) {
@@ -677,7 +714,9 @@ extern "C" int hadacore_launches_per_call(int64_t m, int64_t n) {
 
 extern "C" int hadacore_launches_per_call_dtype(int64_t m, int64_t n, hadacore_dtype_t dtype) {
 #ifndef HC_F32_SIMPLE
+#ifdef HC_F32_TWO_PASS
   if (dtype == HADACORE_F32 && m > 0 && n == 32768) return 2;  // two passes (fwht_f32.cuh)
+#endif
 #endif
   return hadacore_launches_per_call(m, n);
 }
