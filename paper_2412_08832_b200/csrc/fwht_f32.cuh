@@ -25,20 +25,30 @@
 
 namespace hadacore {
 
-// Phase P >= 1 of the fp32 kernel on a tile of `rows` whole rows in shared memory:
-// bits 5P .. 5P+w-1 (w <= 5) over columns of CW = 2^w floats at stride 2^(5P); a lane
-// takes CPL = 32 / CW columns per iteration (NT*32 apart, so a warp's accesses are
-// 32 consecutive words); the last phase multiplies by `scale`.
-template <int N, int P, int NT>
+// Bit plan of the fp32 kernel (k = log2 n): phase 0 takes B0 bits on 2^max(B0, 5)
+// contiguous floats per lane; later phases take W bits starting at LO.  Widths
+// are balanced so that no phase spends a full shared-memory round trip on a
+// single bit (k = 11: 6 + 5, k = 12: 6 + 6 instead of 5 + 5 + 1, 5 + 5 + 2).
+template <int K>
+struct F32Plan {
+  static constexpr int B0 = (K == 11 || K == 12) ? 6 : (K < 5 ? K : 5);
+  static constexpr int NPH = K <= 5 ? 1 : (K <= 12 ? 2 : 3);
+  static constexpr int W1 = NPH == 1 ? 0 : (K == 13 ? 4 : (K - B0 < 5 ? K - B0 : (K == 12 ? 6 : 5)));
+  static constexpr int LO2 = B0 + W1;
+  static constexpr int W2 = NPH == 3 ? K - LO2 : 0;
+};
+
+// Phase of the fp32 kernel on a tile of `rows` whole rows in shared memory: bits
+// LO .. LO+W-1 over columns of CW = 2^W floats at stride 2^LO; a lane takes
+// CPL = max(1, 32 / CW) columns per iteration (NT*32 apart, so a warp's accesses are
+// 32 consecutive words); LAST multiplies by `scale`.
+template <int N, int LO, int W, bool LAST, int NT>
 __device__ __forceinline__ void f32_phase(float* tb, int rows, int tid, float scale) {
   constexpr int K = log2_n<N>();
-  constexpr int NPH = (K + 4) / 5;
-  constexpr int LO = 5 * P;
-  constexpr int W = (K - LO) < 5 ? (K - LO) : 5;
-  constexpr int CW = 1 << W, CPL = 32 / CW, LPR = K - W;
+  constexpr int CW = 1 << W, CPL = CW >= 32 ? 1 : 32 / CW, LPR = K - W, VL = CW * CPL;
   const int cols = rows << LPR;
   for (int q0 = tid; q0 < cols; q0 += NT * 32 * CPL) {
-    float v[32];
+    float v[VL];
     int base[CPL];
 #pragma unroll
     for (int k2 = 0; k2 < CPL; ++k2) {
@@ -51,15 +61,15 @@ __device__ __forceinline__ void f32_phase(float* tb, int rows, int tid, float sc
 #pragma unroll
     for (int b = 0; b < W; ++b)
 #pragma unroll
-      for (int e = 0; e < 32; ++e)
+      for (int e = 0; e < VL; ++e)
         if (!(e & (1 << b))) {
           const float p0 = v[e], p1 = v[e | (1 << b)];
           v[e] = p0 + p1;
           v[e | (1 << b)] = p0 - p1;
         }
-    if constexpr (P == NPH - 1) {
+    if constexpr (LAST) {
 #pragma unroll
-      for (int e = 0; e < 32; ++e) v[e] *= scale;
+      for (int e = 0; e < VL; ++e) v[e] *= scale;
     }
 #pragma unroll
     for (int k2 = 0; k2 < CPL; ++k2)
@@ -74,10 +84,13 @@ __global__ void __launch_bounds__((NT + 1) * 32, 1)
     fwht_f32_fast_kernel(const float* __restrict__ in, float* __restrict__ out, int64_t total_bytes,
                          int64_t num_tiles, float scale) {
   constexpr int K = log2_n<N>();
-  constexpr int NPH = (K + 4) / 5;              // phases of <= 5 bits
-  constexpr int K0 = K < 5 ? K : 5;             // bits of phase 0
-  constexpr uint32_t M0 = K0 > 2 ? ((1u << (K0 - 2)) - 1u) : 0u;  // transformed granule bits of phase 0
-  static_assert(TILE_BYTES % 128 == 0 && (N < 32 || TILE_BYTES % (4 * N) == 0), "tile layout");
+  using PL = F32Plan<K>;
+  constexpr int NPH = PL::NPH;
+  constexpr int K0 = PL::B0;                    // bits of phase 0
+  constexpr int V0 = K0 > 5 ? 64 : 32;          // floats per lane in phase 0
+  constexpr int G0 = V0 / 4;                    // granules per lane in phase 0 (XOR on the low 3 bits)
+  constexpr uint32_t M0 = K0 > 2 ? ((1u << (K0 - 2)) - 1u) & 7u : 0u;  // transformed XOR-ed granule bits
+  static_assert(TILE_BYTES % (4 * V0) == 0 && (N < 32 || TILE_BYTES % (4 * N) == 0), "tile layout");
 
   extern __shared__ __align__(1024) uint8_t smem[];
   SchedCtl* ctl = reinterpret_cast<SchedCtl*>(smem + STAGES * TILE_BYTES);
@@ -177,13 +190,13 @@ __global__ void __launch_bounds__((NT + 1) * 32, 1)
     const int bytes = tile_bytes(tile);
     const int b16 = bytes & ~15;
 
-    // ---- phase 0: bits 0 .. K0-1 on 32 contiguous floats per lane
-    const int items = (bytes + 127) / 128;
+    // ---- phase 0: bits 0 .. K0-1 on V0 contiguous floats per lane
+    const int items = (bytes + 4 * V0 - 1) / (4 * V0);
     for (int item = tid; item < items; item += NT * 32) {
-      float v[32];
+      float v[V0];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const int gi = item * 8 + int(uint32_t(j) ^ c);
+      for (int j = 0; j < G0; ++j) {
+        const int gi = item * G0 + int(uint32_t(j) ^ c);
         float4 w;
         if (N >= 32 || 16 * gi + 16 <= b16) {
           w = *reinterpret_cast<const float4*>(tb + 4 * gi);
@@ -201,28 +214,29 @@ __global__ void __launch_bounds__((NT + 1) * 32, 1)
 #pragma unroll
       for (int b = 0; b < (K0 < 2 ? K0 : 2); ++b)  // element bits inside a granule
 #pragma unroll
-        for (int e = 0; e < 32; ++e)
+        for (int e = 0; e < V0; ++e)
           if (!(e & (1 << b))) {
             const float p0 = v[e], p1 = v[e | (1 << b)];
             v[e] = p0 + p1;
             v[e | (1 << b)] = p0 - p1;
           }
 #pragma unroll
-      for (int b = 0; b < K0 - 2; ++b)  // granule bits, sign-folded (see header)
+      for (int b = 0; b < K0 - 2; ++b)  // granule bits, sign-folded where XOR-ed (see header)
 #pragma unroll
-        for (int e = 0; e < 32; ++e)
+        for (int e = 0; e < V0; ++e)
           if (!(e & (4 << b))) {
             const float p0 = v[e], p1 = v[e | (4 << b)];
-            v[e] = fmaf(p0, al[b], p1);
-            v[e | (4 << b)] = fmaf(p1, -al[b], p0);
+            const float a = b < 3 ? al[b < 3 ? b : 0] : 1.f;
+            v[e] = fmaf(p0, a, p1);
+            v[e | (4 << b)] = fmaf(p1, -a, p0);
           }
       if constexpr (NPH == 1) {
 #pragma unroll
-        for (int e = 0; e < 32; ++e) v[e] *= scale;
+        for (int e = 0; e < V0; ++e) v[e] *= scale;
       }
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const int gi = item * 8 + int(uint32_t(j) ^ c);
+      for (int j = 0; j < G0; ++j) {
+        const int gi = item * G0 + int(uint32_t(j) ^ c);
         const float4 w = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
         if (N >= 32 || 16 * gi + 16 <= b16) {
           *reinterpret_cast<float4*>(tb + 4 * gi) = w;
@@ -234,14 +248,14 @@ __global__ void __launch_bounds__((NT + 1) * 32, 1)
       }
     }
 
-    // ---- phases 1..NPH-1: bits 5p .. 5p+w-1, columns of 2^w floats at stride 2^(5p)
+    // ---- phases 1..NPH-1: bits LO .. LO+W-1 (F32Plan), columns of 2^W floats at stride 2^LO
     if constexpr (NPH > 1) {
       const int rows = bytes / (4 * N);
       named_bar_sync(1, NT * 32);
-      f32_phase<N, 1, NT>(tb, rows, tid, scale);
+      f32_phase<N, PL::B0, PL::W1, NPH == 2, NT>(tb, rows, tid, scale);
       if constexpr (NPH > 2) {
         named_bar_sync(1, NT * 32);
-        f32_phase<N, 2, NT>(tb, rows, tid, scale);
+        f32_phase<N, PL::LO2, PL::W2, true, NT>(tb, rows, tid, scale);
       }
     }
     fence_proxy_async_smem();
@@ -407,9 +421,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((NT + 1) * 32, 1)
               make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
       }
       named_bar_sync(1 + grp, NTG * 32);
-      f32_phase<NH, 1, NTG>(tb, 1, tid, 1.f);
+      f32_phase<NH, 5, 5, false, NTG>(tb, 1, tid, 1.f);
       named_bar_sync(1 + grp, NTG * 32);
-      f32_phase<NH, 2, NTG>(tb, 1, tid, 1.f);  // the last in-CTA phase (scale applied below)
+      f32_phase<NH, 10, 4, false, NTG>(tb, 1, tid, 1.f);  // the last in-CTA phase (scale applied below)
       static_assert(K == 14, "half rows of 2^14");
       // this thread's half is final: tell the partner (release at cluster scope)
       const uint32_t tb_addr = smem_addr(tb);

@@ -45,6 +45,9 @@ def main():
         name = d[hdr.index("Kernel Name")]
         mm = re.search(r"(fwht_\w+)<(?:\(int\))?(\d+), (?:\(int\))?(\d+)", name)
         kern, n, dt = (mm.group(1), int(mm.group(2)), "fp16" if mm.group(3) == "0" else "bf16") if mm else (name[:30], 0, "?")
+        if "f32" in kern or "f32_pair" in name:  # fp32 kernels: <N, TILE_BYTES, ...>, the pair kernel is n = 2^15
+            kern = "fwht_f32_pair_kernel" if "pair" in name else kern
+            n, dt = (32768 if "pair" in name else n), "fp32"
         v = {}
         for k, col in KEYS.items():
             if col in hdr:
@@ -63,7 +66,7 @@ def main():
                     except ValueError:
                         pass
         stalls.sort(reverse=True)
-        alg = 4.0 * (1 << 28)
+        alg = (8.0 if dt == "fp32" else 4.0) * (1 << 28)
         ratio = (v.get("rd", 0) + v.get("wr", 0)) / alg
         lines.append(f"| {kern} | {n} | {dt} | {v.get('dur_us', 0):.1f} | {v.get('rd', 0)/1e6:.1f} | {v.get('wr', 0)/1e6:.1f} | "
                      f"{ratio:.3f} | {v.get('dram_pct', 0):.1f} | {v.get('issue_pct', 0):.1f} | {v.get('warps_pct', 0):.1f} | "
@@ -71,7 +74,8 @@ def main():
                      + ", ".join(f"{nm} {x:.2f}" for x, nm in stalls[:3]) + " |")
         traffic.append({"n": n, "dtype": dt, "dram_bytes": v.get("rd", 0) + v.get("wr", 0), "duration_us": v.get("dur_us")})
     open(out_md, "w").write(f"# ncu --set full summary of `{rep}`\n\nAlgorithmic bytes per launch = 4 B x 2^28 = "
-                            f"{4 * (1 << 28)} (read + write once).\n\n" + "\n".join(lines) + "\n")
+                            f"{4 * (1 << 28)} (16-bit; 8 B x 2^28 for fp32; read + write once).\n\n"
+                            + "\n".join(lines) + "\n")
     print("\n".join(lines))
     if traffic_path:
         avg = sum(t["dram_bytes"] for t in traffic) / max(1, len(traffic))
