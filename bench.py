@@ -35,6 +35,7 @@ METRIC = "FWHT HBM GB/s vs n=2^7..2^15 (bf16/fp16) at 1/2/4/8 B200; % of 8 TB/s"
 NS = [1 << k for k in range(7, 16)]
 SMALL_NS = [1 << k for k in range(1, 7)]  # NEXT-2: rows shorter than the paper's 2^7 floor
 ELEMS = 1 << 28
+C5_ELEMS = 1 << 33  # BASELINE config C5: bf16 n = 2^15, 2^33 elements in total
 NOMINAL_HBM_GBS = 8000.0
 FALLBACK_HBM_GBS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback
 
@@ -49,10 +50,11 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
-    ap.add_argument("--workload", choices=["fwht", "quant-e4m3", "quant-int8", "qk-rotate", "small", "f32"], default="fwht",
+    ap.add_argument("--workload", choices=["fwht", "quant-e4m3", "quant-int8", "qk-rotate", "small", "f32", "c5"], default="fwht",
                     help="fwht = the metric's C3 sweep (default); quant-* = the fused FWHT + per-row "
                          "quantization row (NEXT-1) on the same inputs; small = n=2^1..2^6 (NEXT-2); "
-                         "f32 = the fp32 path over n=2^1..2^15 (NEXT-2)")
+                         "f32 = the fp32 path over n=2^1..2^15 (NEXT-2); c5 = BASELINE config C5: bf16 "
+                         "n=2^15, 2^33 elements row-sharded over the ranks (strong scaling)")
     return ap.parse_args()
 
 
@@ -236,6 +238,10 @@ def config_block(args, world):
         ns = SMALL_NS + NS
         wl = ("NEXT-2 fp32 path: n=2^1..2^15 fp32, 2^28 elements (1 GiB in, 1 GiB out) per n per GPU, "
               "out-of-place, normalized (scale=1/sqrt(n))")
+    if getattr(args, "workload", "fwht") == "c5":
+        ns = [32768]
+        wl = ("C5: bf16 n=2^15, 2^33 elements (262144 rows, 16 GiB in + 16 GiB out) row-sharded across the "
+              "ranks, no collective on the hot path, out-of-place, normalized")
     if getattr(args, "workload", "fwht") == "small":
         wl = ("NEXT-2 small sizes: n=2^1..2^6 x {fp16, bf16}, 2^28 elements per (n, dtype) per GPU, "
               "out-of-place, normalized (scale=1/sqrt(n))")
@@ -244,9 +250,11 @@ def config_block(args, world):
               "H = max(1, 4096/n); the Q and K heads (2/3 of it) transformed in place, normalized")
     return {"workload": wl,
             "elements_per_launch": args.elems, "ns": ns,
-            "dtypes": ["fp32"] if getattr(args, "workload", "fwht") == "f32" else ["fp16", "bf16"],
-            "launches_per_step": (1 if getattr(args, "workload", "fwht") == "f32" else 2) * len(ns), "path": getattr(args, "workload", "fwht"),
-            "l2": "no flush: every launch reads a 512 MiB input and writes a 512 MiB output (> 126 MB L2)",
+            "dtypes": {"f32": ["fp32"], "c5": ["bf16"]}.get(getattr(args, "workload", "fwht"), ["fp16", "bf16"]),
+            "launches_per_step": (1 if getattr(args, "workload", "fwht") in ("f32", "c5") else 2) * len(ns), "path": getattr(args, "workload", "fwht"),
+            "l2": ("no flush: each rank's launch reads 16/N GiB and writes 16/N GiB (> 126 MB L2)"
+                   if getattr(args, "workload", "fwht") == "c5" else
+                   "no flush: every launch reads a 512 MiB input and writes a 512 MiB output (> 126 MB L2)"),
             "parallelism": f"row-sharded x{world}, no collective on the hot path" if world > 1 else "single GPU"}
 
 
@@ -270,10 +278,20 @@ def main():
     # resident inputs: one 2^28-element matrix per dtype (each (n) is a view), rows
     # [rank*m, (rank+1)*m) of the global seeded matrix (weak scaling)
     xin, xout = {}, {}
-    for dt in (torch.float16, torch.bfloat16):
+    c5 = args.workload == "c5"
+    c5_rows = (C5_ELEMS // 32768)
+    if c5:
+        # C5: the global 2^33-element bf16 matrix (262144 rows of 2^15); this rank's rows
+        from paper_2412_08832_b200.shard import row_range
+        lo, hi = row_range(c5_rows, rank, world)
+        args.elems = (hi - lo) * 32768
+    for dt in ((torch.bfloat16,) if c5 else (torch.float16, torch.bfloat16)):
         buf = torch.empty(args.elems, dtype=dt, device=dev)
-        synthetic.generate(args.elems // 256, 256, dt, synthetic.seed_for(2, dt), row0=rank * (args.elems // 256),
-                           out=buf.view(-1, 256))
+        if c5:
+            synthetic.generate(hi - lo, 32768, dt, synthetic.seed_for(5, dt), row0=lo, out=buf.view(-1, 32768))
+        else:
+            synthetic.generate(args.elems // 256, 256, dt, synthetic.seed_for(2, dt),
+                               row0=rank * (args.elems // 256), out=buf.view(-1, 256))
         xin[dt] = buf
     obuf = torch.empty(args.elems, dtype=torch.float16, device=dev)
     stream = torch.cuda.current_stream(dev)
@@ -286,6 +304,8 @@ def main():
                            row0=rank * (args.elems // 256), out=xin[torch.float32].view(-1, 256))
         obuf = torch.empty(args.elems, dtype=torch.float32, device=dev)
     pairs = [(dt, n) for dt in ((torch.float32,) if f32 else (torch.float16, torch.bfloat16)) for n in ns]
+    if c5:
+        ns, pairs = [32768], [(torch.bfloat16, 32768)]
     quant = args.workload.startswith("quant")
     qtype = args.workload.split("-")[1] if quant else None
     if quant:
@@ -377,6 +397,8 @@ def main():
     if rotate:
         bytes_per_launch = sum(4.0 * e for e in elems_of.values()) / len(pairs)
     total_bytes = bytes_per_launch * len(pairs) * args.steps * world
+    if c5:  # strong scaling: the whole 2^33-element job per step, whatever the rank count
+        total_bytes = 4.0 * C5_ELEMS * args.steps
     value = total_bytes / (t_max * 1e-3) / 1e9
 
     # per-(dtype, n) breakdown and the roofline of the kernel (device time per launch)
@@ -453,6 +475,9 @@ def main():
                                            "n=2^7..2^15 (bf16/fp16 in, 8-bit codes + fp32 row scales out)")
         if f32:
             metric = "FWHT HBM GB/s vs n=2^1..2^15, fp32 path (NEXT-2; north_star's fp32 path, tolerance 1e-5)"
+        if c5:
+            metric = ("C5: FWHT HBM GB/s, bf16 n=2^15, 2^33 elements row-sharded across the GPUs "
+                      "(whole-job bytes / max-over-ranks time; strong scaling)")
         if args.workload == "small":
             metric = "FWHT HBM GB/s vs n=2^1..2^6 (bf16/fp16), rows shorter than the paper's 2^7 (NEXT-2)"
         if rotate:
@@ -461,8 +486,9 @@ def main():
         line = {
             "metric": metric, "value": round(value, 1), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(t_max / args.steps, 4), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None,
-            "dtype": "fp32" if f32 else "fp16+bf16 (fp32 last-stage accumulate)",
+            "scaling": "strong" if c5 else "weak", "vs_baseline": None,
+            "dtype": "fp32" if f32 else ("bf16 (fp32 last-stage accumulate)" if c5 else
+                                         "fp16+bf16 (fp32 last-stage accumulate)"),
             "data": "synthetic (counter-based N(0,1), synthetic/)", "config": config_block(args, world),
             "pct_of_8TBps": round(100.0 * value / world / NOMINAL_HBM_GBS, 2),
             "per_n_GBps": per_n, "roofline": roofline, "cpu_baseline": cpu_baseline, "e2e": e2e,

@@ -182,8 +182,8 @@ int hadacore_version(void);
  */
 int hadacore_launches_per_call(int64_t m, int64_t n);
 
-/* The same for a given dtype: the fp32 path takes two launches at n = 2^15 (its
- * rows of 128 KiB are transformed as two halves, then combined). */
+/* The same for a given dtype (every path is one launch in the default build; the
+ * HC_F32_TWO_PASS build takes two for fp32 at n = 2^15). */
 int hadacore_launches_per_call_dtype(int64_t m, int64_t n, hadacore_dtype_t dtype);
 
 #ifdef __cplusplus

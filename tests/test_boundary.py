@@ -128,7 +128,7 @@ def test_status_strings_and_version(lib):
     assert lib.hadacore_launches_per_call(10, 256) == 1
     assert lib.hadacore_launches_per_call(10, 100) == 0
     assert lib.hadacore_launches_per_call(10, 2) == 1
-    assert lib.hadacore_launches_per_call_dtype(10, 32768, 2) == 2     # fp32 n = 2^15: two passes
+    assert lib.hadacore_launches_per_call_dtype(10, 32768, 2) == 1     # fp32 n = 2^15: one cluster launch
     assert lib.hadacore_launches_per_call_dtype(10, 32768, 1) == 1
     assert lib.hadacore_launches_per_call_dtype(0, 32768, 2) == 0
 

@@ -292,3 +292,52 @@ def test_torch_custom_ops(hc):
     # traceable by torch.compile (fake implementation registered)
     f = torch.compile(lambda t: torch.ops.hadacore.fwht(t, None) * 2, fullgraph=True)
     assert torch.equal(f(x).view(torch.int16), (y * 2).view(torch.int16))
+
+
+# ---------------------------------------------------------------- BASELINE configs at full size
+@pytest.mark.slow
+@pytest.mark.parametrize("cfg", ["C1", "C2", "C4"])
+def test_named_configs_full_size(hc, cfg):
+    """BASELINE.json configs C1 (fp16 m=1024 n=256: every row vs the oracle), C2 (bf16
+    n=128, m=8*32*4096) and C4 (fp16 n=4096, m=16384): sampled rows vs the oracle and
+    norm preservation on every row."""
+    dtype, n, m = {"C1": (torch.float16, 256, 1024), "C2": (torch.bfloat16, 128, 8 * 32 * 4096),
+                   "C4": (torch.float16, 4096, 16384)}[cfg]
+    idx = {"C1": 0, "C2": 1, "C4": 3}[cfg]
+    x = torch.empty(m, n, dtype=dtype, device="cuda")
+    synthetic.generate(m, n, dtype, synthetic.seed_for(idx, dtype), out=x, dist="D1")
+    y = hc.hadacore_fwht(x)
+    rows = list(range(m)) if m <= 1024 else sorted(set([0, m - 1] + torch.randint(
+        0, m, (300,), generator=torch.Generator().manual_seed(idx)).tolist()))
+    assert rel_l2_rows(widen(y[rows]), oracle.fwht(widen(x[rows]))).max() <= TOL[dtype]
+    nx, ny = x.float().norm(dim=1), y.float().norm(dim=1)
+    assert ((ny - nx).abs() / nx).max().item() <= TOL[dtype]
+
+
+@pytest.mark.slow
+def test_c5_full_size_and_shard_invariance(hc):
+    """C5: bf16 n=2^15, 2^33 elements (16 GiB in, 16 GiB out) on one B200 -- the whole
+    strong-scaling job -- sampled rows vs the oracle, norm preservation on every row,
+    and the rows of each 8-GPU shard (shard.row_range) transformed on their own are
+    bitwise equal to the same rows of the whole run (sharding invariance)."""
+    from paper_2412_08832_b200.shard import row_range
+    n, m = 32768, (1 << 33) // 32768
+    dt = torch.bfloat16
+    x = torch.empty(m, n, dtype=dt, device="cuda")
+    synthetic.generate(m, n, dt, synthetic.seed_for(5, dt), out=x)
+    y = hc.hadacore_fwht(x)
+    torch.cuda.synchronize()
+    g = torch.Generator().manual_seed(5)
+    rows = sorted(set([0, m - 1] + torch.randint(0, m, (24,), generator=g).tolist()))
+    assert rel_l2_rows(widen(y[rows]), oracle.fwht(widen(x[rows]))).max() <= TOL[dt]
+    worst = 0.0
+    for r0 in range(0, m, 4096):
+        nx, ny = x[r0:r0 + 4096].float().norm(dim=1), y[r0:r0 + 4096].float().norm(dim=1)
+        worst = max(worst, ((ny - nx).abs() / nx).max().item())
+    assert worst <= TOL[dt]
+    for r in (0, 3, 7):
+        lo, hi = row_range(m, r, 8)
+        xs = synthetic.generate(hi - lo, n, dt, synthetic.seed_for(5, dt), row0=lo, device="cuda")
+        assert torch.equal(xs.view(torch.int16), x[lo:hi].view(torch.int16))   # generator keyed on global index
+        ys = hc.hadacore_fwht(xs)
+        assert torch.equal(ys.view(torch.int16), y[lo:hi].view(torch.int16))
