@@ -50,7 +50,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
-    ap.add_argument("--workload", choices=["fwht", "quant-e4m3", "quant-int8", "qk-rotate", "small", "f32", "c5"], default="fwht",
+    ap.add_argument("--workload", choices=["fwht", "quant-e4m3", "quant-int8", "quant-int4", "qk-rotate", "small", "f32", "c5"], default="fwht",
                     help="fwht = the metric's C3 sweep (default); quant-* = the fused FWHT + per-row "
                          "quantization row (NEXT-1) on the same inputs; small = n=2^1..2^6 (NEXT-2); "
                          "f32 = the fp32 path over n=2^1..2^15 (NEXT-2); c5 = BASELINE config C5: bf16 "
@@ -309,8 +309,9 @@ def main():
     quant = args.workload.startswith("quant")
     qtype = args.workload.split("-")[1] if quant else None
     if quant:
-        qbuf = torch.empty(args.elems, dtype=hc.QTYPES[qtype][1], device=dev)
+        qbuf = torch.empty(args.elems // (2 if qtype == "int4" else 1), dtype=hc.QTYPES[qtype][1], device=dev)
         sbuf = torch.empty(args.elems // 128, dtype=torch.float32, device=dev)
+    qb = 0.5 if qtype == "int4" else 1.0  # code bytes per element
 
     rotate = args.workload == "qk-rotate"
     qk = {}
@@ -331,7 +332,8 @@ def main():
             return
         x = xin[dt].view(-1, n)
         if quant:
-            hc.hadacore_fwht_quant(x, qtype=qtype, out=qbuf.view(-1, n), row_scale=sbuf[: x.shape[0]],
+            hc.hadacore_fwht_quant(x, qtype=qtype, out=qbuf.view(-1, n // 2 if qtype == "int4" else n),
+                                   row_scale=sbuf[: x.shape[0]],
                                    stream=stream)
             return
         o = obuf.view(-1, n) if f32 else obuf.view(torch.int16).view(dt).view(-1, n)
@@ -393,7 +395,7 @@ def main():
     # scale per row for the fused quantization (per-n average over the sweep)
     esize = 4 if f32 else 2
     bytes_per_launch = 2.0 * esize * args.elems if not quant else \
-        sum(3.0 * args.elems + 4.0 * (args.elems // n) for n in NS) / len(NS)
+        sum((2.0 + qb) * args.elems + 4.0 * (args.elems // n) for n in NS) / len(NS)
     if rotate:
         bytes_per_launch = sum(4.0 * e for e in elems_of.values()) / len(pairs)
     total_bytes = bytes_per_launch * len(pairs) * args.steps * world
@@ -406,7 +408,7 @@ def main():
     for k, (dt, n) in enumerate(pairs):
         ts = sorted(per[k::len(pairs)])
         med = ts[len(ts) // 2]
-        b_n = 2.0 * esize * elems_of[(dt, n)] if not quant else 3.0 * args.elems + 4.0 * (args.elems // n)
+        b_n = 2.0 * esize * elems_of[(dt, n)] if not quant else (2.0 + qb) * args.elems + 4.0 * (args.elems // n)
         per_n.setdefault({torch.float16: "fp16", torch.bfloat16: "bf16", torch.float32: "fp32"}[dt], {})[str(n)] = round(b_n / (med * 1e-3) / 1e9, 1)
     # roofline over the timed region: every launch of the step is the same transform
     # (one per (dtype, n)), so the kernel's average launch duration is the region time
@@ -472,7 +474,8 @@ def main():
 
     if rank == 0:
         metric = METRIC if not quant else (f"Fused FWHT + per-row {qtype.upper()} quantization HBM GB/s vs "
-                                           "n=2^7..2^15 (bf16/fp16 in, 8-bit codes + fp32 row scales out)")
+                                           "n=2^7..2^15 (bf16/fp16 in, " + ("4" if qtype == "int4" else "8") +
+                                           "-bit codes + fp32 row scales out)")
         if f32:
             metric = "FWHT HBM GB/s vs n=2^1..2^15, fp32 path (NEXT-2; north_star's fp32 path, tolerance 1e-5)"
         if c5:

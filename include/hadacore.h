@@ -65,7 +65,8 @@ typedef enum {
 typedef enum {
   HADACORE_Q_E4M3 = 0, /* FP8 E4M3 ("e4m3fn": no infinities, max finite 448), RNE, saturating */
   HADACORE_Q_INT8 = 1, /* signed 8-bit integer, RNE, clamped to [-127, 127] */
-  HADACORE_Q_INT4 = 2  /* signed 4-bit integer, RNE, clamped to [-7, 7]: hadacore_fake_quant only */
+  HADACORE_Q_INT4 = 2  /* signed 4-bit integer, RNE, clamped to [-7, 7]; two per byte, element 2j in the
+                          low nibble of byte j (two's complement) */
 } hadacore_qtype_t;
 
 typedef enum {
@@ -133,10 +134,10 @@ hadacore_status_t hadacore_fwht_strided(const void* in, void* out, int64_t m_out
  * paper's future work "fused Hadamard transform and quantization", P:207 [Sec. 5],
  * for its FP8-attention use, P:180 [Sec. 4.2]):
  *     y = scale * H_n * in[i, :]            (as hadacore_fwht, never written out)
- *     row_scale[i] = max_j |y_j| / Q        (Q = 448 for E4M3, 127 for INT8; 1 if y == 0)
- *     out_q[i, j]  = round(y_j / row_scale[i])   (E4M3 saturating / INT8 clamped)
+ *     row_scale[i] = max_j |y_j| / Q        (Q = 448 E4M3, 127 INT8, 7 INT4; 1 if y == 0)
+ *     out_q[i, j]  = round(y_j / row_scale[i])   (E4M3 saturating / INT8, INT4 clamped)
  * so out_q[i, j] * row_scale[i] ~= y_j.  A row containing Inf/NaN gets a non-finite
- * row_scale.  out_q: m x n bytes, row-major, 16-byte aligned; row_scale: m floats
+ * row_scale.  out_q: m x n bytes (m x n/2 for INT4), row-major, 16-byte aligned; row_scale: m floats
  * (fp32).  Neither may overlap `in`.  n = 2^7..2^15.  HBM traffic: 2 B read + 1 B
  * written per element.
  * Same validation, stream and error behaviour as hadacore_fwht; qtype outside the

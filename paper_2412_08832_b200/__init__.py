@@ -35,7 +35,7 @@ STATUS = {
     7: "HADACORE_ERR_SCALE", 8: "HADACORE_ERR_CUDA", 9: "HADACORE_ERR_WORKSPACE",
 }
 _DTYPES = {torch.float16: 0, torch.bfloat16: 1, torch.float32: 2}
-QTYPES = {"e4m3": (0, torch.float8_e4m3fn), "int8": (1, torch.int8)}
+QTYPES = {"e4m3": (0, torch.float8_e4m3fn), "int8": (1, torch.int8), "int4": (2, torch.uint8)}  # int4: 2 per byte
 LAB_QTYPES = {"e4m3": 0, "int8": 1, "int4": 2}  # hadacore_fake_quant (quant lab, NEXT-4)
 
 
@@ -170,8 +170,10 @@ def hadacore_fwht_quant(x: torch.Tensor, qtype: str = "e4m3", scale: float | Non
     """Fused transform + per-row symmetric quantization (C: hadacore_fwht_quant).
 
     Returns ``(q, row_scale)``: ``q`` has x's shape and dtype float8_e4m3fn ("e4m3")
-    or int8 ("int8"); ``row_scale`` is float32 with x's shape minus the last dim, so
-    ``q.float() * row_scale[..., None]`` ~= ``hadacore_fwht(x, scale=scale)``.
+    or int8 ("int8"), or x's shape with the last dim halved and dtype uint8 ("int4":
+    element 2j in the low nibble of byte j, two's complement, codes in [-7, 7]);
+    ``row_scale`` is float32 with x's shape minus the last dim, so
+    ``codes * row_scale[..., None]`` ~= ``hadacore_fwht(x, scale=scale)``.
     """
     m, n = _shape(x)
     if qtype not in QTYPES:
@@ -181,12 +183,13 @@ def hadacore_fwht_quant(x: torch.Tensor, qtype: str = "e4m3", scale: float | Non
         raise HadacoreError(6, "the fused quantization takes float16/bfloat16 inputs")
     if not x.is_cuda or not x.is_contiguous():
         raise HadacoreError(8, "x must be a contiguous CUDA tensor")
+    qshape = x.shape if qtype != "int4" else (*x.shape[:-1], n // 2)
     if out is None:
-        out = torch.empty(x.shape, dtype=qdt, device=x.device)
+        out = torch.empty(qshape, dtype=qdt, device=x.device)
     if row_scale is None:
         row_scale = torch.empty(x.shape[:-1], dtype=torch.float32, device=x.device)
-    if out.dtype != qdt or out.shape != x.shape or not out.is_contiguous() or out.device != x.device:
-        raise HadacoreError(3, f"out must be a contiguous {qdt} tensor with x's shape on x's device")
+    if out.dtype != qdt or tuple(out.shape) != tuple(qshape) or not out.is_contiguous() or out.device != x.device:
+        raise HadacoreError(3, f"out must be a contiguous {qdt} tensor of shape {tuple(qshape)} on x's device")
     if row_scale.dtype != torch.float32 or row_scale.numel() != m or not row_scale.is_contiguous():
         raise HadacoreError(3, "row_scale must be a contiguous float32 tensor with one entry per row")
     if scale is None:

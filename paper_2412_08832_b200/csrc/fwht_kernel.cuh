@@ -400,10 +400,17 @@ __device__ __forceinline__ void simt_fwht_pack(const uint32_t x[4], uint32_t mas
 // per-row symmetric scale s = max|y| / Q (Q = 448 for FP8 E4M3, 127 for INT8; s = 1
 // for an all-zero row), codes = RNE(y / s) (E4M3 saturating, INT8 clamped to +-127).
 // A non-finite value in a row makes that row's scale non-finite.
-enum : int { QT_NONE = -1, QT_E4M3 = 0, QT_INT8 = 1 };
+enum : int { QT_NONE = -1, QT_E4M3 = 0, QT_INT8 = 1, QT_INT4 = 2 };
 template <int QT>
 __host__ __device__ constexpr float qmax_of() {
-  return QT == QT_E4M3 ? 448.f : 127.f;
+  return QT == QT_E4M3 ? 448.f : (QT == QT_INT8 ? 127.f : 7.f);
+}
+// INT4 codes ("Q = 7 (INT4)", QuaRot-style 4-bit activations): two
+// per byte, element 2j in the low nibble of byte j (two's complement).  Bytes in
+// b0..b3 hold the codes' two's-complement low bytes; returns the 4 nibbles in 16 bits.
+__device__ __forceinline__ uint32_t nibbles4(uint32_t b0, uint32_t b1, uint32_t b2, uint32_t b3) {
+  const uint32_t w = __byte_perm(__byte_perm(b0, b1, 0x0040), __byte_perm(b2, b3, 0x0040), 0x5410) & 0x0F0F0F0Fu;
+  return __byte_perm(w | (w >> 4), 0u, 0x0020) & 0xFFFFu;  // bytes 0 and 2 of w | w >> 4
 }
 // max of |v| that propagates NaN (max.NaN, one FMNMX.NAN): a NaN anywhere in a row
 // poisons the row's scale, an Inf makes it Inf
@@ -424,6 +431,10 @@ __device__ __forceinline__ uint32_t quant4(float a, float b, float c, float d) {
     asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(lo) : "f"(b), "f"(a));
     asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(hi) : "f"(d), "f"(c));
     return uint32_t(lo) | (uint32_t(hi) << 16);
+  } else if constexpr (QT == QT_INT4) {
+    const float a2 = fminf(fmaxf(rintf(a), -7.f), 7.f), b2 = fminf(fmaxf(rintf(b), -7.f), 7.f);
+    const float c2 = fminf(fmaxf(rintf(c), -7.f), 7.f), d2 = fminf(fmaxf(rintf(d), -7.f), 7.f);
+    return nibbles4(uint32_t(int(a2)), uint32_t(int(b2)), uint32_t(int(c2)), uint32_t(int(d2)));
   } else {
     // RNE with saturation to [-128, 127]; -128 cannot occur because |v| <= Q (up to
     // the rounding of the reciprocal, which stays below 127.5)
@@ -473,9 +484,16 @@ __device__ __forceinline__ uint32_t quant4_fast(float a, float b, float c, float
   } else {
     fma2(a, b, m, 12582912.f);  // 1.5 * 2^23
     fma2(c, d, m, 12582912.f);
+    if constexpr (QT == QT_INT4)  // |v m| <= 7 (1 + 2^-8)(1 + 2^-22) < 7.5: the low nibble is the code
+      return nibbles4(__float_as_uint(a), __float_as_uint(b), __float_as_uint(c), __float_as_uint(d));
     return __byte_perm(__byte_perm(__float_as_uint(a), __float_as_uint(b), 0x0040),
                        __byte_perm(__float_as_uint(c), __float_as_uint(d), 0x0040), 0x5410);
   }
+}
+__device__ __forceinline__ void stg16_if(void* p, uint32_t v, bool pred) {
+  asm volatile("{.reg .pred q;\n .reg .b16 h;\n setp.ne.b32 q, %2, 0;\n cvt.u16.u32 h, %1;\n @q st.global.b16 [%0], h;}"
+               ::"l"(p), "r"(v), "r"(int(pred))
+               : "memory");
 }
 // predicated global stores (no divergent branch around the epilogue)
 __device__ __forceinline__ void stg32_if(void* p, uint32_t v, bool pred) {
@@ -790,7 +808,11 @@ __global__ void __launch_bounds__((NT + 1) * 32, CTAS)
               int64_t i = 0, j = 0;
               const bool ok = FLAT ? 2 * f + h < rows_left : tr.at(g, 2 * f + h, i, j);
               const int64_t row = FLAT ? tr.i0 + 2 * f + h : i * g.m_inner + j;  // codes/scales: contiguous [rows, n]
-              stg32_if(out_q + row * N + lane * 4, code, ok);
+              if constexpr (QT == QT_INT4) {
+                stg16_if(out_q + row * (N / 2) + lane * 2, code, ok);
+              } else {
+                stg32_if(out_q + row * N + lane * 4, code, ok);
+              }
               stf32_if(row_scale + row, sc, ok && lane == 0);
             }
           } else {
@@ -866,7 +888,11 @@ __global__ void __launch_bounds__((NT + 1) * 32, CTAS)
             int64_t i = 0, j = 0;
             const bool ok = FLAT ? r < rows_left : tr.at(g, r, i, j);
             const int64_t row = FLAT ? tr.i0 + r : i * g.m_inner + j;
-            stg64_if(out_q + row * N + lane * 8, c0, c1, ok);
+            if constexpr (QT == QT_INT4) {
+              stg32_if(out_q + row * (N / 2) + lane * 4, c0 | (c1 << 16), ok);
+            } else {
+              stg64_if(out_q + row * N + lane * 8, c0, c1, ok);
+            }
             stf32_if(row_scale + row, sc, ok && lane == 0);
           } else {
             if constexpr (FLAT) {
@@ -1255,7 +1281,7 @@ __global__ void __launch_bounds__((NT + 1) * 32, CTAS)
         int64_t i = 0, j = 0;
         const bool ok = tr.at(g, team + NTEAMS * k, i, j);
         ok_r |= uint32_t(ok) << k;
-        q_r[k] = out_q + (i * g.m_inner + j) * N + lane * 8;
+        q_r[k] = out_q + (i * g.m_inner + j) * (QT == QT_INT4 ? N / 2 : N) + lane * (QT == QT_INT4 ? 4 : 8);
         stf32_if(row_scale + (i * g.m_inner + j), sc, ok && wt == 0 && lane == 0);
       }
       for (int i0 = wt; i0 < ITEMS1; i0 += P * U1) {
@@ -1286,7 +1312,11 @@ __global__ void __launch_bounds__((NT + 1) * 32, CTAS)
             c0 = quant4<QT>(v[0] * inv, v[1] * inv, v[2] * inv, v[3] * inv);
             c1 = quant4<QT>(v[4] * inv, v[5] * inv, v[6] * inv, v[7] * inv);
           }
-          stg64_if(qp + c * 256, c0, c1, (ok_r >> rl) & 1u);
+          if constexpr (QT == QT_INT4) {
+            stg32_if(qp + c * 128, c0 | (c1 << 16), (ok_r >> rl) & 1u);
+          } else {
+            stg64_if(qp + c * 256, c0, c1, (ok_r >> rl) & 1u);
+          }
         }
       }
       // (red[] is rewritten only after the next tile's phase-1 barrier: no race)

@@ -477,14 +477,21 @@ hadacore_status_t run(const void* in, void* out, int64_t m, int64_t n, int dtype
                                : dispatch_n<DT_BF16, QT_NONE>(in, out, nullptr, nullptr, L, n, scale, st);
 }
 
+template <int DT>
+hadacore_status_t run_quant_dt(const void* in, uint8_t* q, float* rs, const Layout& L, int64_t n, int qtype,
+                               float scale, cudaStream_t st) {
+  switch (qtype) {
+    case HADACORE_Q_E4M3: return dispatch_n<DT, QT_E4M3>(in, nullptr, q, rs, L, n, scale, st);
+    case HADACORE_Q_INT8: return dispatch_n<DT, QT_INT8>(in, nullptr, q, rs, L, n, scale, st);
+    default: return dispatch_n<DT, QT_INT4>(in, nullptr, q, rs, L, n, scale, st);
+  }
+}
+
 hadacore_status_t run_quant(const void* in, uint8_t* q, float* rs, int64_t m, int64_t n, int dtype, int qtype,
                             float scale, cudaStream_t st) {
   const Layout L = contiguous(m, n);
-  if (dtype == HADACORE_F16)
-    return qtype == HADACORE_Q_E4M3 ? dispatch_n<DT_F16, QT_E4M3>(in, nullptr, q, rs, L, n, scale, st)
-                                    : dispatch_n<DT_F16, QT_INT8>(in, nullptr, q, rs, L, n, scale, st);
-  return qtype == HADACORE_Q_E4M3 ? dispatch_n<DT_BF16, QT_E4M3>(in, nullptr, q, rs, L, n, scale, st)
-                                  : dispatch_n<DT_BF16, QT_INT8>(in, nullptr, q, rs, L, n, scale, st);
+  return dtype == HADACORE_F16 ? run_quant_dt<DT_F16>(in, q, rs, L, n, qtype, scale, st)
+                               : run_quant_dt<DT_BF16>(in, q, rs, L, n, qtype, scale, st);
 }
 
 hadacore_status_t run_strided(const void* in, void* out, const Layout& L, int64_t n, int dtype, float scale,
@@ -544,7 +551,7 @@ extern "C" hadacore_status_t hadacore_fwht_strided(const void* in, void* out, in
 extern "C" hadacore_status_t hadacore_fwht_quant(const void* in, void* out_q, float* row_scale, int64_t m,
                                                  int64_t n, hadacore_dtype_t dtype, hadacore_qtype_t qtype,
                                                  float scale, hadacore_stream_t stream) {
-  if (qtype != HADACORE_Q_E4M3 && qtype != HADACORE_Q_INT8) return HADACORE_ERR_DTYPE;
+  if (qtype != HADACORE_Q_E4M3 && qtype != HADACORE_Q_INT8 && qtype != HADACORE_Q_INT4) return HADACORE_ERR_DTYPE;
   if (dtype == HADACORE_F32) return HADACORE_ERR_DTYPE;  // the fused path takes 16-bit inputs
   if (!valid_n_paper(n)) return HADACORE_ERR_INVALID_N;
   // validate `in` (and m, n, dtype, scale) exactly like hadacore_fwht, with out = in
@@ -553,7 +560,8 @@ extern "C" hadacore_status_t hadacore_fwht_quant(const void* in, void* out_q, fl
   if (!out_q || !row_scale) return HADACORE_ERR_NULL;
   if ((reinterpret_cast<uintptr_t>(out_q) & 15u) || (reinterpret_cast<uintptr_t>(row_scale) & 3u))
     return HADACORE_ERR_MISALIGNED;
-  const size_t in_bytes = size_t(m) * size_t(n) * 2, q_bytes = size_t(m) * size_t(n), s_bytes = size_t(m) * 4;
+  const size_t in_bytes = size_t(m) * size_t(n) * 2, s_bytes = size_t(m) * 4;
+  const size_t q_bytes = size_t(m) * size_t(n) / (qtype == HADACORE_Q_INT4 ? 2 : 1);  // INT4: two codes per byte
   if (ranges_overlap(in, in_bytes, out_q, q_bytes) || ranges_overlap(in, in_bytes, row_scale, s_bytes) ||
       ranges_overlap(out_q, q_bytes, row_scale, s_bytes))
     return HADACORE_ERR_OVERLAP;

@@ -62,5 +62,6 @@ def fwht_quant(x: torch.Tensor, qtype: str = "e4m3", scale: float | None = None)
 
 @fwht_quant.register_fake
 def _(x: torch.Tensor, qtype: str = "e4m3", scale: float | None = None):
-    return (torch.empty(x.shape, dtype=QTYPES[qtype][1], device=x.device),
+    shape = x.shape if qtype != "int4" else (*x.shape[:-1], x.shape[-1] // 2)  # int4: two codes per byte
+    return (torch.empty(shape, dtype=QTYPES[qtype][1], device=x.device),
             torch.empty(x.shape[:-1], dtype=torch.float32, device=x.device))

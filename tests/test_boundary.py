@@ -103,7 +103,8 @@ def test_host_entry_validation(lib):
 def test_quant_entry_validation(lib):
     a, q, rs = 0x10000, 0x8000000, 0x20000000
     f = lib.hadacore_fwht_quant
-    assert f(a, q, rs, 4, 256, 0, 2, 1.0, None) == DTYPE          # unknown qtype
+    assert f(a, q, rs, 4, 256, 0, 3, 1.0, None) == DTYPE          # unknown qtype
+    assert f(a, a + 512, rs, 4, 256, 0, 2, 1.0, None) == OVERLAP   # int4 codes inside the input
     assert f(a, q, rs, 4, 256, 3, 0, 1.0, None) == DTYPE          # unknown dtype
     assert f(a, q, rs, 4, 100, 0, 0, 1.0, None) == INVALID_N
     assert f(a, q, rs, 4, 64, 0, 0, 1.0, None) == INVALID_N      # fused quantization: the paper's 2^7..2^15

@@ -30,7 +30,23 @@ pytestmark = pytest.mark.gpu
 NS = [1 << k for k in range(7, 16)]
 DTYPES = [torch.float16, torch.bfloat16]
 TOL = {torch.float16: 2e-3, torch.bfloat16: 1.6e-2}
-QMAX = {"e4m3": 448.0, "int8": 127.0}
+QMAX = {"e4m3": 448.0, "int8": 127.0, "int4": 7.0}
+QTYPES = ["e4m3", "int8", "int4"]
+
+
+def unpack_int4(q_u8: np.ndarray) -> np.ndarray:
+    """(m, n/2) bytes -> (m, n) int8 codes: element 2j = low nibble of byte j (two's complement)."""
+    lo = (q_u8 & 0x0F).astype(np.int16)
+    hi = (q_u8 >> 4).astype(np.int16)
+    out = np.empty((q_u8.shape[0], 2 * q_u8.shape[1]), dtype=np.int16)
+    out[:, 0::2], out[:, 1::2] = lo, hi
+    out = np.where(out >= 8, out - 16, out)
+    return out.astype(np.int8).view(np.uint8)
+
+
+def gpu_codes(q: torch.Tensor, qtype: str) -> np.ndarray:
+    c = q.view(torch.uint8).cpu().numpy()
+    return unpack_int4(c) if qtype == "int4" else c
 
 
 @pytest.fixture(scope="module")
@@ -51,7 +67,7 @@ E4M3_VALUES = None
 
 
 def code_values(codes_u8: np.ndarray, qtype: str) -> np.ndarray:
-    if qtype == "int8":
+    if qtype in ("int8", "int4"):
         return codes_u8.view(np.int8).astype(np.float64)
     table = np.array([oracle.e4m3_value(c) for c in range(256)])
     return table[codes_u8]
@@ -59,7 +75,7 @@ def code_values(codes_u8: np.ndarray, qtype: str) -> np.ndarray:
 
 def adjacent(v_gpu: np.ndarray, v_ref: np.ndarray, qtype: str) -> np.ndarray:
     """True where the two code values are equal or neighbours on the code grid."""
-    if qtype == "int8":
+    if qtype in ("int8", "int4"):
         return np.abs(v_gpu - v_ref) <= 1
     global E4M3_VALUES
     if E4M3_VALUES is None:
@@ -73,7 +89,7 @@ def ragged_m(n):
     return max(3, (1 << 19) // n) + 1
 
 
-@pytest.mark.parametrize("qtype", ["e4m3", "int8"])
+@pytest.mark.parametrize("qtype", QTYPES)
 @pytest.mark.parametrize("dist", ["D0", "D1"])
 @pytest.mark.parametrize("dtype", DTYPES, ids=["fp16", "bf16"])
 @pytest.mark.parametrize("n", NS)
@@ -82,7 +98,7 @@ def test_quant_parity(hc, n, dtype, dist, qtype):
     x = synthetic.generate(m, n, dtype, synthetic.seed_for(3, dtype), dist=dist).cuda()
     q, s = hc.hadacore_fwht_quant(x, qtype=qtype)
     torch.cuda.synchronize()
-    codes = q.view(torch.uint8).cpu().numpy()
+    codes = gpu_codes(q, qtype)
     s_gpu = s.cpu().double().numpy()
     y = oracle.fwht(x.cpu().double().numpy())
     codes_ref, s_ref = oracle.quantize_rows(y, qtype)
@@ -90,7 +106,7 @@ def test_quant_parity(hc, n, dtype, dist, qtype):
     assert np.all(np.abs(s_gpu - s_ref) <= tol * s_ref), "row scales"
     vg, vr = code_values(codes, qtype), code_values(codes_ref, qtype)
     eps = (tol * np.linalg.norm(y, axis=1) / math.sqrt(n) / s_ref)[:, None]   # RMS error, code units
-    spacing = np.ones_like(vr) if qtype == "int8" else np.maximum(np.abs(vr) * 2.0 ** -3, 2.0 ** -9)
+    spacing = np.ones_like(vr) if qtype != "e4m3" else np.maximum(np.abs(vr) * 2.0 ** -3, 2.0 ** -9)
     coarse = spacing >= 8 * eps
     assert np.all(adjacent(vg, vr, qtype) | ~coarse), "codes not adjacent to the oracle's"
     same = np.mean(codes == codes_ref)
@@ -98,14 +114,14 @@ def test_quant_parity(hc, n, dtype, dist, qtype):
     deq = vg * s_gpu[:, None]
     err = np.linalg.norm(deq - y, axis=1)
     ny = np.linalg.norm(y, axis=1)
-    if qtype == "int8":
+    if qtype != "e4m3":
         bound = s_gpu / 2 * math.sqrt(n) + tol * ny
     else:
         bound = (2.0 ** -4 + tol) * ny + 2.0 ** -10 * s_gpu * math.sqrt(n)
     assert np.all(err <= bound * 1.0001), f"dequantized error {np.max(err / bound):.3f} x bound"
 
 
-@pytest.mark.parametrize("qtype", ["e4m3", "int8"])
+@pytest.mark.parametrize("qtype", QTYPES)
 @pytest.mark.parametrize("dtype", DTYPES, ids=["fp16", "bf16"])
 @pytest.mark.parametrize("n", NS)
 def test_quant_identity_exact(hc, n, dtype, qtype):
@@ -124,8 +140,10 @@ def test_quant_identity_exact(hc, n, dtype, qtype):
     if qtype == "e4m3":
         expect = torch.where(par == 1, 0xFE, 0x7E).to(torch.uint8)
     else:
-        expect = torch.where(par == 1, -127, 127).to(torch.int8).view(torch.uint8)
-    assert torch.equal(q.view(torch.uint8), expect)
+        qm = int(QMAX[qtype])
+        expect = torch.where(par == 1, -qm, qm).to(torch.int8).view(torch.uint8)
+    got = torch.from_numpy(gpu_codes(q, qtype)).cuda()
+    assert torch.equal(got, expect)
     s_exp = (1.0 / math.sqrt(n)) / QMAX[qtype]
     assert torch.allclose(s.double(), torch.full_like(s.double(), s_exp), rtol=1e-6, atol=0)
 
@@ -136,7 +154,7 @@ def test_quant_special_rows(hc, n):
     sp, names = synthetic.special_rows(n, dtype)
     g = synthetic.generate(4, n, dtype, 5)
     x = torch.cat([g[:2], sp, g[2:]]).contiguous().cuda()
-    for qtype in ("e4m3", "int8"):
+    for qtype in QTYPES:
         q, s = hc.hadacore_fwht_quant(x, qtype=qtype)
         sc = s.cpu().double().numpy()
         y = oracle.fwht(x.cpu().double().numpy())
@@ -163,3 +181,17 @@ def test_quant_matches_fwht_then_quantize_on_gpu_values(hc):
         vg = code_values(q.view(torch.uint8).cpu().numpy(), "int8")
         vr = code_values(codes_ref, "int8")
         assert np.all(np.abs(vg - vr) <= 1)
+
+
+@pytest.mark.parametrize("n", [128, 256, 512, 4096, 32768])
+def test_int4_packing_and_views(hc, n):
+    """INT4 layout: (m, n/2) bytes, element 2j in the low nibble of byte j; leading dims
+    are rows; a ragged m; the codes unpack to the oracle's within one step."""
+    x = synthetic.generate(2 * 3 * 5, n, torch.float16, 17, dist="D1").reshape(2, 3, 5, n).cuda()
+    q, s = hc.hadacore_fwht_quant(x, qtype="int4")
+    assert q.shape == (2, 3, 5, n // 2) and q.dtype == torch.uint8 and s.shape == (2, 3, 5)
+    y = oracle.fwht(x.reshape(-1, n).cpu().double().numpy())
+    cr, sr = oracle.quantize_rows(y, "int4")
+    cg = gpu_codes(q.reshape(-1, n // 2), "int4")
+    assert np.all(np.abs(code_values(cg, "int4") - code_values(cr, "int4")) <= 1)
+    assert np.mean(cg == cr) >= 0.95
