@@ -54,7 +54,22 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
 }
 
+// HC_WAIT_HINT (ns): suspend-time hint of the try_wait loop -- a waiting warp sleeps
+// until the phase completes or the hint expires instead of re-issuing the probe
+// (tools/tune.py A/B; 0 = no hint)
+#ifndef HC_WAIT_HINT
+#define HC_WAIT_HINT 0
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+#if HC_WAIT_HINT > 0
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_addr(bar)),
+      "r"(parity), "n"(HC_WAIT_HINT)
+      : "memory");
+#else
   asm volatile(
       "{\n\t.reg .pred p;\n"
       "WAIT_%=:\n\t"
@@ -62,6 +77,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "@!p bra WAIT_%=;\n}" ::"r"(smem_addr(bar)),
       "r"(parity)
       : "memory");
+#endif
 }
 
 __device__ __forceinline__ uint64_t policy_evict_first() {

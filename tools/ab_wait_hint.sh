@@ -1,0 +1,14 @@
+set -e
+build() { nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-O2 -shared -I include $1 -o paper_2412_08832_b200/libhadacore.so paper_2412_08832_b200/csrc/hadacore.cu 2>/dev/null; }
+for rep in 1 2; do
+for v in "-DHC_WAIT_HINT=0" "-DHC_WAIT_HINT=100000" "-DHC_WAIT_HINT=2000"; do
+  build "$v"
+  for w in fwht quant-e4m3; do
+    timeout 300 python bench.py --workload $w --no-e2e --no-cpu-baseline --steps 20 > gpurun_out/ab.json 2>/dev/null
+    python -c "
+import json
+d=json.loads(open('gpurun_out/ab.json').read().strip().splitlines()[-1]); print('$rep', '$v', '$w', d['value'])
+"
+  done
+done
+done
