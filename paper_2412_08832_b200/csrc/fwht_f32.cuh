@@ -272,9 +272,10 @@ __global__ void __launch_bounds__((NT + 1) * 32, 1)
 // at half of the positions through distributed shared memory (mapa +
 // ld.shared::cluster; 32 KiB per CTA and tile) and computes both scale * (a + b) and
 // scale * (a - b) there; each CTA stores its two 32 KiB output pieces.  Two mbarriers
-// per stage order the exchange: ready[s] (the partner's half is final; one remote
-// release.cluster arrival per partner consumer thread) and consumed[s] (the partner
-// has read this CTA's half, so it may be overwritten).  Rows are scheduled
+// per stage order the exchange: ready[s] (the partner's half is final) and
+// consumed[s] (the partner has read this CTA's half, so it may be overwritten), each
+// armed by ONE remote mbarrier.arrive.release.cluster from the partner's group after
+// a group barrier.  Rows are scheduled
 // statically (row = cluster id + k * clusters), identically in both CTAs.  The
 // consumer warps form G groups that take alternate tiles, so one group's exchange
 // (two cross-SM handshakes and the DSMEM reads) overlaps the other's butterflies.
@@ -337,8 +338,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((NT + 1) * 32, 1)
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&done[s], NTG);
-      mbar_init(&ready[s], NTG * 32);
-      mbar_init(&consumed[s], NTG * 32);
+      mbar_init(&ready[s], 1);
+      mbar_init(&consumed[s], 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     fence_proxy_async_smem();
@@ -425,11 +426,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((NT + 1) * 32, 1)
       named_bar_sync(1 + grp, NTG * 32);
       f32_phase<NH, 10, 4, false, NTG>(tb, 1, tid, 1.f);  // the last in-CTA phase (scale applied below)
       static_assert(K == 14, "half rows of 2^14");
-      // this thread's half is final: tell the partner (release at cluster scope)
+      // this group's half is final (group barrier); one thread tells the partner with a
+      // release at cluster scope, cumulative over the group's writes it synchronized with
       const uint32_t tb_addr = smem_addr(tb);
-      mbar_arrive_remote(mapa_shared(smem_addr(&ready[s]), peer));
+      named_bar_sync(1 + grp, NTG * 32);
+      if (tid == 0) mbar_arrive_remote(mapa_shared(smem_addr(&ready[s]), peer));
       mbar_wait_cluster(&ready[s], ph);  // the partner's half is final
-      named_bar_sync(1 + grp, NTG * 32);  // ... and so is every thread's part of ours
       // positions [rank * NH/2, (rank+1) * NH/2) of both halves are this CTA's: it reads
       // the partner's half only there (32 KiB over DSMEM), and produces both outputs
       // y_lo = a + b and y_hi = a - b for them
@@ -445,7 +447,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((NT + 1) * 32, 1)
 #endif
 #pragma unroll
       for (int k2 = 0; k2 < PER_THREAD; ++k2) own[k2] = *reinterpret_cast<const float4*>(tb + 4 * (q0 + tid + k2 * NTG * 32));
-      mbar_arrive_remote(mapa_shared(smem_addr(&consumed[s]), peer));  // done reading the partner
+      named_bar_sync(1 + grp, NTG * 32);  // the whole group has read the partner's half
+      if (tid == 0) mbar_arrive_remote(mapa_shared(smem_addr(&consumed[s]), peer));
       mbar_wait_cluster(&consumed[s], ph);  // the partner is done reading ours
 #pragma unroll
       for (int k2 = 0; k2 < PER_THREAD; ++k2) {
