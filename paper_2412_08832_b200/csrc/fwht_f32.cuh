@@ -29,11 +29,15 @@ namespace hadacore {
 // contiguous floats per lane; later phases take W bits starting at LO.  Widths
 // are balanced so that no phase spends a full shared-memory round trip on a
 // single bit (k = 11: 6 + 5, k = 12: 6 + 6 instead of 5 + 5 + 1, 5 + 5 + 2).
+#ifndef HC_F32_WIDE
+#define HC_F32_WIDE 0  // 1: k = 13, 14 in two 7-bit phases (128 floats per lane): measured 6.7 -> 5.4 TB/s, off
+#endif
 template <int K>
 struct F32Plan {
-  static constexpr int B0 = (K == 11 || K == 12) ? 6 : (K < 5 ? K : 5);
-  static constexpr int NPH = K <= 5 ? 1 : (K <= 12 ? 2 : 3);
-  static constexpr int W1 = NPH == 1 ? 0 : (K == 13 ? 4 : (K - B0 < 5 ? K - B0 : (K == 12 ? 6 : 5)));
+  static constexpr bool WIDE = HC_F32_WIDE && K >= 13;
+  static constexpr int B0 = WIDE ? 7 : ((K == 11 || K == 12) ? 6 : (K < 5 ? K : 5));
+  static constexpr int NPH = K <= 5 ? 1 : ((K <= 12 || WIDE) ? 2 : 3);
+  static constexpr int W1 = NPH == 1 ? 0 : (WIDE ? K - 7 : (K == 13 ? 4 : (K - B0 < 5 ? K - B0 : (K == 12 ? 6 : 5))));
   static constexpr int LO2 = B0 + W1;
   static constexpr int W2 = NPH == 3 ? K - LO2 : 0;
 };
@@ -87,7 +91,7 @@ __global__ void __launch_bounds__((NT + 1) * 32, 1)
   using PL = F32Plan<K>;
   constexpr int NPH = PL::NPH;
   constexpr int K0 = PL::B0;                    // bits of phase 0
-  constexpr int V0 = K0 > 5 ? 64 : 32;          // floats per lane in phase 0
+  constexpr int V0 = K0 > 5 ? (1 << K0) : 32;   // floats per lane in phase 0
   constexpr int G0 = V0 / 4;                    // granules per lane in phase 0 (XOR on the low 3 bits)
   constexpr uint32_t M0 = K0 > 2 ? ((1u << (K0 - 2)) - 1u) & 7u : 0u;  // transformed XOR-ed granule bits
   static_assert(TILE_BYTES % (4 * V0) == 0 && (N < 32 || TILE_BYTES % (4 * N) == 0), "tile layout");
