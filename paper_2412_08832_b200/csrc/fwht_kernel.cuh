@@ -1300,6 +1300,9 @@ __global__ void __launch_bounds__((NT + 1) * 32, CTAS)
         q_r[k] = out_q + (i * g.m_inner + j) * (QT == QT_INT4 ? N / 2 : N) + lane * (QT == QT_INT4 ? 4 : 8);
         stf32_if(row_scale + (i * g.m_inner + j), sc, ok && wt == 0 && lane == 0);
       }
+#ifdef HC_QDIAG_NOCODE  // diagnostic (wrong output): no code pass
+      if (ok_r == 12345u)
+#endif
       for (int i0 = wt; i0 < ITEMS1; i0 += P * U1) {
         uint32_t z[U1][4];
 #pragma unroll
