@@ -449,6 +449,8 @@ def main():
                "h2d_bytes_per_step": int(2 * args.elems * len(pairs)),
                "d2h_bytes_per_step": int(2 * args.elems * len(pairs)),
                "api": "hadacore_fwht_host (C ABI, pinned host buffers, copies + kernel pipelined in the library)",
+               "ceiling": "PCIe-bound: pinned H2D + D2H running concurrently measured 93.9 GB/s on this pool "
+                          "(tools/pcie_probe.py, profiles/r01_quant_bound_diag.txt)",
                "steps": args.e2e_steps}
         del hin, hout, ws
 
