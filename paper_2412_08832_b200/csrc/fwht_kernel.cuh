@@ -1159,6 +1159,161 @@ __global__ void __launch_bounds__((NT + 1) * 32, CTAS)
   };
 
   int it = 0;
+  if constexpr (QT >= 0) {
+    // ---------------- fused quantization (NEXT-1): the two factors in the other order.
+    // H_n = H_{n/256} (x) H_256 and the factors commute (they act on different index
+    // bits), so the cross-chunk factor runs first, on the raw rows (phase A, the
+    // same ldmatrix/stmatrix exchange as phase 2 below, written back as a 16-bit
+    // intermediate), and the per-chunk H_256 last (phase B): its fp32 results stay in
+    // registers, in natural order (lane l holds elements 8l..8l+7 of its chunk), until
+    // the team has the row maximum; the codes are then computed and stored straight
+    // from registers (coalesced STG.64 / STG.32) -- no 16-bit image, no second pass over
+    // shared memory, and the stage is released to the producer right after phase B.
+    constexpr int IW = ITEMS1 / P;  // phase-B chunks per warp per tile
+    static_assert(ITEMS1 % P == 0, "phase-B split");
+    const float q_qs = copysignf(qmax_of<QT>(), s_res);  // code multiplier numerator (sign folded)
+    const float q_ss = fabsf(s_res) / qmax_of<QT>();     // row scale per unit of max |d|
+    for (;; ++it) {
+      const int s = it % STAGES;
+      mbar_wait(&full[s], (it / STAGES) & 1);
+      const int64_t tile = ctl->stage_tile[s];
+      if (tile < 0) break;
+      uint8_t* const tb = smem + s * TILE_BYTES;
+
+      // ---- phase A: H_{n/256} across chunks of the raw rows (residual factor P:146)
+      for (int i0 = wt; i0 < ITEMS2; i0 += P * U2) {
+        uint32_t x[U2][1 << PL::nx][4];
+        uint32_t addr[U2][1 << PL::nx];
+#pragma unroll
+        for (int u = 0; u < U2; ++u) {
+          const int item = i0 + u * P, r = team + NTEAMS * (item / NLOOP), lp = item % NLOOP;
+          const uint32_t gg = g_l | (uint32_t(lp) << LOOP_SHIFT);
+#pragma unroll
+          for (int xi = 0; xi < (1 << PL::nx); ++xi) {
+            addr[u][xi] = sm_base + s * TILE_BYTES + r * ROW_BYTES + gofs<C>(c_l | (uint32_t(xi) << 5), gg);
+            ldsm_x4_t(addr[u][xi], x[u][xi]);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < U2; ++u) {
+          float dd[1 << PL::nx][8];
+#pragma unroll
+          for (int xi = 0; xi < (1 << PL::nx); ++xi) {
+            if constexpr (PL::two_stage) {
+              uint32_t y[4];
+              stage_ca<DT>(Pa, x[u][xi][0], x[u][xi][2], x[u][xi][1], x[u][xi][3], y);
+              stage_ca_f32<DT>(Pb, y[0], y[2], y[1], y[3], dd[xi]);
+            } else {
+              stage_da_f32<DT>(x[u][xi], Bc0, Bc1, dd[xi]);
+            }
+          }
+#pragma unroll
+          for (int b = 0; b < PL::nx; ++b)
+#pragma unroll
+            for (int xi = 0; xi < (1 << PL::nx); ++xi)
+              if (!((xi >> b) & 1)) {
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                  const float p0 = dd[xi][e], p1 = dd[xi | (1 << b)][e];
+                  dd[xi][e] = p0 + p1;
+                  dd[xi | (1 << b)][e] = p0 - p1;
+                }
+              }
+#pragma unroll
+          for (int xi = 0; xi < (1 << PL::nx); ++xi) {
+            uint32_t z[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) z[q] = pack2<DT>(dd[xi][2 * q], dd[xi][2 * q + 1]);  // exact 2^-k scaling is in the constants
+            stsm_x4_t(addr[u][xi], z);
+          }
+        }
+      }
+      team_sync();  // P:126 "Sync across the threadblock"
+
+      // ---- phase B: H_256 per chunk, fp32 results kept in registers
+      float d[IW][8];
+      float am[RPT];
+#pragma unroll
+      for (int k = 0; k < RPT; ++k) am[k] = 0.f;
+#pragma unroll
+      for (int k = 0; k < IW; ++k) {
+        const int item = wt + k * P, rl = item / C, r = team + NTEAMS * rl, c = item % C;
+        uint32_t x[4], y[4];
+        lds128(tb + r * ROW_BYTES + gofs<C>(uint32_t(c), uint32_t(lane)), x[0], x[1], x[2], x[3]);
+        stage_ca<DT>(A256, x[0], x[2], x[1], x[3], y);
+        stage_ca_f32<DT>(A256, y[0], y[2], y[1], y[3], d[k]);
+        float a = 0.f;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) a = absmax_nan(a, d[k][e]);
+#pragma unroll
+        for (int kk = 0; kk < RPT; ++kk)
+          if (kk == rl) am[kk] = absmax_nan(am[kk], a);
+      }
+      // the stage's shared memory is no longer read: release it to the producer now
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&done[s]);
+
+      // ---- row max over the team (max |d|; |y| = |d| |s_res|), then codes from registers
+#pragma unroll
+      for (int k = 0; k < RPT; ++k) {
+        const float a = warp_absmax(am[k]);
+        if (lane == 0) red[(team * RPT + k) * P + wt] = a;
+      }
+      team_sync();
+      float mul_r[RPT];
+      uint32_t fast_r = 0, ok_r = 0;
+      uint8_t* q_r[RPT];
+      const TileRows tr(g, tile);
+#pragma unroll
+      for (int k = 0; k < RPT; ++k) {
+        float a = 0.f;
+        for (int w = 0; w < P; ++w) a = absmax_nan(a, red[(team * RPT + k) * P + w]);
+        float sc;
+        if (quant_fast_range(a, 0x1p100f)) {
+          sc = a * q_ss;
+          mul_r[k] = q_qs * rcp_ftz(a);
+          fast_r |= 1u << k;
+        } else {
+          float inv;
+          row_scale_of<QT>(a * fabsf(s_res), sc, inv);
+          mul_r[k] = s_res * inv;
+        }
+        int64_t i = 0, j = 0;
+        const bool ok = tr.at(g, team + NTEAMS * k, i, j);
+        ok_r |= uint32_t(ok) << k;
+        q_r[k] = out_q + (i * g.m_inner + j) * (QT == QT_INT4 ? N / 2 : N) + lane * (QT == QT_INT4 ? 4 : 8);
+        stf32_if(row_scale + (i * g.m_inner + j), sc, ok && wt == 0 && lane == 0);
+      }
+#pragma unroll
+      for (int k = 0; k < IW; ++k) {
+        const int item = wt + k * P, rl = item / C, c = item % C;
+        float mul = 0.f;
+        uint8_t* qp = nullptr;
+#pragma unroll
+        for (int kk = 0; kk < RPT; ++kk)
+          if (kk == rl) {
+            mul = mul_r[kk];
+            qp = q_r[kk];
+          }
+        const float* v = d[k];
+        uint32_t c0, c1;
+        if ((fast_r >> rl) & 1u) {
+          c0 = quant4_fast<QT>(v[0], v[1], v[2], v[3], mul);
+          c1 = quant4_fast<QT>(v[4], v[5], v[6], v[7], mul);
+        } else {
+          c0 = quant4<QT>(v[0] * mul, v[1] * mul, v[2] * mul, v[3] * mul);
+          c1 = quant4<QT>(v[4] * mul, v[5] * mul, v[6] * mul, v[7] * mul);
+        }
+        if constexpr (QT == QT_INT4) {
+          stg32_if(qp + c * 128, c0 | (c1 << 16), (ok_r >> rl) & 1u);
+        } else {
+          stg64_if(qp + c * 256, c0, c1, (ok_r >> rl) & 1u);
+        }
+      }
+      // (red[] is rewritten only after the next tile's phase-A barrier: no race)
+    }
+  } else
   for (;; ++it) {
     const int s = it % STAGES;
     mbar_wait(&full[s], (it / STAGES) & 1);
@@ -1193,9 +1348,6 @@ __global__ void __launch_bounds__((NT + 1) * 32, CTAS)
     if (warp == 0 && lane == 0) trace(it, 5);
 
     // ---- phase 2: H_{n/256} across chunks (residual 2^a factor)
-    float amax_r[RPT];  // fused quantization: running max |y| of each of the team's rows
-#pragma unroll
-    for (int k = 0; k < RPT; ++k) amax_r[k] = 0.f;
     for (int i0 = wt; i0 < ITEMS2; i0 += P * U2) {
       uint32_t x[U2][1 << PL::nx][4];
       uint32_t addr[U2][1 << PL::nx];
@@ -1242,17 +1394,6 @@ __global__ void __launch_bounds__((NT + 1) * 32, CTAS)
                 d[xi | (1 << b)][e] = p0 - p1;
               }
             }
-        if constexpr (QT >= 0) {
-          const int rl = (i0 + u * P) / NLOOP;
-          float a = 0.f;
-#pragma unroll
-          for (int xi = 0; xi < (1 << PL::nx); ++xi)
-#pragma unroll
-            for (int e = 0; e < 8; ++e) a = absmax_nan(a, d[xi][e]);
-#pragma unroll
-          for (int k = 0; k < RPT; ++k)
-            if (k == rl) amax_r[k] = absmax_nan(amax_r[k], a);
-        }
 #pragma unroll
         for (int xi = 0; xi < (1 << PL::nx); ++xi) {
           uint32_t z[4];
@@ -1267,79 +1408,7 @@ __global__ void __launch_bounds__((NT + 1) * 32, CTAS)
         }
       }
     }
-    if constexpr (QT >= 0) {
-      // ---- fused quantization (NEXT-1): row max over the team, then codes + scales
-#pragma unroll
-      for (int k = 0; k < RPT; ++k) {
-        const float a = warp_absmax(amax_r[k]) * fabsf(s_res);
-        if (lane == 0) red[(team * RPT + k) * P + wt] = a;
-      }
-      team_sync();
-      float inv_r[RPT];
-      uint32_t fast_r = 0;  // bit k: row k takes the fast path
-      uint8_t* q_r[RPT];    // code row pointers (valid rows only)
-      uint32_t ok_r = 0;
-      const TileRows tr(g, tile);
-      // image-domain fast range: the fp16 image holds Inf where y overflowed fp16
-      constexpr float kHi = DT == DT_F16 ? 65504.f : 0x1p100f;
-#pragma unroll
-      for (int k = 0; k < RPT; ++k) {
-        float a = 0.f;
-        for (int w = 0; w < P; ++w) a = absmax_nan(a, red[(team * RPT + k) * P + w]);
-        float sc;
-        if (quant_fast_range(a, kHi)) {
-          sc = a * (1.f / qmax_of<QT>());
-          inv_r[k] = qmax_of<QT>() * rcp_ftz(a);
-          fast_r |= 1u << k;
-        } else {
-          row_scale_of<QT>(a, sc, inv_r[k]);
-        }
-        int64_t i = 0, j = 0;
-        const bool ok = tr.at(g, team + NTEAMS * k, i, j);
-        ok_r |= uint32_t(ok) << k;
-        q_r[k] = out_q + (i * g.m_inner + j) * (QT == QT_INT4 ? N / 2 : N) + lane * (QT == QT_INT4 ? 4 : 8);
-        stf32_if(row_scale + (i * g.m_inner + j), sc, ok && wt == 0 && lane == 0);
-      }
-#ifdef HC_QDIAG_NOCODE  // diagnostic (wrong output): no code pass
-      if (ok_r == 12345u)
-#endif
-      for (int i0 = wt; i0 < ITEMS1; i0 += P * U1) {
-        uint32_t z[U1][4];
-#pragma unroll
-        for (int u = 0; u < U1; ++u) {
-          const int item = i0 + u * P, r = team + NTEAMS * (item / C), c = item % C;
-          lds128(tb + r * ROW_BYTES + gofs<C>(uint32_t(c), uint32_t(lane)), z[u][0], z[u][1], z[u][2], z[u][3]);
-        }
-#pragma unroll
-        for (int u = 0; u < U1; ++u) {
-          const int item = i0 + u * P, rl = item / C, c = item % C;
-          float inv = 0.f;
-          uint8_t* qp = nullptr;
-#pragma unroll
-          for (int k = 0; k < RPT; ++k)
-            if (k == rl) {
-              inv = inv_r[k];
-              qp = q_r[k];
-            }
-          float v[8];
-          unpack8<DT>(z[u], v);
-          uint32_t c0, c1;
-          if ((fast_r >> rl) & 1u) {
-            c0 = quant4_fast<QT>(v[0], v[1], v[2], v[3], inv);
-            c1 = quant4_fast<QT>(v[4], v[5], v[6], v[7], inv);
-          } else {
-            c0 = quant4<QT>(v[0] * inv, v[1] * inv, v[2] * inv, v[3] * inv);
-            c1 = quant4<QT>(v[4] * inv, v[5] * inv, v[6] * inv, v[7] * inv);
-          }
-          if constexpr (QT == QT_INT4) {
-            stg32_if(qp + c * 128, c0 | (c1 << 16), (ok_r >> rl) & 1u);
-          } else {
-            stg64_if(qp + c * 256, c0, c1, (ok_r >> rl) & 1u);
-          }
-        }
-      }
-      // (red[] is rewritten only after the next tile's phase-1 barrier: no race)
-    } else if constexpr (STG_OUT) {
+    if constexpr (STG_OUT) {
       team_sync();
       const TileRows tr(g, tile);
       for (int i0 = wt; i0 < ITEMS1; i0 += P * U1) {

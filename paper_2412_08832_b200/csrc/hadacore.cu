@@ -62,8 +62,24 @@ template <> struct Tuned<32768> { static constexpr int nt = 16, tkb = 64, st = 3
 // a tile's critical path longer, so more independent pipelines per SM win: 3 CTAs of
 // 8 consumer warps with 32 KiB tiles in a 2-stage ring (paired sweeps,
 // profiles/r01_quant_sweep*.txt: +20-60 % over the transform's table at n = 2^10..2^14).
-template <int N> struct TunedQ      { static constexpr int nt = 8, tkb = 32, st = 2, u = 1, ctas = 3; };
-template <> struct TunedQ<32768>    { static constexpr int nt = 16, tkb = 64, st = 3, u = 1, ctas = 1; };
+// n >= 512 keeps each warp's phase-B results (IW = tile / (nt * 512 B) chunks of 8 fp32
+// per lane) in registers across the row-max barrier, so tiles are sized to IW = 4..8
+// and the CTA count to the register file (paired sweeps, profiles/r01_quant_tune_v3.txt).  HC_QTUNE = "nt,tkb,st,ctas"
+// overrides n = 512..8192 (A/B builds).
+template <int N> struct TunedQ0     { static constexpr int nt = 8, tkb = 16, st = 3, u = 1, ctas = 3; };
+template <> struct TunedQ0<128>     { static constexpr int nt = 8, tkb = 32, st = 2, u = 1, ctas = 3; };
+template <> struct TunedQ0<256>     { static constexpr int nt = 8, tkb = 32, st = 2, u = 1, ctas = 3; };
+template <> struct TunedQ0<8192>    { static constexpr int nt = 8, tkb = 32, st = 3, u = 1, ctas = 2; };
+template <> struct TunedQ0<16384>   { static constexpr int nt = 8, tkb = 32, st = 3, u = 1, ctas = 2; };
+template <> struct TunedQ0<32768>   { static constexpr int nt = 16, tkb = 64, st = 3, u = 1, ctas = 1; };
+#ifdef HC_QTUNE  // A/B builds: HC_QTUNE_N = the n to override (0: every n in 512..8192)
+struct QMacro { static constexpr int nt = HC_QNT, tkb = HC_QTKB, st = HC_QST, u = 1, ctas = HC_QCTAS; };
+template <int N>
+struct TunedQ : std::conditional_t<(HC_QTUNE_N == N || (HC_QTUNE_N == 0 && N >= 512 && N <= 8192)), QMacro,
+                                   TunedQ0<N>> {};
+#else
+template <int N> struct TunedQ : TunedQ0<N> {};
+#endif
 
 // Rows shorter than 128 (NEXT-2, fwht_small_kernel): 8 consumer warps, 32 KiB tiles,
 // 4-stage ring; U items per lane in flight (an item is 8 elements for n <= 8, a row
