@@ -498,10 +498,22 @@ __device__ __forceinline__ uint32_t quant4_fast(float a, float b, float c, float
     asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(hi) : "f"(d), "f"(c));
     return uint32_t(lo) | (uint32_t(hi) << 16);
   } else {
+    if constexpr (QT == QT_INT4) {
+      // |v m| <= 7 (1 + 2^-8)(1 + 2^-22) < 7.5.  Rounding with the addend 1.5 * 2^23 + 8
+      // leaves r + 8 in [1, 15] in the low mantissa bits (above them only the 2^22
+      // bit): an offset-binary nibble with clean neighbours, so a + 16 b + 256 c +
+      // 4096 d (integer multiply-adds) assembles four of them, and XOR 8 per nibble
+      // turns offset binary into two's complement.  Bits above 15 are not cleared
+      // (callers keep the low 16 bits).
+      fma2(a, b, m, 12582920.f);  // 1.5 * 2^23 + 8 (even: ties stay ties-to-even)
+      fma2(c, d, m, 12582920.f);
+      uint32_t t = __float_as_uint(a) + 16u * __float_as_uint(b);
+      t += 256u * __float_as_uint(c);
+      t += 4096u * __float_as_uint(d);
+      return t ^ 0x8888u;
+    }
     fma2(a, b, m, 12582912.f);  // 1.5 * 2^23
     fma2(c, d, m, 12582912.f);
-    if constexpr (QT == QT_INT4)  // |v m| <= 7 (1 + 2^-8)(1 + 2^-22) < 7.5: the low nibble is the code
-      return nibbles4(__float_as_uint(a), __float_as_uint(b), __float_as_uint(c), __float_as_uint(d));
     return __byte_perm(__byte_perm(__float_as_uint(a), __float_as_uint(b), 0x0040),
                        __byte_perm(__float_as_uint(c), __float_as_uint(d), 0x0040), 0x5410);
   }
@@ -905,7 +917,7 @@ __global__ void __launch_bounds__((NT + 1) * 32, CTAS)
             const bool ok = FLAT ? r < rows_left : tr.at(g, r, i, j);
             const int64_t row = FLAT ? tr.i0 + r : i * g.m_inner + j;
             if constexpr (QT == QT_INT4) {
-              stg32_if(out_q + row * (N / 2) + lane * 4, c0 | (c1 << 16), ok);
+              stg32_if(out_q + row * (N / 2) + lane * 4, __byte_perm(c0, c1, 0x5410), ok);
             } else {
               stg64_if(out_q + row * N + lane * 8, c0, c1, ok);
             }
@@ -1306,7 +1318,7 @@ __global__ void __launch_bounds__((NT + 1) * 32, CTAS)
           c1 = quant4<QT>(v[4] * mul, v[5] * mul, v[6] * mul, v[7] * mul);
         }
         if constexpr (QT == QT_INT4) {
-          stg32_if(qp + c * 128, c0 | (c1 << 16), (ok_r >> rl) & 1u);
+          stg32_if(qp + c * 128, __byte_perm(c0, c1, 0x5410), (ok_r >> rl) & 1u);
         } else {
           stg64_if(qp + c * 256, c0, c1, (ok_r >> rl) & 1u);
         }
