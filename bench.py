@@ -390,6 +390,21 @@ def main():
     # per-launch breakdown: a separate pass after the timed region
     _, per = timed_region(max(3, min(args.steps, 10)), True)
 
+    # same-run D2D copy of the same byte count ("% of achievable copy"): cudaMemcpyAsync
+    # of one input buffer into the output buffer, event-timed on the same stream
+    src_b = next(iter(xin.values())).view(torch.uint8)
+    dst_b = obuf.view(torch.uint8)[: src_b.numel()]
+    for _ in range(3):
+        dst_b.copy_(src_b)
+    c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    c0.record(stream)
+    for _ in range(10):
+        dst_b.copy_(src_b)
+    c1.record(stream)
+    torch.cuda.synchronize()
+    copy_gbps = 2.0 * src_b.numel() * 10 / (c0.elapsed_time(c1) * 1e-3) / 1e9
+
     t_max = max_over_ranks(total_ms, dist, torch)
     # algorithmic bytes: 2 B read + 2 B written per element (fwht); 2 + 1 B plus one fp32
     # scale per row for the fused quantization (per-n average over the sweep)
@@ -425,6 +440,8 @@ def main():
                 "traffic_source": (traffic or {}).get("source"),
                 "duration_source": "timed region / launches (CUDA events on the launching stream, max over ranks)",
                 "sum_of_launch_events_GBps": round(bytes_per_launch * len(per) / (sum(per) * 1e-3) / 1e9, 1),
+                "same_run_d2d_copy_GBps": round(copy_gbps, 1),
+                "frac_of_same_run_copy": round(achieved / copy_gbps, 4),
                 "note": "back-to-back PDL launches overlap one grid's tail with the next grid's ramp; the peak is a "
                         "single timed 2 GiB copy, which includes its own ramp and tail, so frac can exceed 1"}
 
@@ -496,6 +513,8 @@ def main():
                                          "fp16+bf16 (fp32 last-stage accumulate)"),
             "data": "synthetic (counter-based N(0,1), synthetic/)", "config": config_block(args, world),
             "pct_of_8TBps": round(100.0 * value / world / NOMINAL_HBM_GBS, 2),
+            # north_star: "reported ... both as GB/s and elements/s" (whole job, all ranks)
+            "elements_per_s": float(f"{(C5_ELEMS * args.steps if c5 else sum(elems_of[p] for p in pairs) * args.steps * world) / (t_max * 1e-3):.4g}"),
             "per_n_GBps": per_n, "roofline": roofline, "cpu_baseline": cpu_baseline, "e2e": e2e,
             "gpu_launches": int(args.steps * sum(hc.launches_per_call(elems_of[(dt, n)] // n, n, dt) for dt, n in pairs)),
             "clocks": clocks, "remeasured_for_clocks": remeasured,
