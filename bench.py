@@ -50,11 +50,12 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
-    ap.add_argument("--workload", choices=["fwht", "quant-e4m3", "quant-int8", "quant-int4", "qk-rotate", "small", "f32", "c5"], default="fwht",
+    ap.add_argument("--workload", choices=["fwht", "quant-e4m3", "quant-int8", "quant-int4", "qk-rotate", "small", "f32", "c5", "c1"], default="fwht",
                     help="fwht = the metric's C3 sweep (default); quant-* = the fused FWHT + per-row "
                          "quantization row (NEXT-1) on the same inputs; small = n=2^1..2^6 (NEXT-2); "
                          "f32 = the fp32 path over n=2^1..2^15 (NEXT-2); c5 = BASELINE config C5: bf16 "
-                         "n=2^15, 2^33 elements row-sharded over the ranks (strong scaling)")
+                         "n=2^15, 2^33 elements row-sharded over the ranks (strong scaling); c1 = BASELINE config "
+                         "C1 (fp16 m=1024 n=256): microseconds per launch, warm (CUDA graph) and cold (L2 flushed)")
     return ap.parse_args()
 
 
@@ -258,6 +259,67 @@ def config_block(args, world):
             "parallelism": f"row-sharded x{world}, no collective on the hot path" if world > 1 else "single GPU"}
 
 
+def run_c1(args, rank, world, dist):
+    """BASELINE configs[0] (C1: fp16, m = 1024, n = 256, 1 MiB of traffic): a launch-latency-bound,
+    L2-resident problem, reported in microseconds per launch -- warm (100 launches captured in one CUDA
+    graph, replayed) and cold (L2 flushed by a 2 x 126 MB write before each timed launch)."""
+    import torch
+    import paper_2412_08832_b200 as hc
+    import synthetic
+    hc._load()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    x = synthetic.generate(1024, 256, torch.float16, synthetic.seed_for(0, torch.float16)).to(dev)
+    y = torch.empty_like(x)
+    stream = torch.cuda.Stream(dev)
+    R = 100
+    with torch.cuda.stream(stream):
+        for _ in range(3):
+            hc.hadacore_fwht(x, out=y, stream=stream)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            for _ in range(R):
+                hc.hadacore_fwht(x, out=y, stream=stream)
+        for _ in range(args.warmup):
+            g.replay()
+        barrier(dist, torch)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            g.replay()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        warm_us = max_over_ranks(e0.elapsed_time(e1) * 1e3 / (args.steps * R), dist, torch)
+        flush = torch.empty(2 * 126 * 1000 * 1000, dtype=torch.uint8, device=dev)
+        cold = []
+        for _ in range(max(3, args.steps)):
+            flush.fill_(1)
+            c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            c0.record(stream)
+            hc.hadacore_fwht(x, out=y, stream=stream)
+            c1.record(stream)
+            torch.cuda.synchronize()
+            cold.append(c0.elapsed_time(c1) * 1e3)
+    cold_us = sorted(cold)[len(cold) // 2]
+    bytes_ = 4.0 * x.numel()
+    if rank != 0:
+        return None
+    return {"metric": "C1 latency: microseconds per hadacore_fwht launch, fp16 m=1024 n=256 (warm, CUDA graph)",
+            "value": round(warm_us, 3), "unit": "us", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(warm_us * R / 1e3, 4), "higher_is_better": False, "scaling": "weak",
+            "vs_baseline": None, "dtype": "fp16 (fp32 last-stage accumulate)", "data": "synthetic (synthetic/)",
+            "config": {"workload": "C1: fp16 m=1024 n=256 (1 MiB traffic), 100 launches per CUDA graph replay; "
+                                   "cold = one launch after a 252 MB L2-flushing write", "l2": "warm: L2-resident by "
+                                   "design (C1 is launch-bound); cold: flushed", "parallelism": "single GPU"},
+            "cold_us": round(cold_us, 3), "warm_GBps": round(bytes_ / (warm_us * 1e-6) / 1e9, 1),
+            "roofline": {"bound": "hbm", "achieved": round(bytes_ / (cold_us * 1e-6) / 1e9, 1),
+                         "peak": measured_hbm_peak()[0], "unit": "GB/s",
+                         "frac": round(bytes_ / (cold_us * 1e-6) / 1e9 / measured_hbm_peak()[0], 4),
+                         "traffic": None, "note": "1 MiB per launch: launch-latency-bound, not bandwidth-bound; "
+                                                  "achieved from the cold launch time"},
+            "gpu_launches": int(args.steps * R), "cpu_baseline": None, "e2e": None}
+
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -270,6 +332,13 @@ def main():
         return
     import torch
     rank, world, local, dist = dist_setup(args)
+    if args.workload == "c1":
+        line = run_c1(args, rank, world, dist)
+        if line is not None:
+            print(json.dumps(line), flush=True)
+        if dist is not None:
+            dist.destroy_process_group()
+        return
 
     import paper_2412_08832_b200 as hc
     import synthetic
