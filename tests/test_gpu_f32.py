@@ -102,3 +102,23 @@ def test_f32_full_size_sampled(hc, n):
     g = torch.Generator().manual_seed(n)
     rows = sorted(set([0, m - 1] + torch.randint(0, m, (40,), generator=g).tolist()))
     assert rel_l2_rows(widen(y[rows]), oracle.fwht(widen(x[rows]))).max() <= TOL
+
+
+def test_f32_pair_kernel_repeatability_stress(hc):
+    """The 2-CTA cluster kernel (fp32 n = 2^15) synchronizes the DSMEM exchange with remote
+    mbarriers only (which racecheck cannot model): 40 back-to-back launches over more rows
+    than co-resident clusters must all give the same bits, in place and out of place."""
+    n, m = 32768, 300
+    x = synthetic.generate(m, n, torch.float32, 13, device="cuda")
+    ref = hc.hadacore_fwht(x)
+    outs = [torch.empty_like(x) for _ in range(4)]
+    for k in range(40):
+        hc.hadacore_fwht(x, out=outs[k % 4])
+        if k % 4 == 3:
+            torch.cuda.synchronize()
+            for o in outs:
+                assert torch.equal(o, ref), k
+    xi = x.clone()
+    hc.hadacore_fwht(xi, out=xi)
+    assert torch.equal(xi, ref)
+    assert rel_l2_rows(widen(ref[:8]), oracle.fwht(widen(x[:8]))).max() <= TOL
