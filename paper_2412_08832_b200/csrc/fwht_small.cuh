@@ -29,9 +29,15 @@
 namespace hadacore {
 
 __device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
+#if HC_STORE_HINT  // evict-first in L2, as the TMA tensor stores (fwht_kernel.cuh)
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(dst),
+               "r"(smem_addr(src)), "r"(bytes), "l"(policy_evict_first())
+               : "memory");
+#else
   asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_addr(src)),
                "r"(bytes)
                : "memory");
+#endif
 }
 
 template <int DT>
