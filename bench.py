@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--ns", default=None, help="comma-separated n list overriding the workload's sweep "
+                                               "(e.g. --workload quant-e4m3 --ns 2,4,8,16,32,64)")
     ap.add_argument("--workload", choices=["fwht", "quant-e4m3", "quant-int8", "quant-int4", "qk-rotate", "small", "f32", "c5", "c1"], default="fwht",
                     help="fwht = the metric's C3 sweep (default); quant-* = the fused FWHT + per-row "
                          "quantization row (NEXT-1) on the same inputs; small = n=2^1..2^6 (NEXT-2); "
@@ -243,6 +245,9 @@ def config_block(args, world):
         ns = [32768]
         wl = ("C5: bf16 n=2^15, 2^33 elements (262144 rows, 16 GiB in + 16 GiB out) row-sharded across the "
               "ranks, no collective on the hot path, out-of-place, normalized")
+    if getattr(args, "ns", None):
+        ns = [int(v) for v in args.ns.split(",")]
+        wl = f"{getattr(args, 'workload', 'fwht')} over n in {ns} (--ns), 2^28 elements per (n, dtype) per GPU"
     if getattr(args, "workload", "fwht") == "small":
         wl = ("NEXT-2 small sizes: n=2^1..2^6 x {fp16, bf16}, 2^28 elements per (n, dtype) per GPU, "
               "out-of-place, normalized (scale=1/sqrt(n))")
@@ -365,6 +370,8 @@ def main():
     obuf = torch.empty(args.elems, dtype=torch.float16, device=dev)
     stream = torch.cuda.current_stream(dev)
     ns = SMALL_NS if args.workload == "small" else NS
+    if args.ns:
+        ns = [int(v) for v in args.ns.split(",")]
     f32 = args.workload == "f32"
     if f32:
         ns = SMALL_NS + NS
@@ -379,7 +386,7 @@ def main():
     qtype = args.workload.split("-")[1] if quant else None
     if quant:
         qbuf = torch.empty(args.elems // (2 if qtype == "int4" else 1), dtype=hc.QTYPES[qtype][1], device=dev)
-        sbuf = torch.empty(args.elems // 128, dtype=torch.float32, device=dev)
+        sbuf = torch.empty(args.elems // min(ns), dtype=torch.float32, device=dev)
     qb = 0.5 if qtype == "int4" else 1.0  # code bytes per element
 
     rotate = args.workload == "qk-rotate"
@@ -479,7 +486,7 @@ def main():
     # scale per row for the fused quantization (per-n average over the sweep)
     esize = 4 if f32 else 2
     bytes_per_launch = 2.0 * esize * args.elems if not quant else \
-        sum((2.0 + qb) * args.elems + 4.0 * (args.elems // n) for n in NS) / len(NS)
+        sum((2.0 + qb) * args.elems + 4.0 * (args.elems // n) for n in ns) / len(ns)
     if rotate:
         bytes_per_launch = sum(4.0 * e for e in elems_of.values()) / len(pairs)
     total_bytes = bytes_per_launch * len(pairs) * args.steps * world
@@ -569,6 +576,8 @@ def main():
         if c5:
             metric = ("C5: FWHT HBM GB/s, bf16 n=2^15, 2^33 elements row-sharded across the GPUs "
                       "(whole-job bytes / max-over-ranks time; strong scaling)")
+        if args.ns:
+            metric = metric.replace("n=2^7..2^15", f"n in {{{args.ns}}}")
         if args.workload == "small":
             metric = "FWHT HBM GB/s vs n=2^1..2^6 (bf16/fp16), rows shorter than the paper's 2^7 (NEXT-2)"
         if rotate:

@@ -12,7 +12,7 @@
  * `scale` is the WHOLE multiplier on the +-1 matrix: pass 1/sqrt(n) for the
  * normalized (orthonormal) transform of P:41 ("+-1/sqrt(d) ... when normalized").
  * n is a power of two in [2^7, 2^15] (the paper's range, P:97, P:128 [Sec. 3.2]) or,
- * for hadacore_fwht / hadacore_fwht_host only, in [2, 2^6] (
+ * except for hadacore_fwht_strided, in [2, 2^6] (
  * SPEC S:49's domain 2 <= d; fp32 register butterflies, DESIGN.md "Rows shorter
  * than 128").
  *
@@ -72,7 +72,7 @@ typedef enum {
 typedef enum {
   HADACORE_OK = 0,
   HADACORE_ERR_INVALID_N = 1,   /* n is not a power of two in [2, 32768] ([128, 32768] for the
-                                   strided and quantizing entry points) */
+                                   strided entry point) */
   HADACORE_ERR_INVALID_M = 2,   /* m < 0, or m * n * element size overflows int64 */
   HADACORE_ERR_NULL = 3,        /* in or out is NULL while m > 0 */
   HADACORE_ERR_MISALIGNED = 4,  /* in or out is not 16-byte aligned */
@@ -138,8 +138,8 @@ hadacore_status_t hadacore_fwht_strided(const void* in, void* out, int64_t m_out
  *     out_q[i, j]  = round(y_j / row_scale[i])   (E4M3 saturating / INT8, INT4 clamped)
  * so out_q[i, j] * row_scale[i] ~= y_j.  A row containing Inf/NaN gets a non-finite
  * row_scale.  out_q: m x n bytes (m x n/2 for INT4), row-major, 16-byte aligned; row_scale: m floats
- * (fp32).  Neither may overlap `in`.  n = 2^7..2^15.  HBM traffic: 2 B read + 1 B
- * written per element.
+ * (fp32).  Neither may overlap `in`.  n = 2..2^15.  HBM traffic: 2 B read + 1 B
+ * (INT4: 0.5 B) written per element.
  * Same validation, stream and error behaviour as hadacore_fwht; qtype outside the
  * enum, or dtype HADACORE_F32, returns HADACORE_ERR_DTYPE.
  */

@@ -11,8 +11,8 @@ library is missing or no GPU is present, calls raise.
 
 ``x`` is a CUDA tensor of dtype float16 or bfloat16 whose last dimension n is a
 power of two in [2, 32768] (the paper's 2^7..2^15, plus n = 2..64: SURVEY.md 8(f)
-NEXT-2); all leading dimensions are rows (m = numel / n).  The strided and
-quantizing entry points take n = 2^7..2^15.
+NEXT-2); all leading dimensions are rows (m = numel / n).  The strided entry
+point takes n = 2^7..2^15.
 """
 from __future__ import annotations
 

@@ -54,10 +54,13 @@ __device__ __forceinline__ void unpack2(uint32_t w, float& lo, float& hi) {
 
 // Rows of N = 2..64 elements; TILE_BYTES per ring stage, NT consumer warps, U items
 // per lane in flight.
-template <int N, int DT, int TILE_BYTES, int STAGES, int NT, int U>
+// QT >= 0: fused per-row quantization (NEXT-1 for n < 128): a lane holds whole rows, so
+// the row max is in-lane; codes go straight from registers to out_q, scales to row_scale.
+template <int N, int DT, int TILE_BYTES, int STAGES, int NT, int U, int QT = QT_NONE>
 __global__ void __launch_bounds__((NT + 1) * 32, 1)
     fwht_small_kernel(const uint16_t* __restrict__ in, uint16_t* __restrict__ out, int64_t total_bytes,
-                      int64_t num_tiles, float scale) {
+                      int64_t num_tiles, float scale, uint8_t* __restrict__ out_q = nullptr,
+                      float* __restrict__ row_scale = nullptr) {
   constexpr int K = log2_n<N>();
   constexpr int G = N >= 8 ? N / 8 : 1;            // granules per item
   constexpr int ITEM_BYTES = 16 * G;
@@ -129,7 +132,7 @@ __global__ void __launch_bounds__((NT + 1) * 32, 1)
         if (t < 0) break;
         mbar_wait(&done[s], (it / STAGES) & 1);
         const uint32_t b16 = uint32_t(tile_bytes(t)) & ~15u;
-        if (b16) bulk_s2g(reinterpret_cast<uint8_t*>(out) + t * TILE_BYTES, smem + s * TILE_BYTES, b16);
+        if (QT < 0 && b16) bulk_s2g(reinterpret_cast<uint8_t*>(out) + t * TILE_BYTES, smem + s * TILE_BYTES, b16);
         bulk_commit();
         if (ended) continue;
         if (tile < 0 || tile >= num_tiles) {
@@ -157,6 +160,11 @@ __global__ void __launch_bounds__((NT + 1) * 32, 1)
   float sc[G];
 #pragma unroll
   for (int j = 0; j < G; ++j) sc[j] = (__popc((uint32_t(j) ^ c) & c) & 1) ? -scale : scale;
+  // fused quantization, fast path: scale = max|v| |scale| / Q, multiplier sign(scale) Q / max|v|
+  const float q_qs = copysignf(qmax_of<QT == QT_NONE ? QT_E4M3 : QT>(), scale);
+  const float q_ss = fabsf(scale) / qmax_of<QT == QT_NONE ? QT_E4M3 : QT>();
+  (void)q_qs;
+  (void)q_ss;
   float sg[KG > 0 ? KG : 1];  // sign of the second operand of the granule-bit butterflies
 #pragma unroll
   for (int b = 0; b < KG; ++b) sg[b] = ((c >> b) & 1u) ? -1.f : 1.f;
@@ -220,6 +228,79 @@ __global__ void __launch_bounds__((NT + 1) * 32, 1)
               v[u][e] = fmaf(p1, sg[b], p0);
               v[u][e | (8 << b)] = fmaf(p1, -sg[b], p0);
             }
+      }
+      if constexpr (QT >= 0) {
+        // ---- fused quantization: rows are in-lane (n >= 16: the item; n <= 8: 8/n rows of
+        // the granule, contiguous in v); y = v * sc[j], so |y| = |v| |scale|
+        constexpr int RI = N >= 8 ? 1 : 8 / N;  // rows per item
+        constexpr int CB2 = QT == QT_INT4 ? 1 : 2;  // code bytes per 2 elements
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int item = i0 + u * NT * 32;
+          if (item >= items) continue;
+          const int64_t el0 = (tile * TILE_BYTES + int64_t(item) * ITEM_BYTES) / 2;  // first element of the item
+          float mul[RI], scr[RI];
+          bool fast = true;
+#pragma unroll
+          for (int rr = 0; rr < RI; ++rr) {
+            float a = 0.f;
+#pragma unroll
+            for (int e = 0; e < (N >= 8 ? 8 * G : N); ++e) a = absmax_nan(a, v[u][rr * N + e]);
+            if (quant_fast_range(a, 0x1p100f)) {
+              scr[rr] = a * q_ss;                 // max |y| / Q
+              mul[rr] = q_qs * rcp_ftz(a);        // Q / max |v|, times sign(scale)
+            } else {
+              float inv;
+              row_scale_of<QT>(a * fabsf(scale), scr[rr], inv);
+              mul[rr] = inv * scale;              // per unit of v (y = v * scale * sign_j)
+              fast = false;
+            }
+          }
+          // row scales: the item's RI rows are consecutive -> one vector store when whole
+          const int64_t row0 = el0 / N;
+          // (row_scale need only be 4-byte aligned: vector stores when it is 8/16-byte aligned)
+          const bool whole = (N >= 8 || item * 16 + 16 <= b16) &&
+                             (reinterpret_cast<uintptr_t>(row_scale) & (RI == 4 ? 15u : (RI == 2 ? 7u : 3u))) == 0;
+          if constexpr (RI == 4) {
+            if (whole) *reinterpret_cast<float4*>(row_scale + row0) = make_float4(scr[0], scr[1], scr[2], scr[3]);
+          } else if constexpr (RI == 2) {
+            if (whole) *reinterpret_cast<float2*>(row_scale + row0) = make_float2(scr[0], scr[1]);
+          } else {
+            row_scale[row0] = scr[0];
+          }
+          if (!whole)  // partial granule (n <= 4): the valid rows only
+            for (int rr = 0; rr < RI; ++rr)
+              if (item * 16 + rr * 2 * N < bytes) row_scale[row0 + rr] = scr[rr];
+#pragma unroll
+          for (int j = 0; j < G; ++j) {
+            // slot sign (sc[j] = +-scale): the multipliers above already carry sign(scale)
+            const float sj = (sc[j] < 0.f) != (scale < 0.f) ? -1.f : 1.f;
+            uint32_t c0, c1;
+            const float* vv = &v[u][8 * j];
+            if (fast && N >= 4) {  // one multiplier per group of 4 (a row has >= 4 elements)
+              c0 = quant4_fast<QT>(vv[0], vv[1], vv[2], vv[3], sj * mul[N >= 8 ? 0 : 0]);
+              c1 = quant4_fast<QT>(vv[4], vv[5], vv[6], vv[7], sj * mul[N >= 8 ? 0 : (4 / N < RI ? 4 / N : 0)]);
+            } else {
+              float t[8];
+#pragma unroll
+              for (int e = 0; e < 8; ++e)  // + 0: a zero stays +0 (code 0x00) whatever the slot's sign
+                t[e] = fmaf(vv[e] * sj, mul[N >= 8 ? 0 : (e / N)], 0.f);
+              c0 = quant4<QT>(t[0], t[1], t[2], t[3]);
+              c1 = quant4<QT>(t[4], t[5], t[6], t[7]);
+            }
+            const int64_t cbyte = ((el0 + 8 * int64_t(uint32_t(j) ^ c)) * CB2) / 2;  // slot j holds granule j ^ c
+            if (N <= 4 && item * 16 + 16 > b16) {  // partial last granule: only the valid rows' codes
+              const int valid = (bytes - item * 16) / 2 * CB2 / 2;  // code bytes
+              const uint32_t cw[2] = {QT == QT_INT4 ? __byte_perm(c0, c1, 0x5410) : c0, c1};
+              for (int bq = 0; bq < valid; ++bq) out_q[cbyte + bq] = uint8_t(cw[bq >> 2] >> (8 * (bq & 3)));
+            } else if constexpr (QT == QT_INT4) {
+              *reinterpret_cast<uint32_t*>(out_q + cbyte) = __byte_perm(c0, c1, 0x5410);
+            } else {
+              *reinterpret_cast<uint2*>(out_q + cbyte) = make_uint2(c0, c1);
+            }
+          }
+        }
+        continue;
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {

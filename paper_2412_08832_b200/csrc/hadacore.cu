@@ -268,35 +268,37 @@ hadacore_status_t launch(const void* in, void* out, uint8_t* out_q, float* row_s
   return cudaPeekAtLastError() == cudaSuccess ? HADACORE_OK : HADACORE_ERR_CUDA;
 }
 
-template <int N, int DT>
-hadacore_status_t launch_small(const void* in, void* out, int64_t m, float scale, cudaStream_t stream) {
+template <int N, int DT, int QT = QT_NONE>
+hadacore_status_t launch_small(const void* in, void* out, int64_t m, float scale, cudaStream_t stream,
+                               uint8_t* out_q = nullptr, float* row_scale = nullptr) {
   using T = TunedS<N>;
   constexpr int tile = T::tkb * 1024;
   constexpr int smem = T::st * tile + int(sizeof(SchedCtl)) + 2 * T::st * 8;
   static std::atomic<uint64_t> attr_done{0};
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return HADACORE_ERR_CUDA;
-  auto kern = fwht_small_kernel<N, DT, tile, T::st, T::nt, T::u>;
+  auto kern = fwht_small_kernel<N, DT, tile, T::st, T::nt, T::u, QT>;
   if (!ensure_smem_attr(kern, smem, attr_done, dev)) return HADACORE_ERR_CUDA;
   const int64_t total = m * N * 2;
   const int64_t tiles = (total + tile - 1) / tile;
   const int64_t max_ctas = kClc ? int64_t(INT32_MAX) : int64_t(sm_count(dev));
   const int grid = int(tiles < max_ctas ? tiles : max_ctas);
   if (launch_pdl(kern, grid, (T::nt + 1) * 32, smem, stream, static_cast<const uint16_t*>(in),
-                 static_cast<uint16_t*>(out), total, tiles, scale) != cudaSuccess)
+                 static_cast<uint16_t*>(out), total, tiles, scale, out_q, row_scale) != cudaSuccess)
     return HADACORE_ERR_CUDA;
   return cudaPeekAtLastError() == cudaSuccess ? HADACORE_OK : HADACORE_ERR_CUDA;
 }
 
-template <int DT>
-hadacore_status_t dispatch_small(const void* in, void* out, int64_t m, int64_t n, float scale, cudaStream_t st) {
+template <int DT, int QT = QT_NONE>
+hadacore_status_t dispatch_small(const void* in, void* out, int64_t m, int64_t n, float scale, cudaStream_t st,
+                                 uint8_t* q = nullptr, float* rs = nullptr) {
   switch (n) {
-    case 2: return launch_small<2, DT>(in, out, m, scale, st);
-    case 4: return launch_small<4, DT>(in, out, m, scale, st);
-    case 8: return launch_small<8, DT>(in, out, m, scale, st);
-    case 16: return launch_small<16, DT>(in, out, m, scale, st);
-    case 32: return launch_small<32, DT>(in, out, m, scale, st);
-    case 64: return launch_small<64, DT>(in, out, m, scale, st);
+    case 2: return launch_small<2, DT, QT>(in, out, m, scale, st, q, rs);
+    case 4: return launch_small<4, DT, QT>(in, out, m, scale, st, q, rs);
+    case 8: return launch_small<8, DT, QT>(in, out, m, scale, st, q, rs);
+    case 16: return launch_small<16, DT, QT>(in, out, m, scale, st, q, rs);
+    case 32: return launch_small<32, DT, QT>(in, out, m, scale, st, q, rs);
+    case 64: return launch_small<64, DT, QT>(in, out, m, scale, st, q, rs);
     default: return HADACORE_ERR_INVALID_N;
   }
 }
@@ -496,6 +498,13 @@ hadacore_status_t run(const void* in, void* out, int64_t m, int64_t n, int dtype
 template <int DT>
 hadacore_status_t run_quant_dt(const void* in, uint8_t* q, float* rs, const Layout& L, int64_t n, int qtype,
                                float scale, cudaStream_t st) {
+  if (n < 128) {  // rows shorter than 128 (fwht_small_kernel's fused epilogue)
+    switch (qtype) {
+      case HADACORE_Q_E4M3: return dispatch_small<DT, QT_E4M3>(in, nullptr, L.m_outer, n, scale, st, q, rs);
+      case HADACORE_Q_INT8: return dispatch_small<DT, QT_INT8>(in, nullptr, L.m_outer, n, scale, st, q, rs);
+      default: return dispatch_small<DT, QT_INT4>(in, nullptr, L.m_outer, n, scale, st, q, rs);
+    }
+  }
   switch (qtype) {
     case HADACORE_Q_E4M3: return dispatch_n<DT, QT_E4M3>(in, nullptr, q, rs, L, n, scale, st);
     case HADACORE_Q_INT8: return dispatch_n<DT, QT_INT8>(in, nullptr, q, rs, L, n, scale, st);
@@ -569,7 +578,6 @@ extern "C" hadacore_status_t hadacore_fwht_quant(const void* in, void* out_q, fl
                                                  float scale, hadacore_stream_t stream) {
   if (qtype != HADACORE_Q_E4M3 && qtype != HADACORE_Q_INT8 && qtype != HADACORE_Q_INT4) return HADACORE_ERR_DTYPE;
   if (dtype == HADACORE_F32) return HADACORE_ERR_DTYPE;  // the fused path takes 16-bit inputs
-  if (!valid_n_paper(n)) return HADACORE_ERR_INVALID_N;
   // validate `in` (and m, n, dtype, scale) exactly like hadacore_fwht, with out = in
   const hadacore_status_t v = validate(in, in, m, n, int(dtype), scale, true);
   if (v != HADACORE_OK || m == 0) return v;
@@ -708,7 +716,7 @@ extern "C" const char* hadacore_status_string(hadacore_status_t s) {
   switch (s) {
     case HADACORE_OK: return "ok";
     case HADACORE_ERR_INVALID_N:
-      return "n must be a power of two in [2, 32768] ([128, 32768] for the strided and quantizing entry points)";
+      return "n must be a power of two in [2, 32768] ([128, 32768] for the strided entry point)";
     case HADACORE_ERR_INVALID_M: return "m must be >= 0 and m*n*2 must fit in int64";
     case HADACORE_ERR_NULL: return "in/out must be non-NULL when m > 0";
     case HADACORE_ERR_MISALIGNED: return "in/out must be 16-byte aligned";

@@ -107,7 +107,8 @@ def test_quant_entry_validation(lib):
     assert f(a, a + 512, rs, 4, 256, 0, 2, 1.0, None) == OVERLAP   # int4 codes inside the input
     assert f(a, q, rs, 4, 256, 3, 0, 1.0, None) == DTYPE          # unknown dtype
     assert f(a, q, rs, 4, 100, 0, 0, 1.0, None) == INVALID_N
-    assert f(a, q, rs, 4, 64, 0, 0, 1.0, None) == INVALID_N      # fused quantization: the paper's 2^7..2^15
+    assert f(a, q, rs, 4, 1, 0, 0, 1.0, None) == INVALID_N       # fused quantization: n = 2..2^15
+    assert f(a, q, rs, 4, 65536, 0, 0, 1.0, None) == INVALID_N
     assert f(a, q, rs, 4, 256, 0, 1, float("nan"), None) == SCALE
     assert f(a, None, rs, 4, 256, 0, 0, 1.0, None) == NULL
     assert f(a, q, None, 4, 256, 0, 0, 1.0, None) == NULL

@@ -27,7 +27,7 @@ import synthetic
 
 pytestmark = pytest.mark.gpu
 
-NS = [1 << k for k in range(7, 16)]
+NS = [1 << k for k in range(1, 16)]  # n < 128: fwht_small_kernel's fused epilogue
 DTYPES = [torch.float16, torch.bfloat16]
 TOL = {torch.float16: 2e-3, torch.bfloat16: 1.6e-2}
 QMAX = {"e4m3": 448.0, "int8": 127.0, "int4": 7.0}
@@ -86,7 +86,7 @@ def adjacent(v_gpu: np.ndarray, v_ref: np.ndarray, qtype: str) -> np.ndarray:
 
 
 def ragged_m(n):
-    return max(3, (1 << 19) // n) + 1
+    return max(3, (1 << 19) // n) + 1  # odd: n <= 4 ends in a partial 16-byte granule
 
 
 @pytest.mark.parametrize("qtype", QTYPES)
@@ -183,7 +183,7 @@ def test_quant_matches_fwht_then_quantize_on_gpu_values(hc):
         assert np.all(np.abs(vg - vr) <= 1)
 
 
-@pytest.mark.parametrize("n", [128, 256, 512, 4096, 32768])
+@pytest.mark.parametrize("n", [2, 8, 64, 128, 256, 512, 4096, 32768])
 def test_int4_packing_and_views(hc, n):
     """INT4 layout: (m, n/2) bytes, element 2j in the low nibble of byte j; leading dims
     are rows; a ragged m; the codes unpack to the oracle's within one step."""
@@ -195,3 +195,36 @@ def test_int4_packing_and_views(hc, n):
     cg = gpu_codes(q.reshape(-1, n // 2), "int4")
     assert np.all(np.abs(code_values(cg, "int4") - code_values(cr, "int4")) <= 1)
     assert np.mean(cg == cr) >= 0.95
+
+
+@pytest.mark.parametrize("qtype", QTYPES)
+@pytest.mark.parametrize("n", [2, 4, 8, 16, 64])
+def test_small_n_quant_tail_and_bounds(hc, n, qtype):
+    """n < 128: every ragged tail (odd m for n <= 4 leaves a partial granule) writes
+    exactly the valid codes and scales -- bytes past the end are untouched."""
+    for m in (1, 2, 3, 5, 7, 4097):
+        x = synthetic.generate(m, n, torch.bfloat16, 60 + m, dist="D1").cuda()
+        cb = n // 2 if qtype == "int4" else n
+        qbuf = torch.full((m * cb + 32,), 0xAB, dtype=torch.uint8, device="cuda")
+        sbuf = torch.full((m + 8,), -7.0, dtype=torch.float32, device="cuda")
+        qv = qbuf[: m * cb].view(m, cb)
+        qv = qv.view(torch.float8_e4m3fn) if qtype == "e4m3" else (qv.view(torch.int8) if qtype == "int8" else qv)
+        hc.hadacore_fwht_quant(x, qtype=qtype, out=qv, row_scale=sbuf[:m])
+        assert torch.all(qbuf[m * cb:] == 0xAB) and torch.all(sbuf[m:] == -7.0), m
+        y = oracle.fwht(x.cpu().double().numpy())
+        cr, sr = oracle.quantize_rows(y, qtype)
+        cg = gpu_codes(qv, qtype)
+        assert np.all(np.abs(sbuf[:m].cpu().double().numpy() - sr) <= TOL[torch.bfloat16] * sr), m
+        assert np.all(adjacent(code_values(cg, qtype), code_values(cr, qtype), qtype)), m
+
+
+def test_small_n_quant_unaligned_row_scale(hc):
+    """row_scale needs only 4-byte alignment (C contract): n = 2, 4 with a row_scale at an
+    odd float offset (the kernel falls back from vector scale stores)."""
+    for n in (2, 4):
+        m = 4099
+        x = synthetic.generate(m, n, torch.float16, 3).cuda()
+        big = torch.zeros(m + 1, dtype=torch.float32, device="cuda")
+        q, s = hc.hadacore_fwht_quant(x, qtype="int8", row_scale=big[1:])
+        q2, s2 = hc.hadacore_fwht_quant(x, qtype="int8")
+        assert torch.equal(s, s2) and torch.equal(q.view(torch.uint8), q2.view(torch.uint8))
