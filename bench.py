@@ -466,6 +466,29 @@ def main():
     # per-launch breakdown: a separate pass after the timed region
     _, per = timed_region(max(3, min(args.steps, 10)), True)
 
+    # output check outside the timed regions, on every rank (no oracle here: a property that
+    # holds at any size) -- the normalized transform preserves every row's
+    # norm; the worst relative norm error over all rows of every (dtype, n) launch, max over ranks
+    check = None
+    if not quant and not rotate:
+        worst, by_dt = 0.0, {}
+        tol_of = {torch.float16: 2e-3, torch.bfloat16: 1.6e-2, torch.float32: 1e-5}
+        for dt, n in pairs:
+            launch(dt, n)
+            x = xin[dt].view(-1, n)
+            y = (obuf.view(-1, n) if f32 else obuf.view(torch.int16).view(dt).view(-1, n))[: x.shape[0]]
+            for r0 in range(0, x.shape[0], max(1, (1 << 26) // n)):
+                nx = torch.linalg.vector_norm(x[r0:r0 + (1 << 26) // n].float(), dim=1)
+                ny = torch.linalg.vector_norm(y[r0:r0 + (1 << 26) // n].float(), dim=1)
+                e = ((ny - nx).abs() / nx.clamp_min(1e-30)).max().item()
+                by_dt[dt] = max(by_dt.get(dt, 0.0), e)
+        names = {torch.float16: "fp16", torch.bfloat16: "bf16", torch.float32: "fp32"}
+        errs = {names[dt]: float(f"{max_over_ranks(e, dist, torch):.3e}") for dt, e in by_dt.items()}
+        check = {"property": "row-norm preservation of the normalized transform, every row of every launch "
+                             "(north_star tolerances per dtype)",
+                 "max_rel_err": errs, "tolerance": {names[dt]: tol_of[dt] for dt in by_dt},
+                 "pass": all(errs[names[dt]] <= tol_of[dt] for dt in by_dt)}
+
     # same-run D2D copy of the same byte count ("% of achievable copy"): cudaMemcpyAsync
     # of one input buffer into the output buffer, event-timed on the same stream
     src_b = next(iter(xin.values())).view(torch.uint8)
@@ -595,7 +618,7 @@ def main():
             "elements_per_s": float(f"{(C5_ELEMS * args.steps if c5 else sum(elems_of[p] for p in pairs) * args.steps * world) / (t_max * 1e-3):.4g}"),
             "per_n_GBps": per_n, "roofline": roofline, "cpu_baseline": cpu_baseline, "e2e": e2e,
             "gpu_launches": int(args.steps * sum(hc.launches_per_call(elems_of[(dt, n)] // n, n, dt) for dt, n in pairs)),
-            "clocks": clocks, "remeasured_for_clocks": remeasured,
+            "clocks": clocks, "remeasured_for_clocks": remeasured, "check": check,
         }
         print(json.dumps(line), flush=True)
     if dist is not None:
