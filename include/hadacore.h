@@ -17,7 +17,7 @@
  * than 128").
  *
  * Layout: `in` and `out` are row-major m x n matrices of 16-bit floats (IEEE
- * binary16 or bfloat16; or binary32 for the HADACORE_F32 debug path), contiguous,
+ * binary16 or bfloat16; or binary32 for the HADACORE_F32 path), contiguous,
  * row pitch = n elements, in DEVICE memory of
  * the current CUDA device, 16-byte aligned.  in == out (in-place, P:264-274
  * [App. B]) is allowed and gives bit-identical results to out-of-place.
