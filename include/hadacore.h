@@ -94,7 +94,7 @@ hadacore_status_t hadacore_fwht(const void* in, void* out, int64_t m, int64_t n,
 
 /*
  * End-to-end variant on HOST buffers (the call a host-side user makes): copies row
- * blocks (<= 16 MiB) host->device into `workspace`, transforms them in place with the
+ * blocks (<= 32 MiB) host->device into `workspace`, transforms them in place with the
  * same kernel, and copies them device->host into `out_host`, pipelined over up to
  * four workspace slots and internal streams so both copy directions overlap the
  * kernels.  Returns after the last

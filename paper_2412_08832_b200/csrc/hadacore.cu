@@ -604,8 +604,14 @@ extern "C" hadacore_status_t hadacore_fwht_host(const void* in_host, void* out_h
   // The workspace is cut into NS slots of at most kBlockBytes, one internal stream
   // each; block b goes H2D -> kernel (in place) -> D2H on stream b % NS.  Small blocks
   // and several streams keep both PCIe directions busy (short pipeline fill/drain).
-  constexpr size_t kBlockBytes = size_t(16) << 20;
-  constexpr int kMaxSlots = 4;
+#ifndef HC_HOST_BLOCK_MB
+#define HC_HOST_BLOCK_MB 32  // A/B: profiles/r01_ab_host_pipeline.txt
+#endif
+#ifndef HC_HOST_SLOTS
+#define HC_HOST_SLOTS 4
+#endif
+  constexpr size_t kBlockBytes = size_t(HC_HOST_BLOCK_MB) << 20;
+  constexpr int kMaxSlots = HC_HOST_SLOTS;
   // slot offsets stay 16-byte aligned: rows of < 16 bytes (n < 8) go in groups of
   // 16 / row_bytes rows
   const int64_t align_rows = row_bytes >= 16 ? 1 : int64_t(16 / row_bytes);
@@ -619,7 +625,7 @@ extern "C" hadacore_status_t hadacore_fwht_host(const void* in_host, void* out_h
     rows_per_slot = workspace_bytes / row_bytes >= size_t(align_rows) ? align_rows : 1;
   }
   cudaStream_t user = reinterpret_cast<cudaStream_t>(stream);
-  cudaStream_t st[kMaxSlots] = {nullptr, nullptr, nullptr, nullptr};
+  cudaStream_t st[kMaxSlots] = {};
   cudaEvent_t ev = nullptr;
   hadacore_status_t rc = HADACORE_OK;
   for (int i = 0; i < slots && rc == HADACORE_OK; ++i)
