@@ -52,7 +52,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--ns", default=None, help="comma-separated n list overriding the workload's sweep "
                                                "(e.g. --workload quant-e4m3 --ns 2,4,8,16,32,64)")
-    ap.add_argument("--workload", choices=["fwht", "quant-e4m3", "quant-int8", "quant-int4", "qk-rotate", "small", "f32", "c5", "c1"], default="fwht",
+    ap.add_argument("--workload", choices=["fwht", "quant-e4m3", "quant-int8", "quant-int4", "qk-rotate", "qk-quant", "small", "f32", "c5",
+                             "c1"], default="fwht",
                     help="fwht = the metric's C3 sweep (default); quant-* = the fused FWHT + per-row "
                          "quantization row (NEXT-1) on the same inputs; small = n=2^1..2^6 (NEXT-2); "
                          "f32 = the fp32 path over n=2^1..2^15 (NEXT-2); c5 = BASELINE config C5: bf16 "
@@ -254,6 +255,10 @@ def config_block(args, world):
     if getattr(args, "workload", "fwht") == "qk-rotate":
         wl = ("QK rotation: n=2^7..2^15 x {fp16, bf16}; a 2^28-element QKV buffer viewed as [T, 3, H, n], "
               "H = max(1, 4096/n); the Q and K heads (2/3 of it) transformed in place, normalized")
+    if getattr(args, "workload", "fwht") == "qk-quant":
+        wl = ("QK rotation + FP8-E4M3 quantization: n=2^7..2^15 x {fp16, bf16}; a 2^28-element QKV buffer viewed "
+              "as [T, 3, H, n], H = max(1, 4096/n); the Q and K heads read strided, codes and row scales written "
+              "contiguously (hadacore_fwht_quant_strided), normalized")
     return {"workload": wl,
             "elements_per_launch": args.elems, "ns": ns,
             "dtypes": {"f32": ["fp32"], "c5": ["bf16"]}.get(getattr(args, "workload", "fwht"), ["fp16", "bf16"]),
@@ -389,7 +394,11 @@ def main():
         sbuf = torch.empty(args.elems // min(ns), dtype=torch.float32, device=dev)
     qb = 0.5 if qtype == "int4" else 1.0  # code bytes per element
 
-    rotate = args.workload == "qk-rotate"
+    rotate = args.workload in ("qk-rotate", "qk-quant")
+    qkq = args.workload == "qk-quant"  # Q/K heads rotated + FP8-quantized in one pass (FP8 attention)
+    if qkq:
+        qbuf = torch.empty(args.elems, dtype=torch.float8_e4m3fn, device=dev)
+        sbuf = torch.empty(args.elems // 128, dtype=torch.float32, device=dev)
     qk = {}
     if rotate:
         # fused QKV activations [T, 3, H, n] (H = max(1, 4096 / n) heads); the Q and K
@@ -404,7 +413,11 @@ def main():
     def launch(dt, n):
         if rotate:
             v = qk[(dt, n)]
-            hc.hadacore_fwht_strided(v, out=v, stream=stream)
+            if qkq:
+                hc.hadacore_fwht_quant_strided(v, qtype="e4m3", out=qbuf[: v.numel()], row_scale=sbuf[: v.numel() // n],
+                                               stream=stream)
+            else:
+                hc.hadacore_fwht_strided(v, out=v, stream=stream)
             return
         x = xin[dt].view(-1, n)
         if quant:
@@ -512,6 +525,8 @@ def main():
         sum((2.0 + qb) * args.elems + 4.0 * (args.elems // n) for n in ns) / len(ns)
     if rotate:
         bytes_per_launch = sum(4.0 * e for e in elems_of.values()) / len(pairs)
+    if qkq:  # 2 B read + 1 B code per element + a 4-byte scale per row
+        bytes_per_launch = sum(3.0 * e + 4.0 * e / n for (dt, n), e in elems_of.items()) / len(pairs)
     total_bytes = bytes_per_launch * len(pairs) * args.steps * world
     if c5:  # strong scaling: the whole 2^33-element job per step, whatever the rank count
         total_bytes = 4.0 * C5_ELEMS * args.steps
@@ -523,6 +538,8 @@ def main():
         ts = sorted(per[k::len(pairs)])
         med = ts[len(ts) // 2]
         b_n = 2.0 * esize * elems_of[(dt, n)] if not quant else (2.0 + qb) * args.elems + 4.0 * (args.elems // n)
+        if qkq:
+            b_n = 3.0 * elems_of[(dt, n)] + 4.0 * elems_of[(dt, n)] / n
         per_n.setdefault({torch.float16: "fp16", torch.bfloat16: "bf16", torch.float32: "fp32"}[dt], {})[str(n)] = round(b_n / (med * 1e-3) / 1e9, 1)
     # roofline over the timed region: every launch of the step is the same transform
     # (one per (dtype, n)), so the kernel's average launch duration is the region time
@@ -603,7 +620,10 @@ def main():
             metric = metric.replace("n=2^7..2^15", f"n in {{{args.ns}}}")
         if args.workload == "small":
             metric = "FWHT HBM GB/s vs n=2^1..2^6 (bf16/fp16), rows shorter than the paper's 2^7 (NEXT-2)"
-        if rotate:
+        if qkq:
+            metric = ("FWHT + FP8-E4M3 quantization of the Q and K heads of fused QKV activations [T, 3, H, n] "
+                      "(strided rows, codes + fp32 scales out) HBM GB/s vs n=2^7..2^15")
+        elif rotate:
             metric = ("In-place FWHT of the Q and K heads of fused QKV activations [T, 3, H, n] (strided rows) "
                       "HBM GB/s vs n=2^7..2^15")
         line = {

@@ -171,6 +171,22 @@ hadacore_status_t hadacore_fake_quant(const float* in, float* out, float* row_am
 hadacore_status_t hadacore_row_sq_error(const float* a, const float* b, double* out, int64_t m, int64_t n,
                                         hadacore_stream_t stream);
 
+/*
+ * Strided rows + fused quantization (NEXT-1 x NEXT-3): the transform of the rows of a
+ * 2-level grid (as hadacore_fwht_strided: row (i, j) at in + i * in_stride_outer +
+ * j * in_stride_inner elements) fused with the per-row quantization of
+ * hadacore_fwht_quant, codes and scales written CONTIGUOUSLY in row order (i, j):
+ * out_q is [m_outer * m_inner, n] bytes ([.., n/2] for INT4), row_scale has
+ * m_outer * m_inner floats -- e.g. the Q (or K) heads of a fused QKV projection
+ * [tokens, 3, H, d] rotated and quantized to FP8 in one pass for FP8 attention
+ * (P:24).  n = 2^7..2^15; stride rules as hadacore_fwht_strided; the input is
+ * not modified; none of the three ranges may overlap.
+ */
+hadacore_status_t hadacore_fwht_quant_strided(const void* in, void* out_q, float* row_scale, int64_t m_outer,
+                                              int64_t m_inner, int64_t in_stride_outer, int64_t in_stride_inner,
+                                              int64_t n, hadacore_dtype_t dtype, hadacore_qtype_t qtype, float scale,
+                                              hadacore_stream_t stream);
+
 /* Static, human-readable description of a status code (never NULL). */
 const char* hadacore_status_string(hadacore_status_t status);
 

@@ -23,7 +23,8 @@ import os
 import torch
 
 __all__ = ["hadacore_fwht", "hadacore_fwht_host", "hadacore_fwht_quant", "hadacore_fwht_strided", "fwht", "HadacoreError",
-           "library_path", "version", "launches_per_call", "STATUS", "QTYPES", "fake_quant", "row_sq_error"]
+           "library_path", "version", "launches_per_call", "STATUS", "QTYPES", "fake_quant", "row_sq_error",
+           "hadacore_fwht_quant_strided"]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_HERE, "libhadacore.so")
@@ -66,6 +67,8 @@ def _load():
     lib.hadacore_fwht_quant.restype = ctypes.c_int
     lib.hadacore_fwht_strided.argtypes = [vp, vp, i64, i64, i64, i64, i64, i64, i64, ctypes.c_int, f32, vp]
     lib.hadacore_fwht_strided.restype = ctypes.c_int
+    lib.hadacore_fwht_quant_strided.argtypes = [vp, vp, vp, i64, i64, i64, i64, i64, ctypes.c_int, ctypes.c_int, f32, vp]
+    lib.hadacore_fwht_quant_strided.restype = ctypes.c_int
     lib.hadacore_fake_quant.argtypes = [vp, vp, vp, i64, i64, ctypes.c_int, ctypes.c_int, vp]
     lib.hadacore_fake_quant.restype = ctypes.c_int
     lib.hadacore_row_sq_error.argtypes = [vp, vp, vp, i64, i64, vp]
@@ -201,6 +204,24 @@ def hadacore_fwht_quant(x: torch.Tensor, qtype: str = "e4m3", scale: float | Non
     return out, row_scale
 
 
+def _row_grid(t: torch.Tensor, n: int):
+    """Collapse a view's leading dims (dropping size-1 dims) into <= 2 strided row dims:
+    (m_outer, m_inner, stride_outer, stride_inner) in elements."""
+    dims = [(s, st) for s, st in zip(t.shape[:-1], t.stride()[:-1]) if s != 1]
+    merged = []
+    for size, st in dims:
+        if merged and merged[-1][1] == st * size:
+            merged[-1] = (merged[-1][0] * size, st)
+        else:
+            merged.append((size, st))
+    if len(merged) > 2:
+        raise HadacoreError(2, "more than two non-collapsible row dimensions")
+    while len(merged) < 2:
+        merged.insert(0, (1, n * (merged[0][0] if merged else 1)))
+    (mo, so), (mi, si) = merged
+    return mo, mi, so, si
+
+
 def hadacore_fwht_strided(x: torch.Tensor, out: torch.Tensor | None = None, scale: float | None = None,
                           stream: torch.cuda.Stream | None = None) -> torch.Tensor:
     """Transform the last dimension of a strided view (C: hadacore_fwht_strided).
@@ -219,24 +240,8 @@ def hadacore_fwht_strided(x: torch.Tensor, out: torch.Tensor | None = None, scal
     if out.shape != x.shape or out.dtype != x.dtype or out.stride(-1) != 1:
         raise HadacoreError(3, "out must have x's shape and dtype and a contiguous last dimension")
 
-    def grid(t):
-        # collapse leading dims (dropping size-1 dims) into <= 2 strided row dims
-        dims = [(s, st) for s, st in zip(t.shape[:-1], t.stride()[:-1]) if s != 1]
-        merged = []
-        for size, st in dims:
-            if merged and merged[-1][1] == st * size:
-                merged[-1] = (merged[-1][0] * size, st)
-            else:
-                merged.append((size, st))
-        if len(merged) > 2:
-            raise HadacoreError(2, "more than two non-collapsible row dimensions")
-        while len(merged) < 2:
-            merged.insert(0, (1, n * (merged[0][0] if merged else 1)))
-        (mo, so), (mi, si) = merged
-        return mo, mi, so, si
-
-    mo, mi, so, si = grid(x)
-    mo2, mi2, oso, osi = grid(out)
+    mo, mi, so, si = _row_grid(x, n)
+    mo2, mi2, oso, osi = _row_grid(out, n)
     if (mo2, mi2) != (mo, mi):
         raise HadacoreError(3, "out's row grid differs from x's")
     if scale is None:
@@ -281,3 +286,33 @@ def row_sq_error(a: torch.Tensor, b: torch.Tensor, stream: torch.cuda.Stream | N
         st = stream if stream is not None else torch.cuda.current_stream(a.device)
         _check(_load().hadacore_row_sq_error(a.data_ptr(), b.data_ptr(), out.data_ptr(), m, n, st.cuda_stream))
     return out[:m]
+
+
+def hadacore_fwht_quant_strided(x: torch.Tensor, qtype: str = "e4m3", scale: float | None = None,
+                                out: torch.Tensor | None = None, row_scale: torch.Tensor | None = None,
+                                stream: torch.cuda.Stream | None = None):
+    """Transform + per-row quantization of a strided view (C: hadacore_fwht_quant_strided), e.g.
+    ``qkv[:, 0:2]`` of a ``[tokens, 3, H, d]`` projection: the Q and K heads rotated and quantized
+    in one pass (FP8 attention).  Returns contiguous ``(q, row_scale)`` with the view's row shape:
+    ``q`` [..., n] (``[..., n/2]`` uint8 for "int4"), ``row_scale`` [...] float32; x is not modified."""
+    m, n = _shape(x)
+    if qtype not in QTYPES:
+        raise HadacoreError(6, f"qtype {qtype!r} (expected one of {sorted(QTYPES)})")
+    if not x.is_cuda or x.stride(-1) != 1:
+        raise HadacoreError(4, "x must be a CUDA view with a contiguous last dimension")
+    code, qdt = QTYPES[qtype]
+    qshape = (*x.shape[:-1], n // 2 if qtype == "int4" else n)
+    q = out if out is not None else torch.empty(qshape, dtype=qdt, device=x.device)
+    rs = row_scale if row_scale is not None else torch.empty(x.shape[:-1], dtype=torch.float32, device=x.device)
+    if q.dtype != qdt or q.numel() != m * qshape[-1] or not q.is_contiguous() or q.device != x.device:
+        raise HadacoreError(3, f"out must be a contiguous {qdt} tensor of {m * qshape[-1]} elements on x's device")
+    if rs.dtype != torch.float32 or rs.numel() != m or not rs.is_contiguous():
+        raise HadacoreError(3, "row_scale must be a contiguous float32 tensor with one entry per row")
+    mo, mi, so, si = _row_grid(x, n)
+    if scale is None:
+        scale = 1.0 / math.sqrt(n) if n > 0 else 1.0
+    with torch.cuda.device(x.device):
+        st = stream if stream is not None else torch.cuda.current_stream(x.device)
+        _check(_load().hadacore_fwht_quant_strided(x.data_ptr(), q.data_ptr(), rs.data_ptr(), mo, mi, so, si, n,
+                                                   _DTYPES[x.dtype], code, float(scale), st.cuda_stream))
+    return q, rs

@@ -573,6 +573,39 @@ extern "C" hadacore_status_t hadacore_fwht_strided(const void* in, void* out, in
   return run_strided(in, out, L, n, int(dtype), scale, reinterpret_cast<cudaStream_t>(stream));
 }
 
+extern "C" hadacore_status_t hadacore_fwht_quant_strided(const void* in, void* out_q, float* row_scale,
+                                                         int64_t m_outer, int64_t m_inner, int64_t in_stride_outer,
+                                                         int64_t in_stride_inner, int64_t n, hadacore_dtype_t dtype,
+                                                         hadacore_qtype_t qtype, float scale,
+                                                         hadacore_stream_t stream) {
+  if (qtype != HADACORE_Q_E4M3 && qtype != HADACORE_Q_INT8 && qtype != HADACORE_Q_INT4) return HADACORE_ERR_DTYPE;
+  if (dtype != HADACORE_F16 && dtype != HADACORE_BF16) return HADACORE_ERR_DTYPE;
+  if (!valid_n_paper(n)) return HADACORE_ERR_INVALID_N;
+  if (m_outer < 0 || m_inner < 0 || m_outer > (int64_t(1) << 31) || m_inner > (int64_t(1) << 31))
+    return HADACORE_ERR_INVALID_M;
+  if (!std::isfinite(scale)) return HADACORE_ERR_SCALE;
+  if (m_outer == 0 || m_inner == 0) return HADACORE_OK;
+  if (!in || !out_q || !row_scale) return HADACORE_ERR_NULL;
+  const int64_t si = m_inner > 1 ? in_stride_inner : n;
+  if (in_stride_outer % 8 || si % 8 || in_stride_outer <= 0 || si <= 0 || in_stride_outer >= (int64_t(1) << 38) ||
+      si >= (int64_t(1) << 38) || (m_inner > 1 && si < n) || (m_outer > 1 && in_stride_outer < (m_inner - 1) * si + n))
+    return HADACORE_ERR_INVALID_M;
+  if (((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out_q)) & 15u) ||
+      (reinterpret_cast<uintptr_t>(row_scale) & 3u))
+    return HADACORE_ERR_MISALIGNED;
+  const int64_t m = m_outer * m_inner;
+  const size_t in_bytes = size_t((m_outer - 1) * in_stride_outer + (m_inner - 1) * si + n) * 2, s_bytes = size_t(m) * 4;
+  const size_t q_bytes = size_t(m) * size_t(n) / (qtype == HADACORE_Q_INT4 ? 2 : 1);
+  if (ranges_overlap(in, in_bytes, out_q, q_bytes) || ranges_overlap(in, in_bytes, row_scale, s_bytes) ||
+      ranges_overlap(out_q, q_bytes, row_scale, s_bytes))
+    return HADACORE_ERR_OVERLAP;
+  const Layout L{m_outer, m_inner, in_stride_outer, si, n * m_inner, n};  // codes: contiguous [m_outer * m_inner, n]
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  return dtype == HADACORE_F16
+             ? run_quant_dt<DT_F16>(in, static_cast<uint8_t*>(out_q), row_scale, L, n, int(qtype), scale, st)
+             : run_quant_dt<DT_BF16>(in, static_cast<uint8_t*>(out_q), row_scale, L, n, int(qtype), scale, st);
+}
+
 extern "C" hadacore_status_t hadacore_fwht_quant(const void* in, void* out_q, float* row_scale, int64_t m,
                                                  int64_t n, hadacore_dtype_t dtype, hadacore_qtype_t qtype,
                                                  float scale, hadacore_stream_t stream) {

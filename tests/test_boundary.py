@@ -31,6 +31,7 @@ def declared_functions():
 def test_header_declares_expected_entry_points():
     assert declared_functions() == sorted(["hadacore_fwht", "hadacore_fwht_host", "hadacore_fwht_quant",
                                            "hadacore_fwht_strided", "hadacore_fake_quant", "hadacore_row_sq_error",
+                                           "hadacore_fwht_quant_strided",
                                            "hadacore_status_string", "hadacore_version",
                                            "hadacore_launches_per_call", "hadacore_launches_per_call_dtype"])
 
@@ -192,3 +193,17 @@ def test_lab_entry_validation(lib):
     assert g(a, b, s + 4, 4, 16, None) == MISALIGNED
     assert g(None, b, s, 4, 16, None) == NULL
     assert g(None, None, None, 0, 16, None) == OK
+
+
+def test_quant_strided_entry_validation(lib):
+    a, q, rs = 0x10000, 0x8000000, 0x20000000
+    f = lib.hadacore_fwht_quant_strided
+    assert f(a, q, rs, 4, 3, 384, 128, 128, 0, 3, 1.0, None) == DTYPE        # qtype
+    assert f(a, q, rs, 4, 3, 384, 128, 128, 2, 0, 1.0, None) == DTYPE        # fp32 input
+    assert f(a, q, rs, 4, 3, 384, 128, 64, 0, 0, 1.0, None) == INVALID_N     # 2^7..2^15 only
+    assert f(a, q, rs, 4, 3, 384, 64, 128, 0, 0, 1.0, None) == INVALID_M     # inner rows overlap
+    assert f(a, q, rs, 4, 3, 384, 128, 128, 0, 0, float("inf"), None) == SCALE
+    assert f(a, None, rs, 4, 3, 384, 128, 128, 0, 0, 1.0, None) == NULL
+    assert f(a + 8, q, rs, 4, 3, 384, 128, 128, 0, 0, 1.0, None) == MISALIGNED
+    assert f(a, a + 256, rs, 4, 3, 384, 128, 128, 0, 0, 1.0, None) == OVERLAP
+    assert f(a, q, rs, 0, 3, 384, 128, 128, 0, 0, 1.0, None) == OK

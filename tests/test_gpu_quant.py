@@ -228,3 +228,21 @@ def test_small_n_quant_unaligned_row_scale(hc):
         q, s = hc.hadacore_fwht_quant(x, qtype="int8", row_scale=big[1:])
         q2, s2 = hc.hadacore_fwht_quant(x, qtype="int8")
         assert torch.equal(s, s2) and torch.equal(q.view(torch.uint8), q2.view(torch.uint8))
+
+
+@pytest.mark.parametrize("qtype", QTYPES)
+@pytest.mark.parametrize("n,heads", [(128, 32), (128, 3), (256, 8), (1024, 5), (4096, 2), (32768, 1)])
+def test_quant_strided_qk_heads(hc, n, heads, qtype):
+    """FP8-attention deployment path: the Q and K heads of a fused QKV
+    projection [T, 3, H, d] rotated + quantized in one pass (hadacore_fwht_quant_strided)
+    give bitwise the codes and scales of the contiguous entry on a copy; the input is
+    untouched."""
+    tokens = max(3, (1 << 19) // (3 * heads * n)) + 1
+    qkv = synthetic.generate(tokens * 3 * heads, n, torch.bfloat16, 33, dist="D1").reshape(tokens, 3, heads, n).cuda()
+    before = qkv.clone()
+    view = qkv[:, 0:2]
+    q, s = hc.hadacore_fwht_quant_strided(view, qtype=qtype)
+    assert torch.equal(qkv.view(torch.int16), before.view(torch.int16))
+    q2, s2 = hc.hadacore_fwht_quant(view.contiguous(), qtype=qtype)
+    assert q.shape == q2.shape and s.shape == s2.shape == (tokens, 2, heads)
+    assert torch.equal(q.view(torch.uint8), q2.view(torch.uint8)) and torch.equal(s, s2)
