@@ -17,7 +17,7 @@ import math
 
 import torch
 
-from . import QTYPES, hadacore_fwht, hadacore_fwht_quant
+from . import QTYPES, HadacoreError, hadacore_fwht, hadacore_fwht_quant, hadacore_fwht_quant_strided
 
 
 @torch.library.custom_op("hadacore::fwht", mutates_args=())
@@ -57,6 +57,11 @@ def _(x: torch.Tensor, scale: float | None = None) -> None:
 
 @torch.library.custom_op("hadacore::fwht_quant", mutates_args=())
 def fwht_quant(x: torch.Tensor, qtype: str = "e4m3", scale: float | None = None) -> tuple[torch.Tensor, torch.Tensor]:
+    if not x.is_contiguous() and x.stride(-1) == 1 and x.shape[-1] >= 128:
+        try:  # strided rows (e.g. Q/K heads of a QKV view): read in place, no copy
+            return hadacore_fwht_quant_strided(x, qtype=qtype, scale=scale)
+        except HadacoreError:
+            pass  # more than two row dims or unsupported strides: fall through to a contiguous copy
     return hadacore_fwht_quant(x.contiguous(), qtype=qtype, scale=scale)
 
 

@@ -341,3 +341,11 @@ def test_c5_full_size_and_shard_invariance(hc):
         assert torch.equal(xs.view(torch.int16), x[lo:hi].view(torch.int16))   # generator keyed on global index
         ys = hc.hadacore_fwht(xs)
         assert torch.equal(ys.view(torch.int16), y[lo:hi].view(torch.int16))
+
+
+def test_torch_op_quant_on_strided_view(hc):
+    import paper_2412_08832_b200.torch_ops  # noqa: F401
+    qkv = synthetic.generate(7 * 3 * 4, 256, torch.bfloat16, 44).reshape(7, 3, 4, 256).cuda()
+    q, s = torch.ops.hadacore.fwht_quant(qkv[:, 0:2], "e4m3", None)
+    q2, s2 = hc.hadacore_fwht_quant(qkv[:, 0:2].contiguous(), "e4m3")
+    assert torch.equal(q.view(torch.uint8), q2.view(torch.uint8)) and torch.equal(s, s2)
