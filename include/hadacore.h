@@ -12,7 +12,7 @@
  * `scale` is the WHOLE multiplier on the +-1 matrix: pass 1/sqrt(n) for the
  * normalized (orthonormal) transform of P:41 ("+-1/sqrt(d) ... when normalized").
  * n is a power of two in [2^7, 2^15] (the paper's range, P:97, P:128 [Sec. 3.2]) or,
- * except for hadacore_fwht_strided, in [2, 2^6] (
+ * except for the strided entry points, in [2, 2^6] (
  * SPEC S:49's domain 2 <= d; fp32 register butterflies, DESIGN.md "Rows shorter
  * than 128").
  *
@@ -35,10 +35,11 @@
  * No C++ exception crosses this ABI.  There is no CPU fallback: without a usable
  * sm_100 device the call returns HADACORE_ERR_CUDA.
  *
- * Numerics: the internal precision is fp16 (for fp16 data) or fp32 accumulate
- * rounded to bf16 between factor stages (for bf16 data), the final factor stage is
- * accumulated in fp32, multiplied by `scale` (times an exact power of two) in fp32
- * and rounded to nearest even.  Rows are independent: a
+ * Numerics (n >= 128): the internal precision is fp16 (for fp16 data) or fp32
+ * accumulate rounded to bf16 between factor stages (for bf16 data), the final factor
+ * stage is accumulated in fp32, multiplied by `scale` (times an exact power of two) in
+ * fp32 and rounded to nearest even; n < 128 and the fp32 path
+ * compute in fp32 throughout with one final rounding.  Rows are independent: a
  * non-finite value in one row never affects another row.
  */
 #ifndef HADACORE_H_
