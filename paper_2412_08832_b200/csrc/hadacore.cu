@@ -69,11 +69,14 @@ template <> struct Tuned<32768> { static constexpr int nt = 16, tkb = 64, st = 3
 template <int N> struct TunedQ0     { static constexpr int nt = 8, tkb = 16, st = 3, u = 1, ctas = 3; };
 template <> struct TunedQ0<128>     { static constexpr int nt = 8, tkb = 32, st = 2, u = 1, ctas = 3; };
 template <> struct TunedQ0<256>     { static constexpr int nt = 8, tkb = 32, st = 2, u = 1, ctas = 3; };
-template <> struct TunedQ0<8192>    { static constexpr int nt = 8, tkb = 32, st = 3, u = 1, ctas = 2; };
+template <> struct TunedQ0<8192>    { static constexpr int nt = 8, tkb = 32, st = 3, u = 2, ctas = 2; };
 template <> struct TunedQ0<16384>   { static constexpr int nt = 8, tkb = 32, st = 3, u = 1, ctas = 2; };
 template <> struct TunedQ0<32768>   { static constexpr int nt = 16, tkb = 64, st = 3, u = 1, ctas = 1; };
 #ifdef HC_QTUNE  // A/B builds: HC_QTUNE_N = the n to override (0: every n in 512..8192)
-struct QMacro { static constexpr int nt = HC_QNT, tkb = HC_QTKB, st = HC_QST, u = 1, ctas = HC_QCTAS; };
+#ifndef HC_QU
+#define HC_QU 1
+#endif
+struct QMacro { static constexpr int nt = HC_QNT, tkb = HC_QTKB, st = HC_QST, u = HC_QU, ctas = HC_QCTAS; };
 template <int N>
 struct TunedQ : std::conditional_t<(HC_QTUNE_N == N || (HC_QTUNE_N == 0 && N >= 512 && N <= 8192)), QMacro,
                                    TunedQ0<N>> {};

@@ -7,6 +7,6 @@ d=json.loads(open('gpurun_out/ab.json').read().strip().splitlines()[-1]); print(
 "; }
 for v in "${@}"; do
   # v = "default" or "n:nt,tkb,st,ctas" (n = 0: every n in 512..8192)
-  if [ "$v" = "default" ]; then build ""; else qn=${v%%:*}; IFS=, read nt tkb st ct <<< "${v#*:}"; build "-DHC_QTUNE -DHC_QTUNE_N=$qn -DHC_QNT=$nt -DHC_QTKB=$tkb -DHC_QST=$st -DHC_QCTAS=$ct"; fi
+  if [ "$v" = "default" ]; then build ""; else qn=${v%%:*}; IFS=, read nt tkb st ct uu <<< "${v#*:}"; build "-DHC_QTUNE -DHC_QTUNE_N=$qn -DHC_QNT=$nt -DHC_QTKB=$tkb -DHC_QST=$st -DHC_QCTAS=$ct -DHC_QU=${uu:-1}"; fi
   run e4m3 "$v"
 done
