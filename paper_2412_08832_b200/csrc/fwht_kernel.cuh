@@ -364,6 +364,30 @@ __device__ __forceinline__ void stage_da_f32(const uint32_t x[4], const uint32_t
   mma_f32<DT>(x, bc0[0], bc0[1], d);      // output columns 0..7  -> regs R0 (rows g), R1 (rows g+8)
   mma_f32<DT>(x, bc1[0], bc1[1], d + 4);  // output columns 8..15 -> R2, R3
 }
+// Two chunk-bit groups at once (n >= 8192): H_16 over the A fragment's column bits as a
+// data-as-A stage (layout kept), then H_2 over the fragment's row-half bit (the ldmatrix
+// matrix index bit j0: d[0..1], d[4..5] are rows g, d[2..3], d[6..7] rows g + 8) as fp32
+// butterflies in registers -- 2 HMMA instead of two const-A stages (4 HMMA and a 16-bit
+// intermediate).  HC_J0_MMA builds keep the const-A pair for A/B.
+template <int DT>
+__device__ __forceinline__ void stage_da_j0_f32(const uint32_t x[4], const uint32_t bc0[2], const uint32_t bc1[2],
+                                                float d[8]) {
+  stage_da_f32<DT>(x, bc0, bc1, d);
+#pragma unroll
+  for (int h = 0; h < 8; h += 4)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const float p0 = d[h + e], p1 = d[h + 2 + e];
+      d[h + e] = p0 + p1;
+      d[h + 2 + e] = p0 - p1;
+    }
+}
+#ifdef HC_J0_MMA
+constexpr bool kJ0Mma = true;
+#else
+constexpr bool kJ0Mma = false;
+#endif
+
 // fp32 epilogue: * s_res (exact normalization remainder), one RNE rounding to 16 bits.
 template <int DT>
 __device__ __forceinline__ void scale_pack(const float d[8], float s_res, uint32_t y[4]) {
@@ -1163,13 +1187,15 @@ __global__ void __launch_bounds__((NT + 1) * 32, CTAS)
   uint32_t A256[4];
   make_const_a<DT>(0xFu, A256);
   uint32_t Pa[4], Pb[4], Bc0[2], Bc1[2];
-  if constexpr (PL::two_stage) {
+  if constexpr (PL::two_stage && kJ0Mma) {
     make_const_a<DT>(0xFu, Pa);  // H_16 over (r0, r1, r2, j1)
     make_const_a<DT>(0x8u, Pb);  // H_2 over j0 (x) I_8
   } else {
-    make_const_b<DT>(PL::mask_a, 0, Bc0);
+    make_const_b<DT>(PL::mask_a, 0, Bc0);  // two-stage (n >= 8192): j0 then by fp32 butterflies
     make_const_b<DT>(PL::mask_a, 1, Bc1);
   }
+  (void)Pa;
+  (void)Pb;
   // phase-2 slot bits of this lane (ldmatrix row address provider: lane = 8*j + r)
   const uint32_t r0 = lane & 1, r1 = (lane >> 1) & 1, r2 = (lane >> 2) & 1, j0 = (lane >> 3) & 1,
                  j1 = (lane >> 4) & 1;
@@ -1231,10 +1257,12 @@ __global__ void __launch_bounds__((NT + 1) * 32, CTAS)
           float dd[1 << PL::nx][8];
 #pragma unroll
           for (int xi = 0; xi < (1 << PL::nx); ++xi) {
-            if constexpr (PL::two_stage) {
+            if constexpr (PL::two_stage && kJ0Mma) {
               uint32_t y[4];
               stage_ca<DT>(Pa, x[u][xi][0], x[u][xi][2], x[u][xi][1], x[u][xi][3], y);
               stage_ca_f32<DT>(Pb, y[0], y[2], y[1], y[3], dd[xi]);
+            } else if constexpr (PL::two_stage) {
+              stage_da_j0_f32<DT>(x[u][xi], Bc0, Bc1, dd[xi]);
             } else {
               stage_da_f32<DT>(x[u][xi], Bc0, Bc1, dd[xi]);
             }
@@ -1404,10 +1432,12 @@ __global__ void __launch_bounds__((NT + 1) * 32, CTAS)
 #pragma unroll
           for (int e = 0; e < 8; ++e) d[xi][e] *= ldexpf(1.f, -stage_shift(PL::mask_a));
 #else
-          if constexpr (PL::two_stage) {
+          if constexpr (PL::two_stage && kJ0Mma) {
             uint32_t y[4];
             stage_ca<DT>(Pa, x[u][xi][0], x[u][xi][2], x[u][xi][1], x[u][xi][3], y);
             stage_ca_f32<DT>(Pb, y[0], y[2], y[1], y[3], d[xi]);
+          } else if constexpr (PL::two_stage) {
+            stage_da_j0_f32<DT>(x[u][xi], Bc0, Bc1, d[xi]);
           } else {
             stage_da_f32<DT>(x[u][xi], Bc0, Bc1, d[xi]);
           }
