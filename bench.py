@@ -62,6 +62,16 @@ def parse():
     return ap.parse_args()
 
 
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def measured_hbm_peak():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -226,6 +236,7 @@ def reference_arm(args, rank, world):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64 (oracle)",
         "data": "synthetic", "config": config_block(args, world),
         "cpu_baseline": {"value": round(gbs, 4), "unit": "GB/s", "cores": threads, "kind": "oracle",
+                         "cpu_model": cpu_model(),
                          "sample": f"{sample} elements per (dtype, n) per step = {sample // (1 << 20)}Mi of the "
                                    f"{args.elems >> 20}Mi-element C3 matrices, 18 (dtype, n) pairs; fp64 "
                                    "listing (oracle/fwht_oracle.c), widening excluded"},
@@ -604,6 +615,7 @@ def main():
             t, e, passes = t + dt_, e + de, passes + 1
         del inputs
         cpu_baseline = {"value": round(4.0 * e / t / 1e9, 4), "unit": "GB/s", "cores": threads, "kind": "oracle",
+                        "cpu_model": cpu_model(), "gel_per_s": round(e / t / 1e9, 4),
                         "sample": f"first {sample >> 20}Mi elements of each of the 18 (dtype, n) C3 inputs, "
                                   f"{passes} passes ({e} elements), fp64 listing, {t:.1f} s; widening excluded"}
 
