@@ -91,12 +91,19 @@ template <int N> struct TunedS {
   static constexpr int nt = 8, tkb = 32, st = 4, u = N <= 8 ? 4 : (N == 16 ? 2 : 1);
 };
 
+// Small problems (n <= 256, contiguous, <= 4 MiB: e.g. BASELINE C1, 1024 x 256 fp16):
+// launch-latency-bound, so tiles of 2 KiB spread the work over more SMs and shorten each
+// CTA's load -> compute -> store chain (C1: 1.93 -> 1.71 us per launch in a CUDA graph,
+// profiles/r01_ab_c1.txt).  Selected at run time as the QT_SMALLM instantiation.
+struct TunedSmallM { static constexpr int nt = 4, tkb = 2, st = 2, u = 1, ctas = 1; };
+constexpr int QT_SMALLM = -2;  // kernels treat every QT < 0 as the plain transform
+
 #ifdef HC_TUNE  // tools/tune.py: one configuration for every n, from -D macros
 template <int N, int QT>
 struct Knobs { static constexpr int nt = HC_NT, tkb = HC_TILE_KB, st = HC_STAGES, u = HC_U, ctas = HC_CTAS; };
 #else
 template <int N, int QT>
-struct Knobs : std::conditional_t<(QT >= 0), TunedQ<N>, Tuned<N>> {};
+struct Knobs : std::conditional_t<(QT >= 0), TunedQ<N>, std::conditional_t<(QT == QT_SMALLM), TunedSmallM, Tuned<N>>> {};
 #endif
 
 template <int N, int QT = -1>
@@ -223,6 +230,12 @@ bool ensure_smem_attr(Kern kern, int smem, std::atomic<uint64_t>& done, int dev)
 template <int N, int DT, int QT>
 hadacore_status_t launch(const void* in, void* out, uint8_t* out_q, float* row_scale, const Layout& L, float scale,
                          cudaStream_t stream) {
+#ifndef HC_TUNE
+  if constexpr (N <= 256 && QT == QT_NONE) {
+    if (L.m_inner == 1 && L.in_so == N && L.out_so == N && L.m_outer * N * 2 <= (int64_t(4) << 20))
+      return launch<N, DT, QT_SMALLM>(in, out, out_q, row_scale, L, scale, stream);
+  }
+#endif
   using C = Cfg<N, QT>;
   constexpr bool seg = seg_mode(N, C::rows);
   // + full[], done[][<=16] and the fused-quantization row-max scratch (one float per warp)
