@@ -47,16 +47,23 @@ int sm_count(int dev) {
 // Tuned per n on B200 in bench.py's launch sequence under CLC scheduling (paired
 // sweeps, profiles/r01_tune_sweep16_clc_retune.txt): compute warps, tile KiB, ring
 // stages, work items per warp in flight, CTAs per SM.
-template <int N> struct Tuned;
-template <> struct Tuned<128>   { static constexpr int nt = 16, tkb = 16, st = 4, u = 1, ctas = 1; };
-template <> struct Tuned<256>   { static constexpr int nt = 16, tkb = 16, st = 4, u = 1, ctas = 1; };
-template <> struct Tuned<512>   { static constexpr int nt = 16, tkb = 16, st = 4, u = 1, ctas = 1; };
-template <> struct Tuned<1024>  { static constexpr int nt = 16, tkb = 16, st = 4, u = 1, ctas = 1; };
-template <> struct Tuned<2048>  { static constexpr int nt = 16, tkb = 16, st = 4, u = 1, ctas = 1; };
-template <> struct Tuned<4096>  { static constexpr int nt = 16, tkb = 16, st = 4, u = 1, ctas = 1; };
-template <> struct Tuned<8192>  { static constexpr int nt = 16, tkb = 16, st = 6, u = 1, ctas = 1; };
-template <> struct Tuned<16384> { static constexpr int nt = 16, tkb = 64, st = 3, u = 1, ctas = 1; };
-template <> struct Tuned<32768> { static constexpr int nt = 16, tkb = 64, st = 3, u = 1, ctas = 1; };
+template <int N> struct Tuned0;
+template <> struct Tuned0<128>   { static constexpr int nt = 16, tkb = 16, st = 4, u = 1, ctas = 1; };
+template <> struct Tuned0<256>   { static constexpr int nt = 16, tkb = 16, st = 4, u = 1, ctas = 1; };
+template <> struct Tuned0<512>   { static constexpr int nt = 16, tkb = 16, st = 4, u = 1, ctas = 1; };
+template <> struct Tuned0<1024>  { static constexpr int nt = 16, tkb = 16, st = 4, u = 1, ctas = 1; };
+template <> struct Tuned0<2048>  { static constexpr int nt = 16, tkb = 16, st = 4, u = 1, ctas = 1; };
+template <> struct Tuned0<4096>  { static constexpr int nt = 16, tkb = 16, st = 4, u = 1, ctas = 1; };
+template <> struct Tuned0<8192>  { static constexpr int nt = 16, tkb = 16, st = 6, u = 1, ctas = 1; };
+template <> struct Tuned0<16384> { static constexpr int nt = 16, tkb = 32, st = 4, u = 1, ctas = 1; };  // r01_ab_transform_tune.txt
+template <> struct Tuned0<32768> { static constexpr int nt = 16, tkb = 64, st = 3, u = 1, ctas = 1; };
+
+#ifdef HC_TTUNE  // A/B builds: override the transform's table for n = HC_TTUNE_N
+struct TMacro { static constexpr int nt = HC_TNT, tkb = HC_TTKB, st = HC_TST, u = 1, ctas = HC_TCTAS; };
+template <int N> struct Tuned : std::conditional_t<(N == HC_TTUNE_N), TMacro, Tuned0<N>> {};
+#else
+template <int N> struct Tuned : Tuned0<N> {};
+#endif
 
 // Fused quantization (QT >= 0): its epilogue (row max, team barrier, code pass) makes
 // a tile's critical path longer, so more independent pipelines per SM win: 3 CTAs of

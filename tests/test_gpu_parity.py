@@ -21,8 +21,8 @@ NS = [1 << k for k in range(7, 16)]
 DTYPES = [torch.float16, torch.bfloat16]
 TOL = {torch.float16: 2e-3, torch.bfloat16: 1.6e-2}
 # rows per pipeline tile in the launch configuration (paper_2412_08832_b200/csrc/hadacore.cu Tuned<N>:
-# 16 KiB tiles of whole rows; 64 KiB tiles for n = 2^14, 2^15)
-TILE_ROWS = {128: 64, 256: 32, 512: 16, 1024: 8, 2048: 4, 4096: 2, 8192: 1, 16384: 2, 32768: 1}
+# 16 KiB tiles of whole rows; one row per tile for n = 2^14 (32 KiB) and 2^15 (64 KiB))
+TILE_ROWS = {128: 64, 256: 32, 512: 16, 1024: 8, 2048: 4, 4096: 2, 8192: 1, 16384: 1, 32768: 1}
 
 
 @pytest.fixture(scope="module")
