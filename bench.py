@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--impl", choices=["hadacore", "reference"], default="hadacore")
     ap.add_argument("--elems", type=int, default=ELEMS, help="elements per (n, dtype) launch per GPU")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--inplace", action="store_true",
+                    help="transform the resident input in place (P:264-274 App. B) instead of out of place")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--ns", default=None, help="comma-separated n list overriding the workload's sweep "
@@ -437,7 +439,7 @@ def main():
                                    stream=stream)
             return
         o = obuf.view(-1, n) if f32 else obuf.view(torch.int16).view(dt).view(-1, n)
-        hc.hadacore_fwht(x, out=o, stream=stream)
+        hc.hadacore_fwht(x, out=x if args.inplace else o, stream=stream)
 
     # warm-up
     for _ in range(args.warmup):
@@ -494,7 +496,7 @@ def main():
     # holds at any size) -- the normalized transform preserves every row's
     # norm; the worst relative norm error over all rows of every (dtype, n) launch, max over ranks
     check = None
-    if not quant and not rotate:
+    if not quant and not rotate and not args.inplace:
         worst, by_dt = 0.0, {}
         tol_of = {torch.float16: 2e-3, torch.bfloat16: 1.6e-2, torch.float32: 1e-5}
         for dt, n in pairs:
@@ -542,6 +544,10 @@ def main():
     if c5:  # strong scaling: the whole 2^33-element job per step, whatever the rank count
         total_bytes = 4.0 * C5_ELEMS * args.steps
     value = total_bytes / (t_max * 1e-3) / 1e9
+
+    # per-launch device times of the per-launch pass: p10 / p50 / p90
+    srt = sorted(per)
+    launch_pct = [round(1e3 * srt[int(q * (len(srt) - 1))], 2) for q in (0.1, 0.5, 0.9)] if srt else None
 
     # per-(dtype, n) breakdown and the roofline of the kernel (device time per launch)
     per_n = {}
@@ -648,7 +654,8 @@ def main():
             "pct_of_8TBps": round(100.0 * value / world / NOMINAL_HBM_GBS, 2),
             # north_star: "reported ... both as GB/s and elements/s" (whole job, all ranks)
             "elements_per_s": float(f"{(C5_ELEMS * args.steps if c5 else sum(elems_of[p] for p in pairs) * args.steps * world) / (t_max * 1e-3):.4g}"),
-            "per_n_GBps": per_n, "roofline": roofline, "cpu_baseline": cpu_baseline, "e2e": e2e,
+            "per_n_GBps": per_n, "launch_us_p10_p50_p90": launch_pct, "inplace": bool(args.inplace),
+            "roofline": roofline, "cpu_baseline": cpu_baseline, "e2e": e2e,
             "gpu_launches": int(args.steps * sum(hc.launches_per_call(elems_of[(dt, n)] // n, n, dt) for dt, n in pairs)),
             "clocks": clocks, "remeasured_for_clocks": remeasured, "check": check,
         }
