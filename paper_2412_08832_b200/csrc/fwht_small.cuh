@@ -300,8 +300,7 @@ __global__ void __launch_bounds__((NT + 1) * 32, 1)
             }
           }
         }
-        continue;
-      }
+      } else {
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int item = i0 + u * NT * 32;
@@ -322,6 +321,7 @@ __global__ void __launch_bounds__((NT + 1) * 32, 1)
             stg_sh128(p + 16 * (uint32_t(j) ^ c), w);
           }
         }
+      }
       }
     }
     fence_proxy_async_smem();  // this warp's smem writes -> visible to the bulk store
