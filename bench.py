@@ -417,7 +417,7 @@ def main():
         # fused QKV activations [T, 3, H, n] (H = max(1, 4096 / n) heads); the Q and K
         # heads are rotated in place through the strided entry (2 row dims: T x 2H)
         for dt in xin:
-            for n in NS:
+            for n in ns:
                 h = max(1, 4096 // n)
                 t = args.elems // (3 * h * n)
                 qk[(dt, n)] = xin[dt][: t * 3 * h * n].view(t, 3, h, n)[:, 0:2]
@@ -634,8 +634,6 @@ def main():
         if c5:
             metric = ("C5: FWHT HBM GB/s, bf16 n=2^15, 2^33 elements row-sharded across the GPUs "
                       "(whole-job bytes / max-over-ranks time; strong scaling)")
-        if args.ns:
-            metric = metric.replace("n=2^7..2^15", f"n in {{{args.ns}}}")
         if args.workload == "small":
             metric = "FWHT HBM GB/s vs n=2^1..2^6 (bf16/fp16), rows shorter than the paper's 2^7 (NEXT-2)"
         if qkq:
@@ -644,6 +642,8 @@ def main():
         elif rotate:
             metric = ("In-place FWHT of the Q and K heads of fused QKV activations [T, 3, H, n] (strided rows) "
                       "HBM GB/s vs n=2^7..2^15")
+        if args.ns:
+            metric = metric.replace("n=2^7..2^15", f"n in {{{args.ns}}}")
         line = {
             "metric": metric, "value": round(value, 1), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(t_max / args.steps, 4), "higher_is_better": True,

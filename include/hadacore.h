@@ -11,8 +11,9 @@
  * [Sec. 2.2]).  H_n is symmetric, so this equals the right multiply in * H_n.
  * `scale` is the WHOLE multiplier on the +-1 matrix: pass 1/sqrt(n) for the
  * normalized (orthonormal) transform of P:41 ("+-1/sqrt(d) ... when normalized").
- * n is a power of two in [2^7, 2^15] (the paper's range, P:97, P:128 [Sec. 3.2]) or,
- * except for the strided entry points, in [2, 2^6] (
+ * n is a power of two in [2^7, 2^15] (the paper's range, P:97, P:128 [Sec. 3.2]) or in
+ * [2, 2^6] (hadacore_fwht_strided: [8, 2^6]; not for
+ * hadacore_fwht_quant_strided;
  * SPEC S:49's domain 2 <= d; fp32 register butterflies, DESIGN.md "Rows shorter
  * than 128").
  *
@@ -123,7 +124,8 @@ hadacore_status_t hadacore_fwht_host(const void* in_host, void* out_host, int64_
  * may not overlap (stride_inner >= n when m_inner > 1; stride_outer >= (m_inner-1) *
  * stride_inner + n when m_outer > 1) -- else HADACORE_ERR_INVALID_M.  in == out
  * requires identical strides; otherwise the two extents may not overlap
- * (HADACORE_ERR_OVERLAP).  fp16/bf16 and n = 2^7..2^15 only.  Other rules as hadacore_fwht.
+ * (HADACORE_ERR_OVERLAP).  fp16/bf16 and n = 2^3..2^15 only (rows of >= 16 bytes: TMA
+ * boxes).  Other rules as hadacore_fwht.
  */
 hadacore_status_t hadacore_fwht_strided(const void* in, void* out, int64_t m_outer, int64_t m_inner,
                                         int64_t in_stride_outer, int64_t in_stride_inner,

@@ -241,7 +241,10 @@ def hadacore_fwht_strided(x: torch.Tensor, out: torch.Tensor | None = None, scal
         raise HadacoreError(3, "out must have x's shape and dtype and a contiguous last dimension")
 
     mo, mi, so, si = _row_grid(x, n)
-    mo2, mi2, oso, osi = _row_grid(out, n)
+    if out.is_contiguous():  # rows in (i, j) order: any grid maps onto it
+        mo2, mi2, oso, osi = mo, mi, mi * n, n
+    else:
+        mo2, mi2, oso, osi = _row_grid(out, n)
     if (mo2, mi2) != (mo, mi):
         raise HadacoreError(3, "out's row grid differs from x's")
     if scale is None:

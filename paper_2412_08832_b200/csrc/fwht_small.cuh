@@ -56,17 +56,22 @@ __device__ __forceinline__ void unpack2(uint32_t w, float& lo, float& hi) {
 // per lane in flight.
 // QT >= 0: fused per-row quantization (NEXT-1 for n < 128): a lane holds whole rows, so
 // the row max is in-lane; codes go straight from registers to out_q, scales to row_scale.
-template <int N, int DT, int TILE_BYTES, int STAGES, int NT, int U, int QT = QT_NONE>
+// GRID: rows on a 2-level grid (NEXT-3 row grids, n >= 8): a tile is a
+// bo x bi box of rows moved by 3-D TMA tensor copies (rows outside the grid are zero-filled
+// on load and clipped on store), instead of a contiguous byte range.
+template <int N, int DT, int TILE_BYTES, int STAGES, int NT, int U, int QT = QT_NONE, bool GRID = false>
 __global__ void __launch_bounds__((NT + 1) * 32, 1)
     fwht_small_kernel(const uint16_t* __restrict__ in, uint16_t* __restrict__ out, int64_t total_bytes,
                       int64_t num_tiles, float scale, uint8_t* __restrict__ out_q = nullptr,
-                      float* __restrict__ row_scale = nullptr) {
+                      float* __restrict__ row_scale = nullptr, const __grid_constant__ CUtensorMap tm_in = {},
+                      const __grid_constant__ CUtensorMap tm_out = {}, const RowGrid g = {}) {
   constexpr int K = log2_n<N>();
   constexpr int G = N >= 8 ? N / 8 : 1;            // granules per item
   constexpr int ITEM_BYTES = 16 * G;
   constexpr int KG = N >= 16 ? K - 3 : 0;          // granule bits of an item
   constexpr int KE = K < 3 ? K : 3;                // element bits inside a granule
   static_assert(TILE_BYTES % ITEM_BYTES == 0 && STAGES <= 16, "tile layout");
+  static_assert(!GRID || (N >= 8 && QT < 0), "row grids: n >= 8 (16-byte TMA rows), transform only");
 
   extern __shared__ __align__(1024) uint8_t smem[];
   SchedCtl* ctl = reinterpret_cast<SchedCtl*>(smem + STAGES * TILE_BYTES);
@@ -89,6 +94,7 @@ __global__ void __launch_bounds__((NT + 1) * 32, 1)
   // bytes of tile t, and its 16-byte-multiple prefix moved by the bulk engine (the
   // rest, < 16 bytes, exists only for n <= 4 and is handled by one consumer lane)
   auto tile_bytes = [&](int64_t t) -> int {
+    if constexpr (GRID) return int(total_bytes);  // GRID: total_bytes carries the (full) box size
     const int64_t left = total_bytes - t * TILE_BYTES;
     return int(left < TILE_BYTES ? left : TILE_BYTES);
   };
@@ -108,10 +114,19 @@ __global__ void __launch_bounds__((NT + 1) * 32, 1)
           return t + gridDim.x;
         }
       };
+      if constexpr (GRID) {
+        tma_prefetch(&tm_in);
+        tma_prefetch(&tm_out);
+      }
       auto load = [&](int st, int64_t t) {
         const uint32_t b16 = uint32_t(tile_bytes(t)) & ~15u;
         mbar_arrive_expect_tx(&full[st], b16);
-        if (b16) bulk_g2s(smem + st * TILE_BYTES, reinterpret_cast<const uint8_t*>(in) + t * TILE_BYTES, b16, &full[st], pol);
+        if constexpr (GRID) {
+          const TileRows tr(g, t);
+          tma_load_3d(smem + st * TILE_BYTES, &tm_in, 0, int(tr.j0), int(tr.i0), &full[st], pol);
+        } else {
+          if (b16) bulk_g2s(smem + st * TILE_BYTES, reinterpret_cast<const uint8_t*>(in) + t * TILE_BYTES, b16, &full[st], pol);
+        }
       };
       bool ended = false;
       for (int k = 0; k < STAGES; ++k) {  // fill the ring
@@ -132,7 +147,12 @@ __global__ void __launch_bounds__((NT + 1) * 32, 1)
         if (t < 0) break;
         mbar_wait(&done[s], (it / STAGES) & 1);
         const uint32_t b16 = uint32_t(tile_bytes(t)) & ~15u;
-        if (QT < 0 && b16) bulk_s2g(reinterpret_cast<uint8_t*>(out) + t * TILE_BYTES, smem + s * TILE_BYTES, b16);
+        if constexpr (GRID) {
+          const TileRows tr(g, t);  // rows outside the grid are clipped by the TMA unit
+          tma_store_3d(&tm_out, 0, int(tr.j0), int(tr.i0), smem + s * TILE_BYTES);
+        } else {
+          if (QT < 0 && b16) bulk_s2g(reinterpret_cast<uint8_t*>(out) + t * TILE_BYTES, smem + s * TILE_BYTES, b16);
+        }
         bulk_commit();
         if (ended) continue;
         if (tile < 0 || tile >= num_tiles) {
@@ -310,7 +330,9 @@ __global__ void __launch_bounds__((NT + 1) * 32, 1)
         for (int j = 0; j < G; ++j) {
           uint32_t w[4];
 #pragma unroll
-          for (int q = 0; q < 4; ++q) w[q] = pack2<DT>(v[u][8 * j + 2 * q] * sc[j], v[u][8 * j + 2 * q + 1] * sc[j]);
+          for (int q = 0; q < 4; ++q)  // fma with +0: an exact zero is +0 whatever the slot's sign (so the
+            w[q] = pack2<DT>(fmaf(v[u][8 * j + 2 * q], sc[j], 0.f),   // bits do not depend on the lane a row lands on)
+                             fmaf(v[u][8 * j + 2 * q + 1], sc[j], 0.f));
           if (N <= 4 && item * 16 + 16 > b16) {
             uint32_t* gdst = reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(out) + tile * TILE_BYTES + item * 16);
             const int nw = (bytes - item * 16) / 4;

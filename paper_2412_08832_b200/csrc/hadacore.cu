@@ -307,7 +307,46 @@ hadacore_status_t launch_small(const void* in, void* out, int64_t m, float scale
   const int64_t max_ctas = kClc ? int64_t(INT32_MAX) : int64_t(sm_count(dev));
   const int grid = int(tiles < max_ctas ? tiles : max_ctas);
   if (launch_pdl(kern, grid, (T::nt + 1) * 32, smem, stream, static_cast<const uint16_t*>(in),
-                 static_cast<uint16_t*>(out), total, tiles, scale, out_q, row_scale) != cudaSuccess)
+                 static_cast<uint16_t*>(out), total, tiles, scale, out_q, row_scale, CUtensorMap{}, CUtensorMap{},
+                 RowGrid{}) != cudaSuccess)
+    return HADACORE_ERR_CUDA;
+  return cudaPeekAtLastError() == cudaSuccess ? HADACORE_OK : HADACORE_ERR_CUDA;
+}
+
+// Row grids with n = 8..64 (hadacore_fwht_strided): 3-D TMA boxes (n, bi, bo) of up to one
+// 32 KiB stage; TMA box dims are capped at 256.
+template <int N, int DT>
+hadacore_status_t launch_small_grid(const void* in, void* out, const Layout& L, float scale, cudaStream_t stream) {
+  using T = TunedS<N>;
+  constexpr int tile = T::tkb * 1024;
+  constexpr int tile_rows = tile / (2 * N);
+  constexpr int smem = T::st * tile + int(sizeof(SchedCtl)) + 2 * T::st * 8;
+  static std::atomic<uint64_t> attr_done{0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return HADACORE_ERR_CUDA;
+  auto kern = fwht_small_kernel<N, DT, tile, T::st, T::nt, T::u, QT_NONE, true>;
+  if (!ensure_smem_attr(kern, smem, attr_done, dev)) return HADACORE_ERR_CUDA;
+  int bi = 1;
+  while (bi * 2 <= tile_rows && bi * 2 <= L.m_inner && bi * 2 <= 256) bi *= 2;
+  const int bo = tile_rows / bi < 256 ? tile_rows / bi : 256;
+  RowGrid g{};
+  g.m_outer = L.m_outer;
+  g.m_inner = L.m_inner;
+  g.out_so = L.out_so;
+  g.out_si = L.out_si;
+  while ((1 << g.lbi) < bi) ++g.lbi;
+  g.bo = bo;
+  g.nib = (L.m_inner + bi - 1) / bi;
+  g.num_tiles = ((L.m_outer + bo - 1) / bo) * g.nib;
+  CUtensorMap tin, tout;
+  if (!encode_small_map(&tin, in, L, L.in_so, L.in_si, N, g) || !encode_small_map(&tout, out, L, L.out_so, L.out_si, N, g))
+    return HADACORE_ERR_CUDA;
+  const int64_t box_bytes = int64_t(bi) * bo * 2 * N;
+  const int64_t max_ctas = kClc ? int64_t(INT32_MAX) : int64_t(sm_count(dev));
+  const int grid = int(g.num_tiles < max_ctas ? g.num_tiles : max_ctas);
+  if (launch_pdl(kern, grid, (T::nt + 1) * 32, smem, stream, static_cast<const uint16_t*>(in),
+                 static_cast<uint16_t*>(out), box_bytes, g.num_tiles, scale, static_cast<uint8_t*>(nullptr),
+                 static_cast<float*>(nullptr), tin, tout, g) != cudaSuccess)
     return HADACORE_ERR_CUDA;
   return cudaPeekAtLastError() == cudaSuccess ? HADACORE_OK : HADACORE_ERR_CUDA;
 }
@@ -542,8 +581,23 @@ hadacore_status_t run_quant(const void* in, uint8_t* q, float* rs, int64_t m, in
                                : run_quant_dt<DT_BF16>(in, q, rs, L, n, qtype, scale, st);
 }
 
+template <int DT>
+hadacore_status_t dispatch_small_grid(const void* in, void* out, const Layout& L, int64_t n, float scale,
+                                      cudaStream_t st) {
+  switch (n) {
+    case 8: return launch_small_grid<8, DT>(in, out, L, scale, st);
+    case 16: return launch_small_grid<16, DT>(in, out, L, scale, st);
+    case 32: return launch_small_grid<32, DT>(in, out, L, scale, st);
+    case 64: return launch_small_grid<64, DT>(in, out, L, scale, st);
+    default: return HADACORE_ERR_INVALID_N;
+  }
+}
+
 hadacore_status_t run_strided(const void* in, void* out, const Layout& L, int64_t n, int dtype, float scale,
                               cudaStream_t st) {
+  if (n < 128)
+    return dtype == HADACORE_F16 ? dispatch_small_grid<DT_F16>(in, out, L, n, scale, st)
+                                 : dispatch_small_grid<DT_BF16>(in, out, L, n, scale, st);
   return dtype == HADACORE_F16 ? dispatch_n<DT_F16, QT_NONE>(in, out, nullptr, nullptr, L, n, scale, st)
                                : dispatch_n<DT_BF16, QT_NONE>(in, out, nullptr, nullptr, L, n, scale, st);
 }
@@ -570,7 +624,7 @@ extern "C" hadacore_status_t hadacore_fwht_strided(const void* in, void* out, in
                                                    int64_t out_stride_outer, int64_t out_stride_inner, int64_t n,
                                                    hadacore_dtype_t dtype, float scale, hadacore_stream_t stream) {
   if (dtype != HADACORE_F16 && dtype != HADACORE_BF16) return HADACORE_ERR_DTYPE;
-  if (!valid_n_paper(n)) return HADACORE_ERR_INVALID_N;
+  if (!valid_n(n) || n < 8) return HADACORE_ERR_INVALID_N;  // row grids: rows of >= 16 bytes (TMA)
   if (m_outer < 0 || m_inner < 0 || m_outer > (int64_t(1) << 31) || m_inner > (int64_t(1) << 31))
     return HADACORE_ERR_INVALID_M;
   if (!std::isfinite(scale)) return HADACORE_ERR_SCALE;
@@ -778,7 +832,8 @@ extern "C" const char* hadacore_status_string(hadacore_status_t s) {
   switch (s) {
     case HADACORE_OK: return "ok";
     case HADACORE_ERR_INVALID_N:
-      return "n must be a power of two in [2, 32768] ([128, 32768] for the strided entry point)";
+      return "n must be a power of two in [2, 32768] ([8, 32768] for hadacore_fwht_strided, [128, 32768] for "
+             "hadacore_fwht_quant_strided)";
     case HADACORE_ERR_INVALID_M: return "m must be >= 0 and m*n*2 must fit in int64";
     case HADACORE_ERR_NULL: return "in/out must be non-NULL when m > 0";
     case HADACORE_ERR_MISALIGNED: return "in/out must be 16-byte aligned";

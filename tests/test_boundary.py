@@ -165,7 +165,8 @@ def test_strided_entry_validation(lib):
     assert f(a, b, 4, 3, 384, 64, 384, 128, 128, 0, 1.0, None) == INVALID_M         # inner rows overlap
     assert f(a, b, 4, 3, 256, 128, 384, 128, 128, 0, 1.0, None) == INVALID_M        # outer rows overlap
     assert f(a, b, 4, 3, 384, 128, 384, 128, 100, 0, 1.0, None) == INVALID_N
-    assert f(a, b, 4, 3, 384, 128, 384, 128, 64, 0, 1.0, None) == INVALID_N   # row grids: 2^7..2^15
+    assert f(a, b, 4, 3, 384, 128, 384, 128, 4, 0, 1.0, None) == INVALID_N    # row grids: n >= 8 (16-byte TMA rows)
+    assert f(a, b, 0, 3, 384, 128, 384, 128, 64, 0, 1.0, None) == OK          # n = 8..64 accepted (m_outer = 0)
     assert f(a, b, 4, 3, 384, 128, 384, 128, 128, 2, 1.0, None) == DTYPE            # fp32: contiguous API only
     assert f(a, a, 4, 3, 384, 128, 768, 128, 128, 0, 1.0, None) == OVERLAP          # in place needs equal strides
     assert f(a, a + 256, 4, 3, 384, 128, 384, 128, 128, 0, 1.0, None) == OVERLAP    # extents overlap

@@ -203,3 +203,32 @@ def test_full_size_sampled(hc, n, dtype):
         ny = y[r0:r0 + blk].float().norm(dim=1)
         worst = max(worst, ((ny - nx).abs() / nx).max().item())
     assert worst <= TOL[dtype]
+
+
+@pytest.mark.parametrize("dtype", DTYPES, ids=["fp16", "bf16"])
+@pytest.mark.parametrize("n,heads", [(8, 4), (16, 3), (32, 8), (64, 32), (64, 1), (64, 300)])
+def test_strided_qkv_heads_small_n(hc, n, heads, dtype):
+    """Row grids for n = 8..64 (3-D TMA boxes, box dims capped at 256): the Q and K heads of
+    [T, 3, H, d] rotated in place equal the contiguous transform bitwise; V untouched."""
+    tokens = max(3, (1 << 18) // (3 * heads * n)) + 1
+    qkv = synthetic.generate(tokens * 3 * heads, n, dtype, 31, dist="D1").reshape(tokens, 3, heads, n).cuda()
+    before = qkv.clone()
+    qk = qkv[:, 0:2]
+    hc.hadacore_fwht_strided(qk, out=qk)
+    y = hc.hadacore_fwht(before[:, 0:2].contiguous())
+    assert torch.equal(qkv[:, 0:2].contiguous().view(torch.int16), y.view(torch.int16))
+    assert torch.equal(qkv[:, 2].view(torch.int16), before[:, 2].view(torch.int16))
+    err = rel_l2_rows(widen(y.reshape(-1, n)), oracle.fwht(widen(before[:, 0:2].reshape(-1, n))))
+    assert err.max() <= TOL[dtype]
+
+
+@pytest.mark.parametrize("n", [8, 32, 64])
+def test_strided_padded_pitch_small_n(hc, n):
+    m, pitch = 1001, n + 8
+    base = synthetic.generate(m, pitch, torch.float16, 32).cuda()
+    x = base[:, :n]
+    y = hc.hadacore_fwht_strided(x)
+    assert torch.equal(y.view(torch.int16), hc.hadacore_fwht(x.contiguous()).view(torch.int16))
+    out_pad = torch.zeros(m, pitch, dtype=torch.float16, device="cuda")
+    hc.hadacore_fwht_strided(x, out=out_pad[:, :n])
+    assert torch.equal(out_pad[:, :n].view(torch.int16), y.view(torch.int16)) and not out_pad[:, n:].any()
