@@ -411,7 +411,7 @@ def main():
     qkq = args.workload == "qk-quant"  # Q/K heads rotated + FP8-quantized in one pass (FP8 attention)
     if qkq:
         qbuf = torch.empty(args.elems, dtype=torch.float8_e4m3fn, device=dev)
-        sbuf = torch.empty(args.elems // 128, dtype=torch.float32, device=dev)
+        sbuf = torch.empty(args.elems // min(ns), dtype=torch.float32, device=dev)
     qk = {}
     if rotate:
         # fused QKV activations [T, 3, H, n] (H = max(1, 4096 / n) heads); the Q and K

@@ -12,8 +12,7 @@
  * `scale` is the WHOLE multiplier on the +-1 matrix: pass 1/sqrt(n) for the
  * normalized (orthonormal) transform of P:41 ("+-1/sqrt(d) ... when normalized").
  * n is a power of two in [2^7, 2^15] (the paper's range, P:97, P:128 [Sec. 3.2]) or in
- * [2, 2^6] (hadacore_fwht_strided: [8, 2^6]; not for
- * hadacore_fwht_quant_strided;
+ * [2, 2^6] (the strided entry points: [8, 2^6];
  * SPEC S:49's domain 2 <= d; fp32 register butterflies, DESIGN.md "Rows shorter
  * than 128").
  *
@@ -182,7 +181,7 @@ hadacore_status_t hadacore_row_sq_error(const float* a, const float* b, double* 
  * out_q is [m_outer * m_inner, n] bytes ([.., n/2] for INT4), row_scale has
  * m_outer * m_inner floats -- e.g. the Q (or K) heads of a fused QKV projection
  * [tokens, 3, H, d] rotated and quantized to FP8 in one pass for FP8 attention
- * (P:24).  n = 2^7..2^15; stride rules as hadacore_fwht_strided; the input is
+ * (P:24).  n = 2^3..2^15; stride rules as hadacore_fwht_strided; the input is
  * not modified; none of the three ranges may overlap.
  */
 hadacore_status_t hadacore_fwht_quant_strided(const void* in, void* out_q, float* row_scale, int64_t m_outer,

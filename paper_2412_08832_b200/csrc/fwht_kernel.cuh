@@ -528,8 +528,8 @@ __device__ __forceinline__ bool quant_fast_range(float amax, float hi) {
 template <int QT>
 __device__ __forceinline__ uint32_t quant4_fast(float a, float b, float c, float d, float m) {
   if constexpr (QT == QT_E4M3) {
-    mul2(a, b, m);
-    mul2(c, d, m);
+    fma2(a, b, m, 0.f);  // + 0: an exact zero codes as +0 (0x00) whatever the multiplier's sign
+    fma2(c, d, m, 0.f);
     uint16_t lo, hi;
     asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(lo) : "f"(b), "f"(a));
     asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(hi) : "f"(d), "f"(c));

@@ -71,7 +71,7 @@ __global__ void __launch_bounds__((NT + 1) * 32, 1)
   constexpr int KG = N >= 16 ? K - 3 : 0;          // granule bits of an item
   constexpr int KE = K < 3 ? K : 3;                // element bits inside a granule
   static_assert(TILE_BYTES % ITEM_BYTES == 0 && STAGES <= 16, "tile layout");
-  static_assert(!GRID || (N >= 8 && QT < 0), "row grids: n >= 8 (16-byte TMA rows), transform only");
+  static_assert(!GRID || N >= 8, "row grids: n >= 8 (16-byte TMA rows)");
 
   extern __shared__ __align__(1024) uint8_t smem[];
   SchedCtl* ctl = reinterpret_cast<SchedCtl*>(smem + STAGES * TILE_BYTES);
@@ -258,7 +258,12 @@ __global__ void __launch_bounds__((NT + 1) * 32, 1)
         for (int u = 0; u < U; ++u) {
           const int item = i0 + u * NT * 32;
           if (item >= items) continue;
-          const int64_t el0 = (tile * TILE_BYTES + int64_t(item) * ITEM_BYTES) / 2;  // first element of the item
+          int64_t el0 = (tile * TILE_BYTES + int64_t(item) * ITEM_BYTES) / 2;  // first element of the item
+          if constexpr (GRID) {  // n >= 8: one row per item, at (i, j) of the grid; codes/scales in row order
+            int64_t gi = 0, gj = 0;
+            if (!TileRows(g, tile).at(g, item, gi, gj)) continue;
+            el0 = (gi * g.m_inner + gj) * N;
+          }
           float mul[RI], scr[RI];
           bool fast = true;
 #pragma unroll

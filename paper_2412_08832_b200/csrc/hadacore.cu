@@ -315,8 +315,9 @@ hadacore_status_t launch_small(const void* in, void* out, int64_t m, float scale
 
 // Row grids with n = 8..64 (hadacore_fwht_strided): 3-D TMA boxes (n, bi, bo) of up to one
 // 32 KiB stage; TMA box dims are capped at 256.
-template <int N, int DT>
-hadacore_status_t launch_small_grid(const void* in, void* out, const Layout& L, float scale, cudaStream_t stream) {
+template <int N, int DT, int QT = QT_NONE>
+hadacore_status_t launch_small_grid(const void* in, void* out, const Layout& L, float scale, cudaStream_t stream,
+                                    uint8_t* out_q = nullptr, float* row_scale = nullptr) {
   using T = TunedS<N>;
   constexpr int tile = T::tkb * 1024;
   constexpr int tile_rows = tile / (2 * N);
@@ -324,7 +325,7 @@ hadacore_status_t launch_small_grid(const void* in, void* out, const Layout& L, 
   static std::atomic<uint64_t> attr_done{0};
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return HADACORE_ERR_CUDA;
-  auto kern = fwht_small_kernel<N, DT, tile, T::st, T::nt, T::u, QT_NONE, true>;
+  auto kern = fwht_small_kernel<N, DT, tile, T::st, T::nt, T::u, QT, true>;
   if (!ensure_smem_attr(kern, smem, attr_done, dev)) return HADACORE_ERR_CUDA;
   int bi = 1;
   while (bi * 2 <= tile_rows && bi * 2 <= L.m_inner && bi * 2 <= 256) bi *= 2;
@@ -339,16 +340,29 @@ hadacore_status_t launch_small_grid(const void* in, void* out, const Layout& L, 
   g.nib = (L.m_inner + bi - 1) / bi;
   g.num_tiles = ((L.m_outer + bo - 1) / bo) * g.nib;
   CUtensorMap tin, tout;
-  if (!encode_small_map(&tin, in, L, L.in_so, L.in_si, N, g) || !encode_small_map(&tout, out, L, L.out_so, L.out_si, N, g))
+  if (!encode_small_map(&tin, in, L, L.in_so, L.in_si, N, g) ||
+      !encode_small_map(&tout, QT >= 0 ? in : out, L, QT >= 0 ? L.in_so : L.out_so, QT >= 0 ? L.in_si : L.out_si, N,
+                        g))  // the output map is unused when quantizing
     return HADACORE_ERR_CUDA;
   const int64_t box_bytes = int64_t(bi) * bo * 2 * N;
   const int64_t max_ctas = kClc ? int64_t(INT32_MAX) : int64_t(sm_count(dev));
   const int grid = int(g.num_tiles < max_ctas ? g.num_tiles : max_ctas);
   if (launch_pdl(kern, grid, (T::nt + 1) * 32, smem, stream, static_cast<const uint16_t*>(in),
-                 static_cast<uint16_t*>(out), box_bytes, g.num_tiles, scale, static_cast<uint8_t*>(nullptr),
-                 static_cast<float*>(nullptr), tin, tout, g) != cudaSuccess)
+                 static_cast<uint16_t*>(out), box_bytes, g.num_tiles, scale, out_q, row_scale, tin, tout, g) != cudaSuccess)
     return HADACORE_ERR_CUDA;
   return cudaPeekAtLastError() == cudaSuccess ? HADACORE_OK : HADACORE_ERR_CUDA;
+}
+
+template <int DT, int QT = QT_NONE>
+hadacore_status_t dispatch_small_grid(const void* in, void* out, const Layout& L, int64_t n, float scale,
+                                      cudaStream_t st, uint8_t* q = nullptr, float* rs = nullptr) {
+  switch (n) {
+    case 8: return launch_small_grid<8, DT, QT>(in, out, L, scale, st, q, rs);
+    case 16: return launch_small_grid<16, DT, QT>(in, out, L, scale, st, q, rs);
+    case 32: return launch_small_grid<32, DT, QT>(in, out, L, scale, st, q, rs);
+    case 64: return launch_small_grid<64, DT, QT>(in, out, L, scale, st, q, rs);
+    default: return HADACORE_ERR_INVALID_N;
+  }
 }
 
 template <int DT, int QT = QT_NONE>
@@ -387,7 +401,6 @@ Layout contiguous(int64_t m, int64_t n) { return Layout{m, 1, n, n, n, n}; }
 // hadacore_fwht / hadacore_fwht_host: n = 2..2^15 (n < 128: NEXT-2, fwht_small_kernel);
 // the strided and fused-quantization entry points: the paper's range 2^7..2^15.
 bool valid_n(int64_t n) { return n >= 2 && n <= 32768 && (n & (n - 1)) == 0; }
-bool valid_n_paper(int64_t n) { return n >= 128 && n <= 32768 && (n & (n - 1)) == 0; }
 
 size_t elem_size(int dtype) { return dtype == HADACORE_F32 ? 4 : 2; }
 
@@ -560,6 +573,13 @@ hadacore_status_t run(const void* in, void* out, int64_t m, int64_t n, int dtype
 template <int DT>
 hadacore_status_t run_quant_dt(const void* in, uint8_t* q, float* rs, const Layout& L, int64_t n, int qtype,
                                float scale, cudaStream_t st) {
+  if (n < 128 && !(L.m_inner == 1 && L.in_so == n)) {  // rows shorter than 128 on a row grid
+    switch (qtype) {
+      case HADACORE_Q_E4M3: return dispatch_small_grid<DT, QT_E4M3>(in, nullptr, L, n, scale, st, q, rs);
+      case HADACORE_Q_INT8: return dispatch_small_grid<DT, QT_INT8>(in, nullptr, L, n, scale, st, q, rs);
+      default: return dispatch_small_grid<DT, QT_INT4>(in, nullptr, L, n, scale, st, q, rs);
+    }
+  }
   if (n < 128) {  // rows shorter than 128 (fwht_small_kernel's fused epilogue)
     switch (qtype) {
       case HADACORE_Q_E4M3: return dispatch_small<DT, QT_E4M3>(in, nullptr, L.m_outer, n, scale, st, q, rs);
@@ -579,18 +599,6 @@ hadacore_status_t run_quant(const void* in, uint8_t* q, float* rs, int64_t m, in
   const Layout L = contiguous(m, n);
   return dtype == HADACORE_F16 ? run_quant_dt<DT_F16>(in, q, rs, L, n, qtype, scale, st)
                                : run_quant_dt<DT_BF16>(in, q, rs, L, n, qtype, scale, st);
-}
-
-template <int DT>
-hadacore_status_t dispatch_small_grid(const void* in, void* out, const Layout& L, int64_t n, float scale,
-                                      cudaStream_t st) {
-  switch (n) {
-    case 8: return launch_small_grid<8, DT>(in, out, L, scale, st);
-    case 16: return launch_small_grid<16, DT>(in, out, L, scale, st);
-    case 32: return launch_small_grid<32, DT>(in, out, L, scale, st);
-    case 64: return launch_small_grid<64, DT>(in, out, L, scale, st);
-    default: return HADACORE_ERR_INVALID_N;
-  }
 }
 
 hadacore_status_t run_strided(const void* in, void* out, const Layout& L, int64_t n, int dtype, float scale,
@@ -657,7 +665,7 @@ extern "C" hadacore_status_t hadacore_fwht_quant_strided(const void* in, void* o
                                                          hadacore_stream_t stream) {
   if (qtype != HADACORE_Q_E4M3 && qtype != HADACORE_Q_INT8 && qtype != HADACORE_Q_INT4) return HADACORE_ERR_DTYPE;
   if (dtype != HADACORE_F16 && dtype != HADACORE_BF16) return HADACORE_ERR_DTYPE;
-  if (!valid_n_paper(n)) return HADACORE_ERR_INVALID_N;
+  if (!valid_n(n) || n < 8) return HADACORE_ERR_INVALID_N;  // row grids: rows of >= 16 bytes (TMA)
   if (m_outer < 0 || m_inner < 0 || m_outer > (int64_t(1) << 31) || m_inner > (int64_t(1) << 31))
     return HADACORE_ERR_INVALID_M;
   if (!std::isfinite(scale)) return HADACORE_ERR_SCALE;
@@ -832,8 +840,7 @@ extern "C" const char* hadacore_status_string(hadacore_status_t s) {
   switch (s) {
     case HADACORE_OK: return "ok";
     case HADACORE_ERR_INVALID_N:
-      return "n must be a power of two in [2, 32768] ([8, 32768] for hadacore_fwht_strided, [128, 32768] for "
-             "hadacore_fwht_quant_strided)";
+      return "n must be a power of two in [2, 32768] ([8, 32768] for the strided entry points)";
     case HADACORE_ERR_INVALID_M: return "m must be >= 0 and m*n*2 must fit in int64";
     case HADACORE_ERR_NULL: return "in/out must be non-NULL when m > 0";
     case HADACORE_ERR_MISALIGNED: return "in/out must be 16-byte aligned";

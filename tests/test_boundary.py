@@ -201,7 +201,7 @@ def test_quant_strided_entry_validation(lib):
     f = lib.hadacore_fwht_quant_strided
     assert f(a, q, rs, 4, 3, 384, 128, 128, 0, 3, 1.0, None) == DTYPE        # qtype
     assert f(a, q, rs, 4, 3, 384, 128, 128, 2, 0, 1.0, None) == DTYPE        # fp32 input
-    assert f(a, q, rs, 4, 3, 384, 128, 64, 0, 0, 1.0, None) == INVALID_N     # 2^7..2^15 only
+    assert f(a, q, rs, 4, 3, 384, 128, 4, 0, 0, 1.0, None) == INVALID_N      # n >= 8 (16-byte TMA rows)
     assert f(a, q, rs, 4, 3, 384, 64, 128, 0, 0, 1.0, None) == INVALID_M     # inner rows overlap
     assert f(a, q, rs, 4, 3, 384, 128, 128, 0, 0, float("inf"), None) == SCALE
     assert f(a, None, rs, 4, 3, 384, 128, 128, 0, 0, 1.0, None) == NULL

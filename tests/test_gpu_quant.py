@@ -231,7 +231,8 @@ def test_small_n_quant_unaligned_row_scale(hc):
 
 
 @pytest.mark.parametrize("qtype", QTYPES)
-@pytest.mark.parametrize("n,heads", [(128, 32), (128, 3), (256, 8), (1024, 5), (4096, 2), (32768, 1)])
+@pytest.mark.parametrize("n,heads", [(8, 4), (16, 3), (32, 8), (64, 32), (64, 300), (128, 32), (128, 3), (256, 8),
+                                     (1024, 5), (4096, 2), (32768, 1)])
 def test_quant_strided_qk_heads(hc, n, heads, qtype):
     """FP8-attention deployment path: the Q and K heads of a fused QKV
     projection [T, 3, H, d] rotated + quantized in one pass (hadacore_fwht_quant_strided)
