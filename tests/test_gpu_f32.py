@@ -122,3 +122,14 @@ def test_f32_pair_kernel_repeatability_stress(hc):
     hc.hadacore_fwht(xi, out=xi)
     assert torch.equal(xi, ref)
     assert rel_l2_rows(widen(ref[:8]), oracle.fwht(widen(x[:8]))).max() <= TOL
+
+
+@pytest.mark.parametrize("n", [2, 1024, 32768])
+def test_f32_host_entry(hc, n):
+    """hadacore_fwht_host with fp32 buffers (slots of >= 16 bytes for n = 2) equals the device entry bitwise."""
+    m = max(3, (1 << 20) // n) + 1
+    x = synthetic.generate(m, n, torch.float32, 17).pin_memory()
+    ws = torch.empty(1 << 20, dtype=torch.uint8, device="cuda")
+    y_host = hc.hadacore_fwht_host(x, workspace=ws)
+    y_dev = hc.hadacore_fwht(x.cuda()).cpu()
+    assert torch.equal(y_host, y_dev)
