@@ -247,3 +247,16 @@ def test_quant_strided_qk_heads(hc, n, heads, qtype):
     q2, s2 = hc.hadacore_fwht_quant(view.contiguous(), qtype=qtype)
     assert q.shape == q2.shape and s.shape == s2.shape == (tokens, 2, heads)
     assert torch.equal(q.view(torch.uint8), q2.view(torch.uint8)) and torch.equal(s, s2)
+
+
+@pytest.mark.parametrize("qtype", QTYPES)
+@pytest.mark.parametrize("n", [16, 64, 256, 2048])
+def test_quant_strided_padded_pitch(hc, n, qtype):
+    """Rows with a padded pitch (m_inner = 1, stride_outer = n + 64): codes and scales equal the
+    contiguous entry's on a copy, bitwise."""
+    m, pitch = 777, n + 64
+    base = synthetic.generate(m, pitch, torch.float16, 35, dist="D1").cuda()
+    x = base[:, :n]
+    q, s = hc.hadacore_fwht_quant_strided(x, qtype=qtype)
+    q2, s2 = hc.hadacore_fwht_quant(x.contiguous(), qtype=qtype)
+    assert torch.equal(q.view(torch.uint8), q2.view(torch.uint8)) and torch.equal(s, s2)
