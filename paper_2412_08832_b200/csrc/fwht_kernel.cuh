@@ -209,6 +209,9 @@ __device__ __forceinline__ void stg_sh128(uint8_t* p, const uint32_t v[4]) {
   *reinterpret_cast<uint4*>(p) = make_uint4(v[0], v[1], v[2], v[3]);
 }
 __device__ __forceinline__ void stg32(uint16_t* p, uint32_t v) { *reinterpret_cast<uint32_t*>(p) = v; }
+#ifndef HC_QPACK_N
+#define HC_QPACK_N 0  // fused quantization: the n whose phase-B results are held as packed 16-bit y
+#endif
 // HC_STORE_HINT (A/B builds): output stores marked evict-first in L2 (st.global.cs and the
 // TMA store's L2::cache_hint), like the input loads
 #ifndef HC_STORE_HINT
@@ -1241,6 +1244,9 @@ __global__ void __launch_bounds__((NT + 1) * 32, CTAS)
     // from registers (coalesced STG.64 / STG.32) -- no 16-bit image, no second pass over
     // shared memory, and the stage is released to the producer right after phase B.
     constexpr int IW = ITEMS1 / P;  // phase-B chunks per warp per tile
+    // PK: keep the phase-B results as packed 16-bit y (RNE16(d * s_res), half the registers) so
+    // that more CTAs fit per SM (HC_QPACK_N = the n that uses it); codes then come from y16
+    constexpr bool PK = (N == HC_QPACK_N);
     static_assert(ITEMS1 % P == 0, "phase-B split");
     const float q_qs = copysignf(qmax_of<QT>(), s_res);  // code multiplier numerator (sign folded)
     const float q_ss = fabsf(s_res) / qmax_of<QT>();     // row scale per unit of max |d|
@@ -1303,8 +1309,9 @@ __global__ void __launch_bounds__((NT + 1) * 32, CTAS)
       }
       team_sync();  // P:126 "Sync across the threadblock"
 
-      // ---- phase B: H_256 per chunk, fp32 results kept in registers
-      float d[IW][8];
+      // ---- phase B: H_256 per chunk, results kept in registers
+      float d[PK ? 1 : IW][8];
+      uint32_t dp[PK ? IW : 1][4];
       float am[RPT];
 #pragma unroll
       for (int k = 0; k < RPT; ++k) am[k] = 0.f;
@@ -1312,12 +1319,14 @@ __global__ void __launch_bounds__((NT + 1) * 32, CTAS)
       for (int k = 0; k < IW; ++k) {
         const int item = wt + k * P, rl = item / C, r = team + NTEAMS * rl, c = item % C;
         uint32_t x[4], y[4];
+        float* dk = d[PK ? 0 : k];
         lds128(tb + r * ROW_BYTES + gofs<C>(uint32_t(c), uint32_t(lane)), x[0], x[1], x[2], x[3]);
         stage_ca<DT>(A256, x[0], x[2], x[1], x[3], y);
-        stage_ca_f32<DT>(A256, y[0], y[2], y[1], y[3], d[k]);
+        stage_ca_f32<DT>(A256, y[0], y[2], y[1], y[3], dk);
         float a = 0.f;
 #pragma unroll
-        for (int e = 0; e < 8; ++e) a = absmax_nan(a, d[k][e]);
+        for (int e = 0; e < 8; ++e) a = absmax_nan(a, dk[e]);
+        if constexpr (PK) scale_pack<DT>(dk, s_res, dp[k]);
 #pragma unroll
         for (int kk = 0; kk < RPT; ++kk)
           if (kk == rl) am[kk] = absmax_nan(am[kk], a);
@@ -1345,12 +1354,12 @@ __global__ void __launch_bounds__((NT + 1) * 32, CTAS)
         float sc;
         if (quant_fast_range(a, 0x1p100f)) {
           sc = a * q_ss;
-          mul_r[k] = q_qs * rcp_ftz(a);
+          mul_r[k] = PK ? qmax_of<QT>() * rcp_ftz(a * fabsf(s_res)) : q_qs * rcp_ftz(a);  // PK: per unit of y
           fast_r |= 1u << k;
         } else {
           float inv;
           row_scale_of<QT>(a * fabsf(s_res), sc, inv);
-          mul_r[k] = s_res * inv;
+          mul_r[k] = PK ? inv : s_res * inv;
         }
         int64_t i = 0, j = 0;
         const bool ok = tr.at(g, team + NTEAMS * k, i, j);
@@ -1369,7 +1378,9 @@ __global__ void __launch_bounds__((NT + 1) * 32, CTAS)
             mul = mul_r[kk];
             qp = q_r[kk];
           }
-        const float* v = d[k];
+        float vv[8];
+        if constexpr (PK) unpack8<DT>(dp[k], vv);  // y16 (an overflowed fp16 y is +-Inf: codes saturate to +-Q)
+        const float* v = PK ? vv : d[PK ? 0 : k];
         uint32_t c0, c1;
         if ((fast_r >> rl) & 1u) {
           c0 = quant4_fast<QT>(v[0], v[1], v[2], v[3], mul);
