@@ -1,11 +1,14 @@
 // fwht_kernel.cuh -- sm_100a kernel for the batched normalized Walsh-Hadamard
 // transform (HadaCore, arXiv 2412.08832).  "P:NN" = /root/reference/PAPER.md line.
 //
-// Design (DESIGN.md "Kernel"):
-//  * Persistent CTAs; one producer warp streams row tiles HBM -> shared memory with
-//    cp.async.bulk (TMA bulk copy, SASS UBLKCP) into a STAGES-deep mbarrier ring, so
-//    tens of KB per SM are always in flight.  Every element is read once and written
-//    once (P:264 in-place allowed: tiles are disjoint and read before written).
+// Design (DESIGN.md §5):
+//  * Warp-specialized CTAs scheduled by cluster launch control (one CTA per tile; resident
+//    CTAs cancel not-yet-launched ones and take their tiles).  One producer warp streams
+//    row tiles HBM -> shared memory into a STAGES-deep mbarrier ring -- 1-D bulk copies
+//    (SASS UBLKCP) for contiguous n <= 256, 3-D/5-D TMA tensor copies (UTMALDG) for row
+//    grids and n >= 512 -- and, for n >= 512, stores finished tiles back with TMA tensor
+//    stores (UTMASTG).  Every element is read once and written once (P:264 in place:
+//    tiles are disjoint and read before written).
 //  * The Kronecker factors H_16 (x) ... (P:150 [Sec. 3.4]) are contractions on the
 //    tensor cores with register operands (mma.sync m16n8k16, SASS HMMA), as in the
 //    paper's Sec. 3: a 256-element fragment lives in one warp, 8 elements per
@@ -13,11 +16,13 @@
 //    CONSTANT in the A operand and the data in the B operand makes each stage return
 //    D = K * X^T, i.e. the transpose comes free, and two such stages give
 //    K_b * X * K_a in natural orientation (P:109's "transpose, H16, transpose back").
-//  * Rows longer than 256 (P:120-129 [Sec. 3.2]): phase 1 applies H_256 to every
-//    256-chunk, writes it back to shared memory with a per-chunk XOR swizzle of the
-//    32-bit word index, phase 2 gathers fragments across chunks (bank-conflict free
-//    because of the swizzle) and applies H_{n/256} (residual 2^a factors as
-//    H_2^a (x) I blocks, P:146 [Sec. 3.3]), phase 3 un-swizzles and stores.
+//  * Rows longer than 256 (P:120-129 [Sec. 3.2]): the TMA box lays each row out with the
+//    hardware 128-byte swizzle; phase 1 applies H_256 to every 256-chunk in place, phase
+//    2 gathers fragments across chunks with ldmatrix/stmatrix .trans (bank-conflict free
+//    because of the swizzle) and applies H_{n/256} (residual 2^a factors as H_2^a (x) I
+//    blocks, P:146 [Sec. 3.3]); the TMA store un-swizzles.  With fused quantization the
+//    two factors run in the other order (they commute) so that H_256 comes last and its
+//    fp32 results stay in registers until the row maximum is known.
 //  * Normalization: every stage multiplies by an exact power of two
 //    (+-2^-floor(h/2) entries); the last stage accumulates in fp32 and multiplies by
 //    s_res = scale * 2^E before the single round-to-nearest-even to 16 bits.
