@@ -39,11 +39,12 @@ int sm_count(int dev) {
   return v;
 }
 
-// Per-n launch configuration.  One persistent
-// CTA per SM: NT compute warps + 1 producer warp, a STAGES-deep ring of tiles of
-// ~TILE_KB KiB (whole rows; one 64 KiB row for n = 2^15), rows split into teams of
-// P warps (n > 256) that synchronise with named barriers.  The HC_* macros let
-// tools/tune.py build variants; the defaults are the tuned values.
+// Per-n launch configuration.  A CTA = NT compute
+// warps + 1 producer warp, a STAGES-deep ring of tiles of ~TILE_KB KiB (whole rows;
+// one row per tile for n = 2^14, 2^15), rows split into teams of P warps (n > 256)
+// that synchronise with named barriers; the grid has one CTA per tile and CTAs steal
+// tiles through cluster launch control.  The HC_* macros let tools/*.sh build A/B
+// variants; the defaults are the tuned values.
 // Tuned per n on B200 in bench.py's launch sequence under CLC scheduling (paired
 // sweeps, profiles/r01_tune_sweep16_clc_retune.txt): compute warps, tile KiB, ring
 // stages, work items per warp in flight, CTAs per SM.
