@@ -10,3 +10,6 @@ for q in e4m3 int8 int4; do
 done
 python bench.py > gpurun_out/final/fwht.json 2> gpurun_out/final/fwht.err
 python bench.py --impl reference --steps 2 --warmup 3 > gpurun_out/final/reference.json 2> gpurun_out/final/reference.err
+timeout 300 python bench.py --workload qk-rotate --ns 8,16,32,64 --no-e2e --no-cpu-baseline > gpurun_out/final/qk-rotate-small-n.json 2>/dev/null
+timeout 300 python bench.py --workload qk-quant --ns 8,16,32,64 --no-e2e --no-cpu-baseline > gpurun_out/final/qk-quant-small-n.json 2>/dev/null
+timeout 300 python bench.py --inplace --no-e2e --no-cpu-baseline > gpurun_out/final/fwht_inplace.json 2>/dev/null
