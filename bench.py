@@ -55,7 +55,7 @@ def parse():
     ap.add_argument("--ns", default=None, help="comma-separated n list overriding the workload's sweep "
                                                "(e.g. --workload quant-e4m3 --ns 2,4,8,16,32,64)")
     ap.add_argument("--workload", choices=["fwht", "quant-e4m3", "quant-int8", "quant-int4", "qk-rotate", "qk-quant", "small", "f32", "c5",
-                             "c1"], default="fwht",
+                             "c1", "lab"], default="fwht",
                     help="fwht = the metric's C3 sweep (default); quant-* = the fused FWHT + per-row "
                          "quantization row (NEXT-1) on the same inputs; small = n=2^1..2^6 (NEXT-2); "
                          "f32 = the fp32 path over n=2^1..2^15 (NEXT-2); c5 = BASELINE config C5: bf16 "
@@ -343,6 +343,30 @@ def run_c1(args, rank, world, dist):
             "gpu_launches": int(args.steps * R), "cpu_baseline": None, "e2e": None}
 
 
+def run_lab(args, rank, world):
+    """NEXT-4 quantization lab (SPEC quant_lab): rotated vs plain per-row INT4 error on the SPEC's
+    default outlier matrices (64 x 1024, rate 1e-3 x 100 sigma), 100 trials -- every step on the GPU
+    (hadacore_fwht fp32 rotations, hadacore_fake_quant, hadacore_row_sq_error)."""
+    import torch
+    from paper_2412_08832_b200 import quant_lab
+    spec = quant_lab.OutlierSpec(rows=64, cols=1024, outlier_rate=1e-3, outlier_scale=100.0, seed=1 + rank)
+    for _ in range(max(1, args.warmup)):
+        quant_lab.run_experiment(spec, "int4", "row", trials=5)
+    torch.cuda.synchronize()
+    rep = quant_lab.run_experiment(spec, "int4", "row", trials=100)
+    a = rep["aggregate"]
+    if rank != 0:
+        return None
+    return {"metric": "INT4 per-row quantization MSE, rotated / plain (SPEC quant_lab outlier matrices, 100 trials)",
+            "value": round(a["mse_rotated"] / a["mse_plain"], 4), "unit": "ratio", "n_gpus": world, "steps": 100,
+            "warmup": args.warmup, "ms_per_step": round(1e3 * rep["seconds"] / 100, 3), "higher_is_better": False,
+            "scaling": "weak", "vs_baseline": None, "dtype": "fp32 rotations, INT4 codes", "data": "synthetic OutlierSpec",
+            "config": {"workload": "NEXT-4 lab: 64 x 1024 fp32, outlier rate 1e-3, scale 100, INT4 per row"},
+            "win_rate": a["win_rate"], "mse_plain": a["mse_plain"], "mse_rotated": a["mse_rotated"],
+            "max_abs_plain": a["max_abs_plain"], "max_abs_rotated": a["max_abs_rotated"],
+            "roofline": None, "cpu_baseline": None, "e2e": None, "gpu_launches": None}
+
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -355,8 +379,8 @@ def main():
         return
     import torch
     rank, world, local, dist = dist_setup(args)
-    if args.workload == "c1":
-        line = run_c1(args, rank, world, dist)
+    if args.workload in ("c1", "lab"):
+        line = run_c1(args, rank, world, dist) if args.workload == "c1" else run_lab(args, rank, world)
         if line is not None:
             print(json.dumps(line), flush=True)
         if dist is not None:
