@@ -747,6 +747,30 @@ struct TileRows {
     return i < g.m_outer && j < g.m_inner;
   }
 };
+// The same per tile, with the epilogue's per-row work reduced to 32-bit tests and one
+// wide multiply-add: rows (r >> lbi, r & mask) of the box are valid below (ni, nj), and
+// row r's linear index (i * m_inner + j: codes/scales) and output element offset
+// (i * out_so + j * out_si) are bases plus small multiples.
+struct TileRowsFast {
+  int64_t lin0, off0;  // i0 * m_inner + j0, i0 * out_so + j0 * out_si
+  int ni, nj, lbi;
+  __device__ __forceinline__ TileRowsFast(const RowGrid& g, int64_t tile) : lbi(g.lbi) {
+    const int64_t ob = tile / g.nib, ib = tile - ob * g.nib;
+    const int64_t i0 = ob * g.bo, j0 = ib << g.lbi;
+    lin0 = i0 * g.m_inner + j0;
+    off0 = i0 * g.out_so + j0 * g.out_si;
+    const int64_t ri = g.m_outer - i0, rj = g.m_inner - j0;
+    ni = int(ri < g.bo ? ri : g.bo);
+    nj = int(rj < (int64_t(1) << g.lbi) ? rj : (int64_t(1) << g.lbi));
+  }
+  __device__ __forceinline__ bool valid(int r) const { return (r >> lbi) < ni && (r & ((1 << lbi) - 1)) < nj; }
+  __device__ __forceinline__ int64_t lin(const RowGrid& g, int r) const {
+    return lin0 + int64_t(r >> lbi) * g.m_inner + (r & ((1 << lbi) - 1));
+  }
+  __device__ __forceinline__ int64_t off(const RowGrid& g, int r) const {
+    return off0 + int64_t(r >> lbi) * g.out_so + int64_t(r & ((1 << lbi) - 1)) * g.out_si;
+  }
+};
 
 // ------------------------------------------------------------------ kernel
 // Template parameters: N (row length), DT (dtype), TILE_ROWS (rows per pipeline
@@ -842,6 +866,8 @@ __global__ void __launch_bounds__((NT + 1) * 32, CTAS)
       const int64_t tile = ctl->stage_tile[s];
       if (tile < 0) break;
       const TileRows tr(g, tile);
+      const TileRowsFast trf(g, tile);
+      (void)trf;
       const int64_t left = g.m_outer - tr.i0;
       const int rows_left = left < TILE_ROWS ? int(left) : TILE_ROWS;  // FLAT only
       const uint8_t* tb = smem + s * TILE_BYTES;
@@ -898,9 +924,8 @@ __global__ void __launch_bounds__((NT + 1) * 32, CTAS)
                 const float mul = s_res * inv;
                 code = quant4<QT>(v[0] * mul, v[1] * mul, v[2] * mul, v[3] * mul);
               }
-              int64_t i = 0, j = 0;
-              const bool ok = FLAT ? 2 * f + h < rows_left : tr.at(g, 2 * f + h, i, j);
-              const int64_t row = FLAT ? tr.i0 + 2 * f + h : i * g.m_inner + j;  // codes/scales: contiguous [rows, n]
+              const bool ok = FLAT ? 2 * f + h < rows_left : trf.valid(2 * f + h);
+              const int64_t row = FLAT ? tr.i0 + 2 * f + h : trf.lin(g, 2 * f + h);  // codes/scales: contiguous [rows, n]
               if constexpr (QT == QT_INT4) {
                 stg16_if(out_q + row * (N / 2) + lane * 2, code, ok);
               } else {
@@ -914,9 +939,8 @@ __global__ void __launch_bounds__((NT + 1) * 32, CTAS)
               if (2 * f < rows_left) stg64(o, z[u][0], z[u][1]);
               if (2 * f + 1 < rows_left) stg64(o + N, z[u][2], z[u][3]);
             } else {
-              int64_t i, j;
-              if (tr.at(g, 2 * f, i, j)) stg64(out + i * g.out_so + j * g.out_si + lane * 4, z[u][0], z[u][1]);
-              if (tr.at(g, 2 * f + 1, i, j)) stg64(out + i * g.out_so + j * g.out_si + lane * 4, z[u][2], z[u][3]);
+              if (trf.valid(2 * f)) stg64(out + trf.off(g, 2 * f) + lane * 4, z[u][0], z[u][1]);
+              if (trf.valid(2 * f + 1)) stg64(out + trf.off(g, 2 * f + 1) + lane * 4, z[u][2], z[u][3]);
             }
           }
         }
@@ -935,6 +959,8 @@ __global__ void __launch_bounds__((NT + 1) * 32, CTAS)
       const int64_t tile = ctl->stage_tile[s];
       if (tile < 0) break;
       const TileRows tr(g, tile);
+      const TileRowsFast trf(g, tile);
+      (void)trf;
       const int64_t left = g.m_outer - tr.i0;
       const int rows_left = left < TILE_ROWS ? int(left) : TILE_ROWS;  // FLAT only
       const uint8_t* tb = smem + s * TILE_BYTES;
@@ -978,9 +1004,8 @@ __global__ void __launch_bounds__((NT + 1) * 32, CTAS)
               c0 = quant4<QT>(v[0] * mul, v[1] * mul, v[2] * mul, v[3] * mul);
               c1 = quant4<QT>(v[4] * mul, v[5] * mul, v[6] * mul, v[7] * mul);
             }
-            int64_t i = 0, j = 0;
-            const bool ok = FLAT ? r < rows_left : tr.at(g, r, i, j);
-            const int64_t row = FLAT ? tr.i0 + r : i * g.m_inner + j;
+            const bool ok = FLAT ? r < rows_left : trf.valid(r);
+            const int64_t row = FLAT ? tr.i0 + r : trf.lin(g, r);
             if constexpr (QT == QT_INT4) {
               stg32_if(out_q + row * (N / 2) + lane * 4, __byte_perm(c0, c1, 0x5410), ok);
             } else {
@@ -991,9 +1016,7 @@ __global__ void __launch_bounds__((NT + 1) * 32, CTAS)
             if constexpr (FLAT) {
               if (r < rows_left) stg128(out + (tr.i0 + r) * N + lane * 8, z[u][0], z[u][1], z[u][2], z[u][3]);
             } else {
-              int64_t i, j;
-              if (tr.at(g, r, i, j))
-                stg128(out + i * g.out_so + j * g.out_si + lane * 8, z[u][0], z[u][1], z[u][2], z[u][3]);
+              if (trf.valid(r)) stg128(out + trf.off(g, r) + lane * 8, z[u][0], z[u][1], z[u][2], z[u][3]);
             }
           }
         }
