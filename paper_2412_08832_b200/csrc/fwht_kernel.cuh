@@ -731,6 +731,11 @@ struct RowGrid {
   // valid rows instead of the 3-D tensor box, whose 256-byte box rows (n = 128)
   // measured 6-9 % slower (profiles/r01_ab_strided.txt)
   const uint16_t* flat_in;
+  // non-null when the inner rows are contiguous (stride_inner = n, e.g. the Q and K heads
+  // of a token): fwht_kernel then loads each of a tile's bo outer row blocks with one 1-D
+  // bulk copy of its valid rows (row r = ob * bi + jj of the tile) instead of a 3-D box
+  const uint16_t* rows_in;
+  int64_t in_so;
 };
 struct TileRows {
   int64_t i0, j0;
@@ -765,7 +770,8 @@ struct TileRowsFast {
   }
   __device__ __forceinline__ bool valid(int r) const { return (r >> lbi) < ni && (r & ((1 << lbi) - 1)) < nj; }
   __device__ __forceinline__ int64_t lin(const RowGrid& g, int r) const {
-    return lin0 + int64_t(r >> lbi) * g.m_inner + (r & ((1 << lbi) - 1));
+    // m_inner <= 2^31 (validated): one 32 x 32 -> 64-bit multiply-add (IMAD.WIDE.U32)
+    return lin0 + int64_t(uint64_t(uint32_t(r >> lbi)) * uint32_t(g.m_inner)) + (r & ((1 << lbi) - 1));
   }
   __device__ __forceinline__ int64_t off(const RowGrid& g, int r) const {
     return off0 + int64_t(r >> lbi) * g.out_so + int64_t(r & ((1 << lbi) - 1)) * g.out_si;
@@ -810,7 +816,7 @@ __global__ void __launch_bounds__((NT + 1) * 32, CTAS)
   if (warp == NT) {
     // ---------------- producer: TMA loads (3-D row-grid box) of row tiles into the ring
     if (lane == 0) {
-      if (!FLAT) tma_prefetch(&tm_in);
+      if (!FLAT && g.rows_in == nullptr) tma_prefetch(&tm_in);
       pdl_wait();  // the previous kernel on the stream has completed; all our global traffic follows this
       const uint64_t pol = policy_evict_first();
       uint32_t clc_phase = 0;
@@ -832,6 +838,16 @@ __global__ void __launch_bounds__((NT + 1) * 32, CTAS)
           const uint32_t bytes = uint32_t(rem < TILE_ROWS ? rem : TILE_ROWS) * ROW_BYTES;
           mbar_arrive_expect_tx(&full[s], bytes);
           bulk_g2s(smem + s * TILE_BYTES, g.flat_in + tr.i0 * N, bytes, &full[s], pol);
+        } else if (g.rows_in != nullptr) {
+          // rows outside the grid are not loaded: their (stale) slots are computed but never stored
+          const int bi = 1 << g.lbi;
+          const int64_t rj = g.m_inner - tr.j0, ri = g.m_outer - tr.i0;
+          const int nj = int(rj < bi ? rj : bi), ni = int(ri < g.bo ? ri : g.bo);
+          const uint32_t blk = uint32_t(nj) * ROW_BYTES;
+          mbar_arrive_expect_tx(&full[s], blk * uint32_t(ni));
+          for (int ob = 0; ob < ni; ++ob)
+            bulk_g2s(smem + s * TILE_BYTES + ob * bi * ROW_BYTES, g.rows_in + (tr.i0 + ob) * g.in_so + tr.j0 * N, blk,
+                     &full[s], pol);
         } else {
           mbar_arrive_expect_tx(&full[s], TILE_BYTES);  // full box; rows outside the grid are zero-filled
           tma_load_3d(smem + s * TILE_BYTES, &tm_in, 0, int(tr.j0), int(tr.i0), &full[s], pol);

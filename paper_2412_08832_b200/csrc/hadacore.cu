@@ -271,6 +271,9 @@ hadacore_status_t launch(const void* in, void* out, uint8_t* out_q, float* row_s
     CUtensorMap tin{};
     if (flat) {
       gs.flat_in = static_cast<const uint16_t*>(in);
+    } else if (L.in_si == N || L.m_inner == 1) {  // inner rows contiguous: per-outer-block bulk copies
+      gs.rows_in = static_cast<const uint16_t*>(in);
+      gs.in_so = L.in_so;
     } else if (!encode_small_map(&tin, in, L, L.in_so, L.in_si, N, g)) {
       return HADACORE_ERR_CUDA;
     }
