@@ -22,7 +22,7 @@ import os
 
 import torch
 
-__all__ = ["hadacore_fwht", "hadacore_fwht_host", "hadacore_fwht_quant", "hadacore_fwht_strided", "fwht", "HadacoreError",
+__all__ = ["ARG_ERROR", "hadacore_fwht", "hadacore_fwht_host", "hadacore_fwht_quant", "hadacore_fwht_strided", "fwht", "HadacoreError",
            "library_path", "version", "launches_per_call", "STATUS", "QTYPES", "fake_quant", "row_sq_error",
            "hadacore_fwht_quant_strided"]
 
@@ -30,7 +30,9 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_HERE, "libhadacore.so")
 _lib = None
 
+ARG_ERROR = -1  # Python-side argument check (tensor shape / dtype / device / layout mismatch), not a C status
 STATUS = {
+    ARG_ERROR: "PYTHON_ARGUMENT",
     0: "HADACORE_OK", 1: "HADACORE_ERR_INVALID_N", 2: "HADACORE_ERR_INVALID_M", 3: "HADACORE_ERR_NULL",
     4: "HADACORE_ERR_MISALIGNED", 5: "HADACORE_ERR_OVERLAP", 6: "HADACORE_ERR_DTYPE",
     7: "HADACORE_ERR_SCALE", 8: "HADACORE_ERR_CUDA", 9: "HADACORE_ERR_WORKSPACE",
@@ -104,7 +106,7 @@ def _shape(x: torch.Tensor):
     if x.dtype not in _DTYPES:
         raise HadacoreError(6, f"dtype {x.dtype} (expected float16, bfloat16 or float32)")
     if x.dim() < 1:
-        raise HadacoreError(1, "need at least one dimension")
+        raise HadacoreError(ARG_ERROR, "need at least one dimension")
     n = x.shape[-1]
     m = x.numel() // n if n else 0
     return m, n
@@ -119,13 +121,13 @@ def hadacore_fwht(x: torch.Tensor, out: torch.Tensor | None = None, scale: float
     """
     m, n = _shape(x)
     if not x.is_cuda:
-        raise HadacoreError(8, "x must be a CUDA tensor (use hadacore_fwht_host for host buffers)")
+        raise HadacoreError(ARG_ERROR, "x must be a CUDA tensor (use hadacore_fwht_host for host buffers)")
     if not x.is_contiguous():
-        raise HadacoreError(4, "x must be contiguous (row pitch = n)")
+        raise HadacoreError(ARG_ERROR, "x must be contiguous (row pitch = n; strided views: hadacore_fwht_strided)")
     if out is None:
         out = torch.empty_like(x)
     elif out.shape != x.shape or out.dtype != x.dtype or out.device != x.device or not out.is_contiguous():
-        raise HadacoreError(3, "out must be a contiguous tensor with x's shape, dtype and device")
+        raise HadacoreError(ARG_ERROR, "out must be a contiguous tensor with x's shape, dtype and device")
     if scale is None:
         scale = 1.0 / math.sqrt(n) if n > 0 else 1.0
     with torch.cuda.device(x.device):
@@ -149,11 +151,11 @@ def hadacore_fwht_host(x: torch.Tensor, out: torch.Tensor | None = None, scale: 
     """
     m, n = _shape(x)
     if x.is_cuda or not x.is_contiguous():
-        raise HadacoreError(3, "x must be a contiguous CPU tensor")
+        raise HadacoreError(ARG_ERROR, "x must be a contiguous CPU tensor")
     if out is None:
         out = torch.empty_like(x, pin_memory=x.is_pinned())
     elif out.is_cuda or out.shape != x.shape or out.dtype != x.dtype or not out.is_contiguous():
-        raise HadacoreError(3, "out must be a contiguous CPU tensor with x's shape and dtype")
+        raise HadacoreError(ARG_ERROR, "out must be a contiguous CPU tensor with x's shape and dtype")
     dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
     if workspace is None:
         es = x.element_size()
@@ -185,16 +187,16 @@ def hadacore_fwht_quant(x: torch.Tensor, qtype: str = "e4m3", scale: float | Non
     if x.dtype == torch.float32:
         raise HadacoreError(6, "the fused quantization takes float16/bfloat16 inputs")
     if not x.is_cuda or not x.is_contiguous():
-        raise HadacoreError(8, "x must be a contiguous CUDA tensor")
+        raise HadacoreError(ARG_ERROR, "x must be a contiguous CUDA tensor")
     qshape = x.shape if qtype != "int4" else (*x.shape[:-1], n // 2)
     if out is None:
         out = torch.empty(qshape, dtype=qdt, device=x.device)
     if row_scale is None:
         row_scale = torch.empty(x.shape[:-1], dtype=torch.float32, device=x.device)
     if out.dtype != qdt or tuple(out.shape) != tuple(qshape) or not out.is_contiguous() or out.device != x.device:
-        raise HadacoreError(3, f"out must be a contiguous {qdt} tensor of shape {tuple(qshape)} on x's device")
+        raise HadacoreError(ARG_ERROR, f"out must be a contiguous {qdt} tensor of shape {tuple(qshape)} on x's device")
     if row_scale.dtype != torch.float32 or row_scale.numel() != m or not row_scale.is_contiguous():
-        raise HadacoreError(3, "row_scale must be a contiguous float32 tensor with one entry per row")
+        raise HadacoreError(ARG_ERROR, "row_scale must be a contiguous float32 tensor with one entry per row")
     if scale is None:
         scale = 1.0 / math.sqrt(n) if n > 0 else 1.0
     with torch.cuda.device(x.device):
@@ -215,7 +217,7 @@ def _row_grid(t: torch.Tensor, n: int):
         else:
             merged.append((size, st))
     if len(merged) > 2:
-        raise HadacoreError(2, "more than two non-collapsible row dimensions")
+        raise HadacoreError(ARG_ERROR, "more than two non-collapsible row dimensions")
     while len(merged) < 2:
         merged.insert(0, (1, n * (merged[0][0] if merged else 1)))
     (mo, so), (mi, si) = merged
@@ -234,11 +236,11 @@ def hadacore_fwht_strided(x: torch.Tensor, out: torch.Tensor | None = None, scal
     """
     m, n = _shape(x)
     if not x.is_cuda or x.stride(-1) != 1:
-        raise HadacoreError(4, "x must be a CUDA view with a contiguous last dimension")
+        raise HadacoreError(ARG_ERROR, "x must be a CUDA view with a contiguous last dimension")
     if out is None:
         out = torch.empty(x.shape, dtype=x.dtype, device=x.device)
     if out.shape != x.shape or out.dtype != x.dtype or out.stride(-1) != 1:
-        raise HadacoreError(3, "out must have x's shape and dtype and a contiguous last dimension")
+        raise HadacoreError(ARG_ERROR, "out must have x's shape and dtype and a contiguous last dimension")
 
     mo, mi, so, si = _row_grid(x, n)
     if out.is_contiguous():  # rows in (i, j) order: any grid maps onto it
@@ -246,7 +248,7 @@ def hadacore_fwht_strided(x: torch.Tensor, out: torch.Tensor | None = None, scal
     else:
         mo2, mi2, oso, osi = _row_grid(out, n)
     if (mo2, mi2) != (mo, mi):
-        raise HadacoreError(3, "out's row grid differs from x's")
+        raise HadacoreError(ARG_ERROR, "out's row grid differs from x's")
     if scale is None:
         scale = 1.0 / math.sqrt(n) if n > 0 else 1.0
     with torch.cuda.device(x.device):
@@ -267,7 +269,7 @@ def fake_quant(x: torch.Tensor, qtype: str = "int4", per_tensor: bool = False, o
     if qtype not in LAB_QTYPES:
         raise HadacoreError(6, f"qtype {qtype!r} (expected one of {sorted(LAB_QTYPES)})")
     if x.dtype != torch.float32 or not x.is_cuda or not x.is_contiguous():
-        raise HadacoreError(6, "x must be a contiguous float32 CUDA tensor")
+        raise HadacoreError(ARG_ERROR, "x must be a contiguous float32 CUDA tensor")
     if out is None:
         out = torch.empty_like(x)
     amax = torch.empty(max(m, 1), dtype=torch.float32, device=x.device)
@@ -283,7 +285,7 @@ def row_sq_error(a: torch.Tensor, b: torch.Tensor, stream: torch.cuda.Stream | N
     m, n = _shape(a)
     if a.shape != b.shape or a.dtype != torch.float32 or b.dtype != torch.float32 or not (a.is_cuda and b.is_cuda) \
             or not (a.is_contiguous() and b.is_contiguous()):
-        raise HadacoreError(3, "a, b must be contiguous float32 CUDA tensors of one shape")
+        raise HadacoreError(ARG_ERROR, "a, b must be contiguous float32 CUDA tensors of one shape")
     out = torch.empty(max(m, 1), dtype=torch.float64, device=a.device)
     with torch.cuda.device(a.device):
         st = stream if stream is not None else torch.cuda.current_stream(a.device)
@@ -302,15 +304,15 @@ def hadacore_fwht_quant_strided(x: torch.Tensor, qtype: str = "e4m3", scale: flo
     if qtype not in QTYPES:
         raise HadacoreError(6, f"qtype {qtype!r} (expected one of {sorted(QTYPES)})")
     if not x.is_cuda or x.stride(-1) != 1:
-        raise HadacoreError(4, "x must be a CUDA view with a contiguous last dimension")
+        raise HadacoreError(ARG_ERROR, "x must be a CUDA view with a contiguous last dimension")
     code, qdt = QTYPES[qtype]
     qshape = (*x.shape[:-1], n // 2 if qtype == "int4" else n)
     q = out if out is not None else torch.empty(qshape, dtype=qdt, device=x.device)
     rs = row_scale if row_scale is not None else torch.empty(x.shape[:-1], dtype=torch.float32, device=x.device)
     if q.dtype != qdt or q.numel() != m * qshape[-1] or not q.is_contiguous() or q.device != x.device:
-        raise HadacoreError(3, f"out must be a contiguous {qdt} tensor of {m * qshape[-1]} elements on x's device")
+        raise HadacoreError(ARG_ERROR, f"out must be a contiguous {qdt} tensor of {m * qshape[-1]} elements on x's device")
     if rs.dtype != torch.float32 or rs.numel() != m or not rs.is_contiguous():
-        raise HadacoreError(3, "row_scale must be a contiguous float32 tensor with one entry per row")
+        raise HadacoreError(ARG_ERROR, "row_scale must be a contiguous float32 tensor with one entry per row")
     mo, mi, so, si = _row_grid(x, n)
     if scale is None:
         scale = 1.0 / math.sqrt(n) if n > 0 else 1.0
