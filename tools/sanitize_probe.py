@@ -22,6 +22,15 @@ for dt in (torch.float16, torch.bfloat16):
                 hc.hadacore_fwht_quant(y, q)
     qkv = torch.randn(5, 3, 4, 128, device=dev).to(dt)
     hc.hadacore_fwht_strided(qkv[:, 0:2], out=qkv[:, 0:2])
+for dt in (torch.float16, torch.bfloat16):  # row grids n = 8..64 (GRID small kernel), quantized grids, small-n quant
+    for n in (8, 16, 64, 128, 1024):
+        qkv = torch.randn(7, 3, 5, n, device=dev).to(dt)
+        hc.hadacore_fwht_strided(qkv[:, 0:2], out=qkv[:, 0:2])
+        for q in ("e4m3", "int8", "int4"):
+            hc.hadacore_fwht_quant_strided(qkv[:, 0:2], q)
+    for n, m in ((2, 7), (4, 5), (8, 3), (64, 33)):
+        for q in ("e4m3", "int8", "int4"):
+            hc.hadacore_fwht_quant(torch.randn(m, n, device=dev).to(dt), q)
 for n, m in ((2, 5), (64, 9), (2048, 3), (16384, 2), (32768, 3)):
     x = torch.randn(m, n, device=dev)
     hc.hadacore_fwht(x)
