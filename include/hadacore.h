@@ -72,8 +72,8 @@ typedef enum {
 
 typedef enum {
   HADACORE_OK = 0,
-  HADACORE_ERR_INVALID_N = 1,   /* n is not a power of two in [2, 32768] ([128, 32768] for the
-                                   strided entry point) */
+  HADACORE_ERR_INVALID_N = 1,   /* n is not a power of two in [2, 32768] ([8, 32768] for the
+                                   strided entry points) */
   HADACORE_ERR_INVALID_M = 2,   /* m < 0, or m * n * element size overflows int64 */
   HADACORE_ERR_NULL = 3,        /* in or out is NULL while m > 0 */
   HADACORE_ERR_MISALIGNED = 4,  /* in or out is not 16-byte aligned */
