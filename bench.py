@@ -262,23 +262,37 @@ def config_block(args, world):
     if getattr(args, "ns", None):
         ns = [int(v) for v in args.ns.split(",")]
         wl = f"{getattr(args, 'workload', 'fwht')} over n in {ns} (--ns), 2^28 elements per (n, dtype) per GPU"
-    if getattr(args, "workload", "fwht") == "small":
+    if getattr(args, "workload", "fwht") == "small" and not getattr(args, "ns", None):
         wl = ("NEXT-2 small sizes: n=2^1..2^6 x {fp16, bf16}, 2^28 elements per (n, dtype) per GPU, "
               "out-of-place, normalized (scale=1/sqrt(n))")
-    if getattr(args, "workload", "fwht") == "qk-rotate":
-        wl = ("QK rotation: n=2^7..2^15 x {fp16, bf16}; a 2^28-element QKV buffer viewed as [T, 3, H, n], "
+    w = getattr(args, "workload", "fwht")
+    if w.startswith("quant-") and not getattr(args, "ns", None):
+        wl = (f"NEXT-1 fused FWHT + per-row {w[6:].upper()} quantization: n=2^7..2^15 x {{fp16, bf16}}, 2^28 "
+              "elements per (n, dtype) per GPU, codes + fp32 row scales out, normalized (scale=1/sqrt(n))")
+    nrange = f"n in {ns}" if getattr(args, "ns", None) else "n=2^7..2^15"
+    if w == "qk-rotate":
+        wl = (f"QK rotation: {nrange} x {{fp16, bf16}}; a 2^28-element QKV buffer viewed as [T, 3, H, n], "
               "H = max(1, 4096/n); the Q and K heads (2/3 of it) transformed in place, normalized")
-    if getattr(args, "workload", "fwht") == "qk-quant":
-        wl = ("QK rotation + FP8-E4M3 quantization: n=2^7..2^15 x {fp16, bf16}; a 2^28-element QKV buffer viewed "
+    if w == "qk-quant":
+        wl = (f"QK rotation + FP8-E4M3 quantization: {nrange} x {{fp16, bf16}}; a 2^28-element QKV buffer viewed "
               "as [T, 3, H, n], H = max(1, 4096/n); the Q and K heads read strided, codes and row scales written "
               "contiguously (hadacore_fwht_quant_strided), normalized")
+    mib_in = args.elems * (4 if w == "f32" else 2) >> 20
+    if w == "c5":
+        l2 = "no flush: each rank's launch reads 16/N GiB and writes 16/N GiB (> 126 MB L2)"
+    elif w in ("qk-rotate", "qk-quant"):
+        l2 = (f"no flush: every launch reads the {mib_in * 2 // 3} MiB of Q and K heads (> 126 MB L2) and writes "
+              + ("them back in place" if w == "qk-rotate" else f"{args.elems * 2 // 3 >> 20} MiB of codes"))
+    elif w.startswith("quant-"):
+        codes = args.elems // (2 if w == "quant-int4" else 1) >> 20
+        l2 = f"no flush: every launch reads a {mib_in} MiB input and writes {codes} MiB of codes (> 126 MB L2)"
+    else:
+        l2 = f"no flush: every launch reads a {mib_in} MiB input and writes a {mib_in} MiB output (> 126 MB L2)"
     return {"workload": wl,
             "elements_per_launch": args.elems, "ns": ns,
-            "dtypes": {"f32": ["fp32"], "c5": ["bf16"]}.get(getattr(args, "workload", "fwht"), ["fp16", "bf16"]),
-            "launches_per_step": (1 if getattr(args, "workload", "fwht") in ("f32", "c5") else 2) * len(ns), "path": getattr(args, "workload", "fwht"),
-            "l2": ("no flush: each rank's launch reads 16/N GiB and writes 16/N GiB (> 126 MB L2)"
-                   if getattr(args, "workload", "fwht") == "c5" else
-                   "no flush: every launch reads a 512 MiB input and writes a 512 MiB output (> 126 MB L2)"),
+            "dtypes": {"f32": ["fp32"], "c5": ["bf16"]}.get(w, ["fp16", "bf16"]),
+            "launches_per_step": (1 if w in ("f32", "c5") else 2) * len(ns), "path": w,
+            "l2": l2,
             "parallelism": f"row-sharded x{world}, no collective on the hot path" if world > 1 else "single GPU"}
 
 
