@@ -98,6 +98,22 @@ template <int N> struct TunedQ : TunedQ0<N> {};
 template <int N> struct TunedS {
   static constexpr int nt = 8, tkb = 32, st = 4, u = N <= 8 ? 4 : (N == 16 ? 2 : 1);
 };
+// The same kernel with the fused quantization epilogue (codes straight from registers):
+// one item per lane in flight (U = 1) and, for n <= 8, 16 consumer warps (paired sweep,
+// profiles/r01_ab_small_quant.txt: n = 2..32 from 3.1-5.7 to 5.6-6.6 TB/s).
+// HC_SQTUNE = "n: nt,tkb,st,u" overrides it (A/B builds, tools/ab_small_quant.sh; n = 0: every n).
+template <int N> struct TunedSQ0 { static constexpr int nt = 8, tkb = 32, st = 4, u = 1; };
+template <> struct TunedSQ0<2> { static constexpr int nt = 16, tkb = 16, st = 4, u = 1; };
+template <> struct TunedSQ0<4> { static constexpr int nt = 16, tkb = 16, st = 4, u = 1; };
+template <> struct TunedSQ0<8> { static constexpr int nt = 16, tkb = 32, st = 4, u = 1; };
+template <> struct TunedSQ0<16> { static constexpr int nt = 8, tkb = 16, st = 4, u = 1; };
+template <> struct TunedSQ0<32> { static constexpr int nt = 8, tkb = 16, st = 4, u = 1; };
+#ifdef HC_SQTUNE
+struct SQMacro { static constexpr int nt = HC_SQNT, tkb = HC_SQTKB, st = HC_SQST, u = HC_SQU; };
+template <int N> struct TunedSQ : std::conditional_t<(HC_SQTUNE_N == N || HC_SQTUNE_N == 0), SQMacro, TunedSQ0<N>> {};
+#else
+template <int N> struct TunedSQ : TunedSQ0<N> {};
+#endif
 
 // Small problems (n <= 256, contiguous, <= 4 MiB: e.g. BASELINE C1, 1024 x 256 fp16):
 // launch-latency-bound, so tiles of 2 KiB spread the work over more SMs and shorten each
@@ -298,7 +314,7 @@ hadacore_status_t launch(const void* in, void* out, uint8_t* out_q, float* row_s
 template <int N, int DT, int QT = QT_NONE>
 hadacore_status_t launch_small(const void* in, void* out, int64_t m, float scale, cudaStream_t stream,
                                uint8_t* out_q = nullptr, float* row_scale = nullptr) {
-  using T = TunedS<N>;
+  using T = std::conditional_t<(QT >= 0), TunedSQ<N>, TunedS<N>>;
   constexpr int tile = T::tkb * 1024;
   constexpr int smem = T::st * tile + int(sizeof(SchedCtl)) + 2 * T::st * 8;
   static std::atomic<uint64_t> attr_done{0};
@@ -322,7 +338,7 @@ hadacore_status_t launch_small(const void* in, void* out, int64_t m, float scale
 template <int N, int DT, int QT = QT_NONE>
 hadacore_status_t launch_small_grid(const void* in, void* out, const Layout& L, float scale, cudaStream_t stream,
                                     uint8_t* out_q = nullptr, float* row_scale = nullptr) {
-  using T = TunedS<N>;
+  using T = std::conditional_t<(QT >= 0), TunedSQ<N>, TunedS<N>>;
   constexpr int tile = T::tkb * 1024;
   constexpr int tile_rows = tile / (2 * N);
   constexpr int smem = T::st * tile + int(sizeof(SchedCtl)) + 2 * T::st * 8;
