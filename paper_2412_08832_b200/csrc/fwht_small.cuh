@@ -26,6 +26,10 @@
 #pragma once
 #include "fwht_kernel.cuh"
 
+#ifndef HC_SMALL_STAGE_CODES
+#define HC_SMALL_STAGE_CODES 1
+#endif
+
 namespace hadacore {
 
 __device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
@@ -38,6 +42,15 @@ __device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t by
                "r"(bytes)
                : "memory");
 #endif
+}
+
+// Fused quantization with rows of >= 32 elements (contiguous rows, not GRID): the codes of a
+// tile are staged in a per-stage shared-memory buffer and written by the producer with one
+// 1-D bulk store, instead of per-lane 4/8-byte global stores at a row stride (which touch
+// 32 sectors per warp instruction).  Bytes of that buffer per stage (0: codes from registers).
+template <int N, int QT, bool GRID, int TILE_BYTES>
+__host__ __device__ constexpr int small_code_stage_bytes() {
+  return (QT >= 0 && !GRID && N >= 32 && HC_SMALL_STAGE_CODES) ? TILE_BYTES / 2 * (QT == QT_INT4 ? 1 : 2) / 2 : 0;
 }
 
 template <int DT>
@@ -73,9 +86,11 @@ __global__ void __launch_bounds__((NT + 1) * 32, 1)
   static_assert(TILE_BYTES % ITEM_BYTES == 0 && STAGES <= 16, "tile layout");
   static_assert(!GRID || N >= 8, "row grids: n >= 8 (16-byte TMA rows)");
 
+  constexpr int CODE_STAGE = small_code_stage_bytes<N, QT, GRID, TILE_BYTES>();
   extern __shared__ __align__(1024) uint8_t smem[];
-  SchedCtl* ctl = reinterpret_cast<SchedCtl*>(smem + STAGES * TILE_BYTES);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * TILE_BYTES + sizeof(SchedCtl));
+  uint8_t* const codes = smem + STAGES * TILE_BYTES;  // CODE_STAGE bytes per stage (may be 0)
+  SchedCtl* ctl = reinterpret_cast<SchedCtl*>(smem + STAGES * (TILE_BYTES + CODE_STAGE));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * (TILE_BYTES + CODE_STAGE) + sizeof(SchedCtl));
   uint64_t* done = full + STAGES;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -152,6 +167,8 @@ __global__ void __launch_bounds__((NT + 1) * 32, 1)
           tma_store_3d(&tm_out, 0, int(tr.j0), int(tr.i0), smem + s * TILE_BYTES);
         } else {
           if (QT < 0 && b16) bulk_s2g(reinterpret_cast<uint8_t*>(out) + t * TILE_BYTES, smem + s * TILE_BYTES, b16);
+          if (CODE_STAGE > 0)  // the tile's codes, staged by the consumers (a multiple of 16 bytes: n >= 32)
+            bulk_s2g(out_q + t * CODE_STAGE, codes + s * CODE_STAGE, uint32_t(tile_bytes(t)) / 2 * (QT == QT_INT4 ? 1 : 2) / 2);
         }
         bulk_commit();
         if (ended) continue;
@@ -318,6 +335,13 @@ __global__ void __launch_bounds__((NT + 1) * 32, 1)
               const int valid = (bytes - item * 16) / 2 * CB2 / 2;  // code bytes
               const uint32_t cw[2] = {QT == QT_INT4 ? __byte_perm(c0, c1, 0x5410) : c0, c1};
               for (int bq = 0; bq < valid; ++bq) out_q[cbyte + bq] = uint8_t(cw[bq >> 2] >> (8 * (bq & 3)));
+            } else if constexpr (CODE_STAGE > 0) {  // into the stage's code buffer (tile-relative offset)
+              uint8_t* dst = codes + s * CODE_STAGE + (cbyte - tile * CODE_STAGE);
+              if constexpr (QT == QT_INT4) {
+                asm volatile("st.shared.u32 [%0], %1;" ::"r"(smem_addr(dst)), "r"(__byte_perm(c0, c1, 0x5410)) : "memory");
+              } else {
+                asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(smem_addr(dst)), "r"(c0), "r"(c1) : "memory");
+              }
             } else if constexpr (QT == QT_INT4) {
               *reinterpret_cast<uint32_t*>(out_q + cbyte) = __byte_perm(c0, c1, 0x5410);
             } else {

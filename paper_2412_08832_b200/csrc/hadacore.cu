@@ -316,7 +316,7 @@ hadacore_status_t launch_small(const void* in, void* out, int64_t m, float scale
                                uint8_t* out_q = nullptr, float* row_scale = nullptr) {
   using T = std::conditional_t<(QT >= 0), TunedSQ<N>, TunedS<N>>;
   constexpr int tile = T::tkb * 1024;
-  constexpr int smem = T::st * tile + int(sizeof(SchedCtl)) + 2 * T::st * 8;
+  constexpr int smem = T::st * (tile + small_code_stage_bytes<N, QT, false, tile>()) + int(sizeof(SchedCtl)) + 2 * T::st * 8;
   static std::atomic<uint64_t> attr_done{0};
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return HADACORE_ERR_CUDA;
