@@ -44,13 +44,19 @@ __device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t by
 #endif
 }
 
-// Fused quantization with rows of >= 32 elements (contiguous rows, not GRID): the codes of a
-// tile are staged in a per-stage shared-memory buffer and written by the producer with one
-// 1-D bulk store, instead of per-lane 4/8-byte global stores at a row stride (which touch
-// 32 sectors per warp instruction).  Bytes of that buffer per stage (0: codes from registers).
+// Fused quantization with rows of >= 16 elements: the codes of a tile are staged in a
+// per-stage shared-memory buffer and written by the producer with one 1-D bulk store,
+// instead of per-lane 4/8-byte global stores at a row stride (which touch 32 sectors per
+// warp instruction).  Bytes of that buffer per stage (0: codes from registers).  A row-grid
+// tile uses it when its codes are one contiguous range of a multiple of 16 bytes (whole
+// inner rows per box, bi == m_inner); otherwise its codes go from registers
+// (profiles/r01_ab_small_stage_codes.txt).
 template <int N, int QT, bool GRID, int TILE_BYTES>
 __host__ __device__ constexpr int small_code_stage_bytes() {
-  return (QT >= 0 && !GRID && N >= 32 && HC_SMALL_STAGE_CODES) ? TILE_BYTES / 2 * (QT == QT_INT4 ? 1 : 2) / 2 : 0;
+  // (contiguous rows: only with >= 16 code bytes per row -- INT4 n = 16 measured faster from registers)
+  return (QT >= 0 && N >= 16 && (GRID || N * (QT == QT_INT4 ? 1 : 2) / 2 % 16 == 0) && HC_SMALL_STAGE_CODES)
+             ? TILE_BYTES / 2 * (QT == QT_INT4 ? 1 : 2) / 2
+             : 0;
 }
 
 template <int DT>
@@ -114,6 +120,26 @@ __global__ void __launch_bounds__((NT + 1) * 32, 1)
     return int(left < TILE_BYTES ? left : TILE_BYTES);
   };
 
+  // codes of tile t staged in shared memory (CODE_STAGE > 0): the destination byte offset
+  // in out_q and the byte count, or a count of 0 (codes from registers)
+  constexpr int CR = N * (QT == QT_INT4 ? 1 : 2) / 2;  // code bytes per row
+  // contiguous rows with >= 16 code bytes each: every tile's codes are staged
+  constexpr bool STAGE_ALWAYS = CODE_STAGE > 0 && !GRID;
+  auto staged_codes = [&](int64_t t, int64_t& dst) -> uint32_t {
+    if constexpr (CODE_STAGE == 0) {
+      return 0u;
+    } else if constexpr (GRID) {
+      if (g.nib != 1 || g.m_inner != (int64_t(1) << g.lbi) || ((CR << g.lbi) & 15) != 0) return 0u;
+      const TileRowsFast tr(g, t);
+      dst = tr.lin0 * CR;
+      return uint32_t(tr.ni << g.lbi) * CR;
+    } else {
+      const uint32_t cb = uint32_t(tile_bytes(t)) / (2 * N) * CR;
+      dst = t * CODE_STAGE;
+      return (cb & 15u) ? 0u : cb;
+    }
+  };
+
   pdl_launch_dependents();
   if (warp == NT) {
     // ---------------- producer: 1-D bulk loads into the ring, 1-D bulk stores out of it
@@ -162,13 +188,17 @@ __global__ void __launch_bounds__((NT + 1) * 32, 1)
         if (t < 0) break;
         mbar_wait(&done[s], (it / STAGES) & 1);
         const uint32_t b16 = uint32_t(tile_bytes(t)) & ~15u;
-        if constexpr (GRID) {
-          const TileRows tr(g, t);  // rows outside the grid are clipped by the TMA unit
-          tma_store_3d(&tm_out, 0, int(tr.j0), int(tr.i0), smem + s * TILE_BYTES);
-        } else {
-          if (QT < 0 && b16) bulk_s2g(reinterpret_cast<uint8_t*>(out) + t * TILE_BYTES, smem + s * TILE_BYTES, b16);
-          if (CODE_STAGE > 0)  // the tile's codes, staged by the consumers (a multiple of 16 bytes: n >= 32)
-            bulk_s2g(out_q + t * CODE_STAGE, codes + s * CODE_STAGE, uint32_t(tile_bytes(t)) / 2 * (QT == QT_INT4 ? 1 : 2) / 2);
+        if constexpr (QT < 0) {
+          if constexpr (GRID) {
+            const TileRows tr(g, t);  // rows outside the grid are clipped by the TMA unit
+            tma_store_3d(&tm_out, 0, int(tr.j0), int(tr.i0), smem + s * TILE_BYTES);
+          } else {
+            if (b16) bulk_s2g(reinterpret_cast<uint8_t*>(out) + t * TILE_BYTES, smem + s * TILE_BYTES, b16);
+          }
+        } else {  // quantizing: the stage itself is not written back; the staged codes are
+          int64_t dst = 0;
+          const uint32_t cb = staged_codes(t, dst);
+          if (cb) bulk_s2g(out_q + dst, codes + s * CODE_STAGE, cb);
         }
         bulk_commit();
         if (ended) continue;
@@ -215,6 +245,9 @@ __global__ void __launch_bounds__((NT + 1) * 32, 1)
     const int bytes = tile_bytes(tile);
     const int b16 = bytes & ~15;
     const int items = (bytes + ITEM_BYTES - 1) / ITEM_BYTES;
+    int64_t qdst_unused = 0;
+    const bool stage_q = STAGE_ALWAYS || staged_codes(tile, qdst_unused) != 0u;
+    (void)stage_q;
     for (int i0 = warp * 32 + lane; i0 < items; i0 += NT * 32 * U) {
       float v[U][8 * G];
 #pragma unroll
@@ -335,8 +368,8 @@ __global__ void __launch_bounds__((NT + 1) * 32, 1)
               const int valid = (bytes - item * 16) / 2 * CB2 / 2;  // code bytes
               const uint32_t cw[2] = {QT == QT_INT4 ? __byte_perm(c0, c1, 0x5410) : c0, c1};
               for (int bq = 0; bq < valid; ++bq) out_q[cbyte + bq] = uint8_t(cw[bq >> 2] >> (8 * (bq & 3)));
-            } else if constexpr (CODE_STAGE > 0) {  // into the stage's code buffer (tile-relative offset)
-              uint8_t* dst = codes + s * CODE_STAGE + (cbyte - tile * CODE_STAGE);
+            } else if (STAGE_ALWAYS || (CODE_STAGE > 0 && stage_q)) {  // into the stage's code buffer (row `item`)
+              uint8_t* dst = codes + s * CODE_STAGE + ((int64_t(item) * N + 8 * int64_t(uint32_t(j) ^ c)) * CB2) / 2;
               if constexpr (QT == QT_INT4) {
                 asm volatile("st.shared.u32 [%0], %1;" ::"r"(smem_addr(dst)), "r"(__byte_perm(c0, c1, 0x5410)) : "memory");
               } else {

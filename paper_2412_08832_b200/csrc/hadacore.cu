@@ -341,7 +341,7 @@ hadacore_status_t launch_small_grid(const void* in, void* out, const Layout& L, 
   using T = std::conditional_t<(QT >= 0), TunedSQ<N>, TunedS<N>>;
   constexpr int tile = T::tkb * 1024;
   constexpr int tile_rows = tile / (2 * N);
-  constexpr int smem = T::st * tile + int(sizeof(SchedCtl)) + 2 * T::st * 8;
+  constexpr int smem = T::st * (tile + small_code_stage_bytes<N, QT, true, tile>()) + int(sizeof(SchedCtl)) + 2 * T::st * 8;
   static std::atomic<uint64_t> attr_done{0};
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return HADACORE_ERR_CUDA;
