@@ -2,7 +2,7 @@
 set -x
 python -m paper_2412_08832_b200.build >/dev/null
 mkdir -p gpurun_out/final
-for w in c1 c5 small f32 qk-rotate qk-quant quant-e4m3 quant-int8 quant-int4; do
+for w in c1 c5 small f32 lab qk-rotate qk-quant quant-e4m3 quant-int8 quant-int4; do
   timeout 400 python bench.py --workload $w --no-e2e --no-cpu-baseline > gpurun_out/final/$w.json 2> gpurun_out/final/$w.err
 done
 for q in e4m3 int8 int4; do
