@@ -340,7 +340,24 @@ hadacore_status_t launch_small_grid(const void* in, void* out, const Layout& L, 
                                     uint8_t* out_q = nullptr, float* row_scale = nullptr) {
   using T = std::conditional_t<(QT >= 0), TunedSQ<N>, TunedS<N>>;
   constexpr int tile = T::tkb * 1024;
-  constexpr int tile_rows = tile / (2 * N);
+  // The transform only needs the tile's bytes in shared memory, not row coordinates: when
+  // each outer row block is contiguous (inner stride = n on both sides, e.g. the Q and K
+  // heads of a token), the TMA boxes describe it as pseudo-rows of up to 256 elements
+  // instead of rows of n (16-byte box rows at n = 8 move slowly), the kernel still
+  // transforming rows of n (a pseudo-row holds whole rows of one outer block).
+  Layout Lk = L;
+  int nb = N;  // box row length in elements
+  if (QT < 0 && L.in_si == N && L.out_si == N && L.m_inner > 1) {
+    const int64_t block_el = L.m_inner * N;
+    int pn = 256;
+    while (pn > N && block_el % pn != 0) pn /= 2;
+    if (pn >= 2 * N) {
+      Lk.m_inner = block_el / pn;
+      Lk.in_si = Lk.out_si = pn;
+      nb = pn;
+    }
+  }
+  const int tile_rows = tile / (2 * nb);
   constexpr int smem = T::st * (tile + small_code_stage_bytes<N, QT, true, tile>()) + int(sizeof(SchedCtl)) + 2 * T::st * 8;
   static std::atomic<uint64_t> attr_done{0};
   int dev = 0;
@@ -348,23 +365,23 @@ hadacore_status_t launch_small_grid(const void* in, void* out, const Layout& L, 
   auto kern = fwht_small_kernel<N, DT, tile, T::st, T::nt, T::u, QT, true>;
   if (!ensure_smem_attr(kern, smem, attr_done, dev)) return HADACORE_ERR_CUDA;
   int bi = 1;
-  while (bi * 2 <= tile_rows && bi * 2 <= L.m_inner && bi * 2 <= 256) bi *= 2;
+  while (bi * 2 <= tile_rows && bi * 2 <= Lk.m_inner && bi * 2 <= 256) bi *= 2;
   const int bo = tile_rows / bi < 256 ? tile_rows / bi : 256;
   RowGrid g{};
-  g.m_outer = L.m_outer;
-  g.m_inner = L.m_inner;
-  g.out_so = L.out_so;
-  g.out_si = L.out_si;
+  g.m_outer = Lk.m_outer;
+  g.m_inner = Lk.m_inner;
+  g.out_so = Lk.out_so;
+  g.out_si = Lk.out_si;
   while ((1 << g.lbi) < bi) ++g.lbi;
   g.bo = bo;
-  g.nib = (L.m_inner + bi - 1) / bi;
-  g.num_tiles = ((L.m_outer + bo - 1) / bo) * g.nib;
+  g.nib = (Lk.m_inner + bi - 1) / bi;
+  g.num_tiles = ((Lk.m_outer + bo - 1) / bo) * g.nib;
   CUtensorMap tin, tout;
-  if (!encode_small_map(&tin, in, L, L.in_so, L.in_si, N, g) ||
-      !encode_small_map(&tout, QT >= 0 ? in : out, L, QT >= 0 ? L.in_so : L.out_so, QT >= 0 ? L.in_si : L.out_si, N,
+  if (!encode_small_map(&tin, in, Lk, Lk.in_so, Lk.in_si, nb, g) ||
+      !encode_small_map(&tout, QT >= 0 ? in : out, Lk, QT >= 0 ? Lk.in_so : Lk.out_so, QT >= 0 ? Lk.in_si : Lk.out_si, nb,
                         g))  // the output map is unused when quantizing
     return HADACORE_ERR_CUDA;
-  const int64_t box_bytes = int64_t(bi) * bo * 2 * N;
+  const int64_t box_bytes = int64_t(bi) * bo * 2 * nb;
   const int64_t max_ctas = kClc ? int64_t(INT32_MAX) : int64_t(sm_count(dev));
   const int grid = int(g.num_tiles < max_ctas ? g.num_tiles : max_ctas);
   if (launch_pdl(kern, grid, (T::nt + 1) * 32, smem, stream, static_cast<const uint16_t*>(in),
