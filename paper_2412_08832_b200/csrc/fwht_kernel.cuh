@@ -736,6 +736,9 @@ struct RowGrid {
   // bulk copy of its valid rows (row r = ob * bi + jj of the tile) instead of a 3-D box
   const uint16_t* rows_in;
   int64_t in_so;
+  // fwht_small_kernel row grids: log2 of the n-element rows per grid row (the grid then
+  // describes contiguous outer row blocks as pseudo-rows of 2^lp rows; 0 = rows of n)
+  int32_t lp;
 };
 struct TileRows {
   int64_t i0, j0;

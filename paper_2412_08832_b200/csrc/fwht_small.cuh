@@ -129,10 +129,10 @@ __global__ void __launch_bounds__((NT + 1) * 32, 1)
     if constexpr (CODE_STAGE == 0) {
       return 0u;
     } else if constexpr (GRID) {
-      if (g.nib != 1 || g.m_inner != (int64_t(1) << g.lbi) || ((CR << g.lbi) & 15) != 0) return 0u;
+      if (g.nib != 1 || g.m_inner != (int64_t(1) << g.lbi) || ((CR << (g.lbi + g.lp)) & 15) != 0) return 0u;
       const TileRowsFast tr(g, t);
-      dst = tr.lin0 * CR;
-      return uint32_t(tr.ni << g.lbi) * CR;
+      dst = (tr.lin0 << g.lp) * CR;
+      return uint32_t(tr.ni << (g.lbi + g.lp)) * CR;
     } else {
       const uint32_t cb = uint32_t(tile_bytes(t)) / (2 * N) * CR;
       dst = t * CODE_STAGE;
@@ -311,8 +311,8 @@ __global__ void __launch_bounds__((NT + 1) * 32, 1)
           int64_t el0 = (tile * TILE_BYTES + int64_t(item) * ITEM_BYTES) / 2;  // first element of the item
           if constexpr (GRID) {  // n >= 8: one row per item, at (i, j) of the grid; codes/scales in row order
             int64_t gi = 0, gj = 0;
-            if (!TileRows(g, tile).at(g, item, gi, gj)) continue;
-            el0 = (gi * g.m_inner + gj) * N;
+            if (!TileRows(g, tile).at(g, item >> g.lp, gi, gj)) continue;  // (pseudo-)row of the grid
+            el0 = (((gi * g.m_inner + gj) << g.lp) + (item & ((1 << g.lp) - 1))) * N;
           }
           float mul[RI], scr[RI];
           bool fast = true;

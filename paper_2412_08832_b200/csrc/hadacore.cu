@@ -340,20 +340,21 @@ hadacore_status_t launch_small_grid(const void* in, void* out, const Layout& L, 
                                     uint8_t* out_q = nullptr, float* row_scale = nullptr) {
   using T = std::conditional_t<(QT >= 0), TunedSQ<N>, TunedS<N>>;
   constexpr int tile = T::tkb * 1024;
-  // The transform only needs the tile's bytes in shared memory, not row coordinates: when
-  // each outer row block is contiguous (inner stride = n on both sides, e.g. the Q and K
-  // heads of a token), the TMA boxes describe it as pseudo-rows of up to 256 elements
-  // instead of rows of n (16-byte box rows at n = 8 move slowly), the kernel still
-  // transforming rows of n (a pseudo-row holds whole rows of one outer block).
+  // The kernel only needs the tile's bytes in shared memory plus, when quantizing, each
+  // row's linear index: when each outer row block is contiguous (inner stride = n, e.g.
+  // the Q and K heads of a token), the TMA boxes describe it as pseudo-rows of up to 256
+  // elements instead of rows of n (16-byte box rows at n = 8 move slowly), the kernel still
+  // transforming rows of n (a pseudo-row holds 2^lp whole rows of one outer block).
   Layout Lk = L;
   int nb = N;  // box row length in elements
-  if (QT < 0 && L.in_si == N && L.out_si == N && L.m_inner > 1) {
+  if (L.in_si == N && (QT >= 0 || L.out_si == N) && L.m_inner > 1) {
     const int64_t block_el = L.m_inner * N;
     int pn = 256;
     while (pn > N && block_el % pn != 0) pn /= 2;
     if (pn >= 2 * N) {
       Lk.m_inner = block_el / pn;
-      Lk.in_si = Lk.out_si = pn;
+      Lk.in_si = pn;
+      if (QT < 0) Lk.out_si = pn;
       nb = pn;
     }
   }
@@ -376,6 +377,7 @@ hadacore_status_t launch_small_grid(const void* in, void* out, const Layout& L, 
   g.bo = bo;
   g.nib = (Lk.m_inner + bi - 1) / bi;
   g.num_tiles = ((Lk.m_outer + bo - 1) / bo) * g.nib;
+  while ((N << g.lp) < nb) ++g.lp;
   CUtensorMap tin, tout;
   if (!encode_small_map(&tin, in, Lk, Lk.in_so, Lk.in_si, nb, g) ||
       !encode_small_map(&tout, QT >= 0 ? in : out, Lk, QT >= 0 ? Lk.in_so : Lk.out_so, QT >= 0 ? Lk.in_si : Lk.out_si, nb,
