@@ -54,13 +54,21 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--ns", default=None, help="comma-separated n list overriding the workload's sweep "
                                                "(e.g. --workload quant-e4m3 --ns 2,4,8,16,32,64)")
+    ap.add_argument("--check-rows", type=int, default=4,
+                    help="output rows per rank per launch gathered to rank 0 for the oracle and bitwise checks")
+    ap.add_argument("--misshard", action="store_true",
+                    help="negative control of the multi-rank check: rank 1 (rank 0 at N=1) generates its rows "
+                         "one base row off; the sampled-row check must then fail (exit code 3)")
     ap.add_argument("--workload", choices=["fwht", "quant-e4m3", "quant-int8", "quant-int4", "qk-rotate", "qk-quant", "small", "f32", "c5",
-                             "c1", "lab"], default="fwht",
+                             "c1", "c2", "c4", "lab"], default="fwht",
                     help="fwht = the metric's C3 sweep (default); quant-* = the fused FWHT + per-row "
                          "quantization row (NEXT-1) on the same inputs; small = n=2^1..2^6 (NEXT-2); "
                          "f32 = the fp32 path over n=2^1..2^15 (NEXT-2); c5 = BASELINE config C5: bf16 "
                          "n=2^15, 2^33 elements row-sharded over the ranks (strong scaling); c1 = BASELINE config "
-                         "C1 (fp16 m=1024 n=256): microseconds per launch, warm (CUDA graph) and cold (L2 flushed)")
+                         "C1 (fp16 m=1024 n=256): microseconds per launch, warm (CUDA graph) and cold (L2 flushed); "
+                         "c2 = BASELINE config C2 (bf16 n=128, m=2^20: Llama-3 8B Q/K head_dim rotation); c4 = "
+                         "BASELINE config C4 (fp16 n=4096, m=16384: QuaRot Llama-2 7B online rotation), L2 scrubbed "
+                         "before every launch")
     return ap.parse_args()
 
 
@@ -82,9 +90,12 @@ def measured_hbm_peak():
         return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic():
-    """Per-launch DRAM bytes from the committed ncu --set full capture, if present."""
-    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+def ncu_traffic(workload: str = "fwht"):
+    """Per-launch DRAM bytes from the committed ncu --set full capture of this workload's
+    launches (profiles/ncu_traffic.json for the C3 sweep, ncu_traffic_<workload>.json for
+    the others), if present."""
+    name = "ncu_traffic.json" if workload == "fwht" else f"ncu_traffic_{workload}.json"
+    p = os.path.join(ROOT, "profiles", name)
     try:
         return json.load(open(p))
     except Exception:
@@ -163,6 +174,10 @@ def dist_setup(args):
     if world > 1:
         import torch.distributed as dist
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        # NCCL communicator INIT lines (nranks, transports) in the log, so a scaling run
+        # shows which communicator the ranks formed
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         ndev = torch.cuda.device_count()
         dev = local % ndev
         torch.cuda.set_device(dev)
@@ -277,9 +292,26 @@ def config_block(args, world):
         wl = (f"QK rotation + FP8-E4M3 quantization: {nrange} x {{fp16, bf16}}; a 2^28-element QKV buffer viewed "
               "as [T, 3, H, n], H = max(1, 4096/n); the Q and K heads read strided, codes and row scales written "
               "contiguously (hadacore_fwht_quant_strided), normalized")
+    if w == "c2":
+        ns = [128]
+        wl = ("C2: Llama-3 8B FP8-attention Q/K rotation, bf16 n=128 (head_dim), m=8x32x4096=2^20 rows per GPU, "
+              "normalized")
+    if w == "c4":
+        ns = [4096]
+        wl = "C4: QuaRot Llama-2 7B online rotation, fp16 n=4096, m=16384 tokens per GPU, normalized"
+    if getattr(args, "inplace", False):
+        wl = wl.replace("out-of-place", "in place (out = in, P:264-274)")
+        if "in place" not in wl:
+            wl += "; in place (out = in, P:264-274)"
+    elif w in ("c2", "c4"):
+        wl += "; out-of-place"
     mib_in = args.elems * (4 if w == "f32" else 2) >> 20
     if w == "c5":
         l2 = "no flush: each rank's launch reads 16/N GiB and writes 16/N GiB (> 126 MB L2)"
+    elif w == "c4":
+        l2 = ("flushed: a 2 x L2-size buffer is written before every timed launch, outside its CUDA events "
+              f"(each launch reads {mib_in} MiB and writes {mib_in} MiB, about the size of the 126 MB L2); value = "
+              "bytes / sum of the per-launch event times")
     elif w in ("qk-rotate", "qk-quant"):
         l2 = (f"no flush: every launch reads the {mib_in * 2 // 3} MiB of Q and K heads (> 126 MB L2) and writes "
               + ("them back in place" if w == "qk-rotate" else f"{args.elems * 2 // 3 >> 20} MiB of codes"))
@@ -290,8 +322,9 @@ def config_block(args, world):
         l2 = f"no flush: every launch reads a {mib_in} MiB input and writes a {mib_in} MiB output (> 126 MB L2)"
     return {"workload": wl,
             "elements_per_launch": args.elems, "ns": ns,
-            "dtypes": {"f32": ["fp32"], "c5": ["bf16"]}.get(w, ["fp16", "bf16"]),
-            "launches_per_step": (1 if w in ("f32", "c5") else 2) * len(ns), "path": w,
+            "dtypes": {"f32": ["fp32"], "c5": ["bf16"], "c2": ["bf16"], "c4": ["fp16"]}.get(w, ["fp16", "bf16"]),
+            "launches_per_step": (1 if w in ("f32", "c5", "c2", "c4") else 2) * len(ns), "path": w,
+            "inplace": bool(getattr(args, "inplace", False)),
             "l2": l2,
             "parallelism": f"row-sharded x{world}, no collective on the hot path" if world > 1 else "single GPU"}
 
@@ -321,12 +354,18 @@ def run_c1(args, rank, world, dist):
             g.replay()
         barrier(dist, torch)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(args.steps):
-            g.replay()
-        e1.record(stream)
-        torch.cuda.synchronize()
-        warm_us = max_over_ranks(e0.elapsed_time(e1) * 1e3 / (args.steps * R), dist, torch)
+        # at least ~0.5 s of replays so nvidia-smi samples the timed region (20 ms period)
+        reps = max(args.steps, 3000)
+        with ClockSampler(torch.cuda.current_device()) as cs:
+            cs.mark_start()
+            e0.record(stream)
+            for _ in range(reps):
+                g.replay()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            cs.mark_end()
+        clocks = cs.summary()
+        warm_us = max_over_ranks(e0.elapsed_time(e1) * 1e3 / (reps * R), dist, torch)
         flush = torch.empty(2 * 126 * 1000 * 1000, dtype=torch.uint8, device=dev)
         cold = []
         for _ in range(max(3, args.steps)):
@@ -342,7 +381,7 @@ def run_c1(args, rank, world, dist):
     if rank != 0:
         return None
     return {"metric": "C1 latency: microseconds per hadacore_fwht launch, fp16 m=1024 n=256 (warm, CUDA graph)",
-            "value": round(warm_us, 3), "unit": "us", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "value": round(warm_us, 3), "unit": "us", "n_gpus": world, "steps": reps, "warmup": args.warmup,
             "ms_per_step": round(warm_us * R / 1e3, 4), "higher_is_better": False, "scaling": "weak",
             "vs_baseline": None, "dtype": "fp16 (fp32 last-stage accumulate)", "data": "synthetic (synthetic/)",
             "config": {"workload": "C1: fp16 m=1024 n=256 (1 MiB traffic), 100 launches per CUDA graph replay; "
@@ -354,7 +393,8 @@ def run_c1(args, rank, world, dist):
                          "frac": round(bytes_ / (cold_us * 1e-6) / 1e9 / measured_hbm_peak()[0], 4),
                          "traffic": None, "note": "1 MiB per launch: launch-latency-bound, not bandwidth-bound; "
                                                   "achieved from the cold launch time"},
-            "gpu_launches": int(args.steps * R), "cpu_baseline": None, "e2e": None}
+            "gpu_launches": int(reps * R), "cpu_baseline": None, "e2e": None, "clocks": clocks,
+            "graph_replays": reps}
 
 
 def run_lab(args, rank, world):
@@ -381,6 +421,144 @@ def run_lab(args, rank, world):
             "roofline": None, "cpu_baseline": None, "e2e": None, "gpu_launches": None}
 
 
+# ---------------------------------------------------------------- resident inputs and the sampled check
+# Every workload's data is a slice of one global seeded matrix generated at a base width W
+# (synthetic/ keys its generator on the global element index): rank r's
+# resident buffer holds global elements [flat0_r, flat0_r + elems), and the row of width n
+# at local index i is global row flat0_r / n + i.  So any rank -- and rank 0 when it checks
+# the others -- can regenerate any global row without communication.
+WORKLOADS = {
+    # workload: (config index for the seed, base width W, dtypes, ns)
+    "fwht": (2, 256, ("fp16", "bf16"), NS),
+    "small": (2, 256, ("fp16", "bf16"), SMALL_NS),
+    "f32": (2, 256, ("fp32",), SMALL_NS + NS),
+    "c2": (1, 128, ("bf16",), [128]),
+    "c4": (3, 4096, ("fp16",), [4096]),
+    "c5": (5, 32768, ("bf16",), [32768]),
+}
+C2_ROWS, C4_ROWS, C5_ROWS = 8 * 32 * 4096, 16384, C5_ELEMS // 32768
+
+
+def torch_dtype(name):
+    import torch
+    return {"fp16": torch.float16, "bf16": torch.bfloat16, "fp32": torch.float32}[name]
+
+
+def dtype_name(dt):
+    import torch
+    return {torch.float16: "fp16", torch.bfloat16: "bf16", torch.float32: "fp32"}[dt]
+
+
+def seed_of(workload, dt):
+    import synthetic
+    idx = WORKLOADS.get(workload, WORKLOADS["fwht"])[0]  # C5: 5, the parity tests' seed
+    return synthetic.seed_for(idx, dt)
+
+
+def gen_rows(workload, dt, n, g0, count, device, shift_elems=0):
+    """Rows [g0, g0 + count) of width n of the workload's global matrix (fresh from synthetic/)."""
+    import synthetic
+    w = WORKLOADS.get(workload, WORKLOADS["fwht"])[1]
+    start = g0 * n + shift_elems
+    end = start + count * n
+    r0, r1 = start // w, -(-end // w)
+    blk = synthetic.generate(r1 - r0, w, dt, seed_of(workload, dt), row0=r0, device=device).view(-1)
+    return blk[start - r0 * w: end - r0 * w].view(count, n)
+
+
+def rank_layout(workload, rank, world, elems):
+    """(flat0, elems) of this rank's slice of the global matrix, and the global element count."""
+    from paper_2412_08832_b200.shard import row_range
+    if workload == "c5":
+        lo, hi = row_range(C5_ROWS, rank, world)
+        return lo * 32768, (hi - lo) * 32768, C5_ELEMS
+    if workload == "c2":
+        return rank * C2_ROWS * 128, C2_ROWS * 128, world * C2_ROWS * 128
+    if workload == "c4":
+        return rank * C4_ROWS * 4096, C4_ROWS * 4096, world * C4_ROWS * 4096
+    return rank * elems, elems, world * elems
+
+
+def fill_resident(buf, workload, dt, flat0, shift_elems=0):
+    """buf (1-D, numel multiple of W) <- global elements [flat0, flat0 + numel) (+ shift)."""
+    import synthetic
+    w = WORKLOADS.get(workload, WORKLOADS["fwht"])[1]
+    start = flat0 + shift_elems
+    assert start % w == 0 and buf.numel() % w == 0
+    synthetic.generate(buf.numel() // w, w, dt, seed_of(workload, dt), row0=start // w, out=buf.view(-1, w))
+
+
+def sample_local_rows(n, dt, rank, m_loc, k):
+    """The local row indices rank `rank` contributes to the check: its first and last row and
+    k - 2 seeded random rows (the same list on every rank, so rank 0 can rebuild it)."""
+    import torch
+    g = torch.Generator().manual_seed(1000003 * n + 7919 * rank + (17 if dt == torch.bfloat16 else 0) +
+                                      (29 if dt == torch.float32 else 0))
+    extra = torch.randint(0, m_loc, (max(0, k - 2),), generator=g).tolist() if m_loc > 0 else []
+    return ([0, m_loc - 1] + extra)[:max(k, 1)]
+
+
+def gather_sample(y, n, dt, rank, world, k, dist):
+    """This rank's sampled output rows (sample_local_rows) gathered to rank 0 with
+    shard.gather_rows (NCCL; CPU tensors over gloo): [k * world, n] on rank 0, None elsewhere."""
+    from paper_2412_08832_b200.shard import gather_rows
+    loc = y[sample_local_rows(n, dt, rank, y.shape[0], k)].contiguous()
+    if dist is None:
+        return loc
+    if dist.get_backend() != "nccl":
+        loc = loc.cpu()
+    return gather_rows(loc, k * world, dist)
+
+
+def sampled_rows_check(results, workload, world, elems, k, dist, transform, device):
+    """Rank 0's half of the multi-rank result check (north_star "NCCL only to
+    gather results for checking").  `results[(dt, n)]` is the [k * world, n] block gathered from
+    every rank (rank order; rank r's rows are sample_local_rows(...)).  Each row is compared with
+    (a) the fp64 oracle on the regenerated global input (north_star tolerances) and (b) bitwise
+    with rank 0's own transform of the same global rows (a 16-row aligned block regenerated on
+    rank 0's GPU): sharding invariance, ambiguity 17."""
+    import numpy as np
+    import torch
+    import oracle
+    tol = {"fp16": 2e-3, "bf16": 1.6e-2, "fp32": 1e-5}
+    dev = device
+    worst, mism, checked, bad_rows = {}, 0, 0, []
+    for (dt, n), got in results.items():
+        got = got.to("cpu")
+        rows_global = []
+        for r in range(world):
+            flat0, el, total = rank_layout(workload, r, world, elems)
+            m_loc = el // n
+            rows_global += [flat0 // n + i for i in sample_local_rows(n, dt, r, m_loc, k)]
+        m_global = total // n
+        x = torch.cat([gen_rows(workload, dt, n, g, 1, "cpu") for g in rows_global])
+        ref = oracle.fwht(x.double().numpy())
+        g64 = got.double().numpy()
+        err = np.linalg.norm(g64 - ref, axis=1) / np.maximum(np.linalg.norm(ref, axis=1), 1e-300)
+        name = dtype_name(dt)
+        worst[name] = max(worst.get(name, 0.0), float(err.max()))
+        for j, g in enumerate(rows_global):
+            b = min(g - g % 16, max(0, m_global - 16))
+            cnt = min(16, m_global - b)
+            y = transform(gen_rows(workload, dt, n, b, cnt, dev))
+            iv = torch.int32 if dt == torch.float32 else torch.int16
+            same = torch.equal(y[g - b].cpu().view(iv), got[j].view(iv))
+            checked += 1
+            if not same or err[j] > tol[name]:
+                mism += int(not same)
+                if len(bad_rows) < 8:
+                    bad_rows.append({"dtype": name, "n": n, "row": int(g), "rel_err": float(f"{err[j]:.3e}"),
+                                     "bitwise_equal": bool(same)})
+    ok_oracle = all(worst[nm] <= tol[nm] for nm in worst)
+    return {"ranks": world, "rows_per_rank_per_launch": k, "rows_checked": checked,
+            "gather": ("NCCL" if dist is not None and dist.get_backend() == "nccl" else
+                       ("gloo" if dist is not None else "none (1 rank)")) + " gather of sampled output rows to rank 0",
+            "oracle_max_rel_err": {nm: float(f"{v:.3e}") for nm, v in worst.items()},
+            "tolerance": {nm: tol[nm] for nm in worst}, "oracle_pass": ok_oracle,
+            "bitwise_mismatches_vs_rank0_recompute": mism, "bitwise_pass": mism == 0,
+            "pass": ok_oracle and mism == 0, "failing_rows": bad_rows}
+
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -402,51 +580,35 @@ def main():
         return
 
     import paper_2412_08832_b200 as hc
-    import synthetic
     hc._load()  # fails loudly without the CUDA library
     dev = torch.device("cuda", local)
-    # resident inputs: one 2^28-element matrix per dtype (each (n) is a view), rows
-    # [rank*m, (rank+1)*m) of the global seeded matrix (weak scaling)
-    xin, xout = {}, {}
-    c5 = args.workload == "c5"
-    c5_rows = (C5_ELEMS // 32768)
-    if c5:
-        # C5: the global 2^33-element bf16 matrix (262144 rows of 2^15); this rank's rows
-        from paper_2412_08832_b200.shard import row_range
-        lo, hi = row_range(c5_rows, rank, world)
-        args.elems = (hi - lo) * 32768
-    for dt in ((torch.bfloat16,) if c5 else (torch.float16, torch.bfloat16)):
-        buf = torch.empty(args.elems, dtype=dt, device=dev)
-        if c5:
-            synthetic.generate(hi - lo, 32768, dt, synthetic.seed_for(5, dt), row0=lo, out=buf.view(-1, 32768))
-        else:
-            synthetic.generate(args.elems // 256, 256, dt, synthetic.seed_for(2, dt),
-                               row0=rank * (args.elems // 256), out=buf.view(-1, 256))
-        xin[dt] = buf
-    obuf = torch.empty(args.elems, dtype=torch.float16, device=dev)
+    wl = args.workload
+    src_wl = wl if wl in WORKLOADS else "fwht"  # quant-* / qk-*: the C3 matrices
+    c5, f32, scrub = wl == "c5", wl == "f32", wl == "c4"
+    flat0, args.elems, _ = rank_layout(src_wl, rank, world, args.elems)
+    # negative control (--misshard): the last rank (rank 0 at N = 1) generates its slice one
+    # base row off, so its outputs belong to other global rows than it reports
+    shift = WORKLOADS[src_wl][1] if (args.misshard and rank == world - 1) else 0
+    dtypes = [torch_dtype(d) for d in WORKLOADS[src_wl][2]]
+    xin = {}
+    for dt in dtypes:
+        xin[dt] = torch.empty(args.elems, dtype=dt, device=dev)
+        fill_resident(xin[dt], src_wl, dt, flat0, shift)
+    obuf = torch.empty(args.elems, dtype=torch.float32 if f32 else torch.float16, device=dev)
     stream = torch.cuda.current_stream(dev)
-    ns = SMALL_NS if args.workload == "small" else NS
+    ns = list(WORKLOADS[src_wl][3])
     if args.ns:
         ns = [int(v) for v in args.ns.split(",")]
-    f32 = args.workload == "f32"
-    if f32:
-        ns = SMALL_NS + NS
-        xin = {torch.float32: torch.empty(args.elems, dtype=torch.float32, device=dev)}
-        synthetic.generate(args.elems // 256, 256, torch.float32, synthetic.seed_for(2, torch.float32),
-                           row0=rank * (args.elems // 256), out=xin[torch.float32].view(-1, 256))
-        obuf = torch.empty(args.elems, dtype=torch.float32, device=dev)
-    pairs = [(dt, n) for dt in ((torch.float32,) if f32 else (torch.float16, torch.bfloat16)) for n in ns]
-    if c5:
-        ns, pairs = [32768], [(torch.bfloat16, 32768)]
-    quant = args.workload.startswith("quant")
-    qtype = args.workload.split("-")[1] if quant else None
+    pairs = [(dt, n) for dt in dtypes for n in ns]
+    quant = wl.startswith("quant")
+    qtype = wl.split("-")[1] if quant else None
     if quant:
         qbuf = torch.empty(args.elems // (2 if qtype == "int4" else 1), dtype=hc.QTYPES[qtype][1], device=dev)
         sbuf = torch.empty(args.elems // min(ns), dtype=torch.float32, device=dev)
     qb = 0.5 if qtype == "int4" else 1.0  # code bytes per element
 
-    rotate = args.workload in ("qk-rotate", "qk-quant")
-    qkq = args.workload == "qk-quant"  # Q/K heads rotated + FP8-quantized in one pass (FP8 attention)
+    rotate = wl in ("qk-rotate", "qk-quant")
+    qkq = wl == "qk-quant"  # Q/K heads rotated + FP8-quantized in one pass (FP8 attention)
     if qkq:
         qbuf = torch.empty(args.elems, dtype=torch.float8_e4m3fn, device=dev)
         sbuf = torch.empty(args.elems // min(ns), dtype=torch.float32, device=dev)
@@ -460,6 +622,9 @@ def main():
                 t = args.elems // (3 * h * n)
                 qk[(dt, n)] = xin[dt][: t * 3 * h * n].view(t, 3, h, n)[:, 0:2]
     elems_of = {(dt, n): (qk[(dt, n)].numel() if rotate else args.elems) for dt, n in pairs}
+
+    def out_view(dt, n):
+        return obuf.view(-1, n) if f32 else obuf.view(torch.int16).view(dt).view(-1, n)
 
     def launch(dt, n):
         if rotate:
@@ -476,12 +641,17 @@ def main():
                                    row_scale=sbuf[: x.shape[0]],
                                    stream=stream)
             return
-        o = obuf.view(-1, n) if f32 else obuf.view(torch.int16).view(dt).view(-1, n)
-        hc.hadacore_fwht(x, out=x if args.inplace else o, stream=stream)
+        hc.hadacore_fwht(x, out=x if args.inplace else out_view(dt, n), stream=stream)
+
+    # C4 (about the L2's size): a 2 x L2 write before every timed launch, outside its events
+    l2_bytes = getattr(torch.cuda.get_device_properties(dev), "L2_cache_size", 126 * 1000 * 1000) or 126000000
+    scrub_buf = torch.empty(2 * l2_bytes, dtype=torch.uint8, device=dev) if scrub else None
 
     # warm-up
     for _ in range(args.warmup):
         for dt, n in pairs:
+            if scrub:
+                scrub_buf.fill_(1)
             launch(dt, n)
     barrier(dist, torch)
 
@@ -490,9 +660,11 @@ def main():
         # kernels breaks programmatic dependent launch (the next grid's prologue and
         # first loads no longer overlap the previous grid's tail), which measured -5 %
         # on the sweep (tools/gap_probe.py, profiles/r01_gap_probe.txt). The per-(dtype,
-        # n) breakdown comes from a separate pass with per-launch events.
+        # n) breakdown comes from a separate pass with per-launch events.  With an L2
+        # scrub (C4) every launch has its own events and the region's time is their sum.
+        ple = per_launch_events or scrub
         evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-               for _ in range(steps * len(pairs) if per_launch_events else 0)]
+               for _ in range(steps * len(pairs) if ple else 0)]
         g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         barrier(dist, torch)
         torch.cuda.synchronize()
@@ -500,16 +672,18 @@ def main():
         i = 0
         for _ in range(steps):
             for dt, n in pairs:
-                if per_launch_events:
+                if scrub:
+                    scrub_buf.fill_(1)
+                if ple:
                     evs[i][0].record(stream)
                 launch(dt, n)
-                if per_launch_events:
+                if ple:
                     evs[i][1].record(stream)
                 i += 1
         g1.record(stream)
         torch.cuda.synchronize()
-        total_ms = g0.elapsed_time(g1)
         per = [a.elapsed_time(b) for a, b in evs]
+        total_ms = sum(per) if scrub else g0.elapsed_time(g1)
         barrier(dist, torch)
         return total_ms, per
 
@@ -530,28 +704,47 @@ def main():
     # per-launch breakdown: a separate pass after the timed region
     _, per = timed_region(max(3, min(args.steps, 10)), True)
 
-    # output check outside the timed regions, on every rank (no oracle here: a property that
-    # holds at any size) -- the normalized transform preserves every row's
-    # norm; the worst relative norm error over all rows of every (dtype, n) launch, max over ranks
+    # output checks outside the timed regions, on every rank:
+    # (1) a property that holds at any size: the normalized transform preserves
+    #     every row's norm -- every row of every (dtype, n) launch, max over ranks;
+    # (2) sampled rows: every rank's first, last and k-2 random rows of every launch are gathered
+    #     to rank 0 (NCCL; gloo when ranks share a GPU) and checked there against the fp64 oracle
+    #     and bitwise against rank 0's own transform of the same global rows.
+    # In-place runs regenerate the input first (the timed launches transformed it repeatedly).
     check = None
-    if not quant and not rotate and not args.inplace:
+    if not quant and not rotate:
         worst, by_dt = 0.0, {}
         tol_of = {torch.float16: 2e-3, torch.bfloat16: 1.6e-2, torch.float32: 1e-5}
+        gathered = {}
         for dt, n in pairs:
+            if args.inplace:
+                fill_resident(xin[dt], src_wl, dt, flat0, shift)
+                xcopy = out_view(dt, n)
+                xcopy.view(-1).copy_(xin[dt])
             launch(dt, n)
-            x = xin[dt].view(-1, n)
-            y = (obuf.view(-1, n) if f32 else obuf.view(torch.int16).view(dt).view(-1, n))[: x.shape[0]]
+            x = (xcopy if args.inplace else xin[dt].view(-1, n))
+            y = (xin[dt].view(-1, n) if args.inplace else out_view(dt, n))[: x.shape[0]]
             for r0 in range(0, x.shape[0], max(1, (1 << 26) // n)):
                 nx = torch.linalg.vector_norm(x[r0:r0 + (1 << 26) // n].float(), dim=1)
                 ny = torch.linalg.vector_norm(y[r0:r0 + (1 << 26) // n].float(), dim=1)
                 e = ((ny - nx).abs() / nx.clamp_min(1e-30)).max().item()
                 by_dt[dt] = max(by_dt.get(dt, 0.0), e)
-        names = {torch.float16: "fp16", torch.bfloat16: "bf16", torch.float32: "fp32"}
-        errs = {names[dt]: float(f"{max_over_ranks(e, dist, torch):.3e}") for dt, e in by_dt.items()}
+            gathered[(dt, n)] = gather_sample(y, n, dt, rank, world, args.check_rows, dist)
+        errs = {dtype_name(dt): float(f"{max_over_ranks(e, dist, torch):.3e}") for dt, e in by_dt.items()}
         check = {"property": "row-norm preservation of the normalized transform, every row of every launch "
-                             "(north_star tolerances per dtype)",
-                 "max_rel_err": errs, "tolerance": {names[dt]: tol_of[dt] for dt in by_dt},
-                 "pass": all(errs[names[dt]] <= tol_of[dt] for dt in by_dt)}
+                             "(north_star tolerances per dtype)" + ("; input regenerated, one in-place launch"
+                                                                    if args.inplace else ""),
+                 "max_rel_err": errs, "tolerance": {dtype_name(dt): tol_of[dt] for dt in by_dt}}
+        check["norm_pass"] = all(errs[dtype_name(dt)] <= tol_of[dt] for dt in by_dt)
+        if rank == 0:
+            mr = sampled_rows_check(gathered, src_wl, world, args.elems, args.check_rows, dist, hc.hadacore_fwht, dev)
+            check["multi_rank"] = mr
+        ok = torch.tensor([1.0 if (rank != 0 or check["multi_rank"]["pass"]) else 0.0], dtype=torch.float64)
+        if dist is not None:
+            okd = ok.to(dev) if dist.get_backend() == "nccl" else ok
+            dist.broadcast(okd, src=0)
+            ok = okd.cpu()
+        check["pass"] = bool(check["norm_pass"] and ok.item() == 1.0)
 
     # same-run D2D copy of the same byte count ("% of achievable copy"): cudaMemcpyAsync
     # of one input buffer into the output buffer, event-timed on the same stream
@@ -595,21 +788,22 @@ def main():
         b_n = 2.0 * esize * elems_of[(dt, n)] if not quant else (2.0 + qb) * args.elems + 4.0 * (args.elems // n)
         if qkq:
             b_n = 3.0 * elems_of[(dt, n)] + 4.0 * elems_of[(dt, n)] / n
-        per_n.setdefault({torch.float16: "fp16", torch.bfloat16: "bf16", torch.float32: "fp32"}[dt], {})[str(n)] = round(b_n / (med * 1e-3) / 1e9, 1)
+        per_n.setdefault(dtype_name(dt), {})[str(n)] = round(b_n / (med * 1e-3) / 1e9, 1)
     # roofline over the timed region: every launch of the step is the same transform
     # (one per (dtype, n)), so the kernel's average launch duration is the region time
     # over the launches in it (per-(dtype, n) values: per_n_GBps)
     avg_launch_ms = t_max / (args.steps * len(pairs))
     peak, peak_src = measured_hbm_peak()
     achieved = bytes_per_launch / (avg_launch_ms * 1e-3) / 1e9
-    traffic = ncu_traffic() if args.workload == "fwht" else None
+    traffic = ncu_traffic(wl)
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "peak_source": peak_src,
                 "frac_of_8TBps": round(achieved / NOMINAL_HBM_GBS, 4),
                 "algorithmic_bytes_per_launch": int(bytes_per_launch),
                 "traffic": (traffic or {}).get("avg_dram_bytes_per_launch"),
                 "traffic_source": (traffic or {}).get("source"),
-                "duration_source": "timed region / launches (CUDA events on the launching stream, max over ranks)",
+                "duration_source": ("sum of per-launch CUDA events (L2 scrubbed between launches)" if scrub else
+                                    "timed region / launches (CUDA events on the launching stream, max over ranks)"),
                 "sum_of_launch_events_GBps": round(bytes_per_launch * len(per) / (sum(per) * 1e-3) / 1e9, 1),
                 "same_run_d2d_copy_GBps": round(copy_gbps, 1),
                 "frac_of_same_run_copy": round(achieved / copy_gbps, 4),
@@ -618,7 +812,7 @@ def main():
 
     # end to end through the public host-buffer C entry (hadacore_fwht_host)
     e2e = None
-    if not args.no_e2e and args.workload == "fwht":
+    if not args.no_e2e and wl in ("fwht", "c2", "c4"):
         hin = {dt: xin[dt].cpu().pin_memory() for dt in xin}
         hout = torch.empty(args.elems, dtype=torch.float16).pin_memory()
         ws = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
@@ -643,14 +837,14 @@ def main():
         del hin, hout, ws
 
     cpu_baseline = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline and args.workload == "fwht":
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and wl in ("fwht", "c2", "c4", "c5"):
         import oracle
         oracle.build()
         threads = oracle.default_threads()
         import numpy as np
         sample = 1 << 24
-        # widened once (fp64, 2.4 GB), then whole passes over the 18 samples until
-        # >= 10 s of oracle time (bounded CPU work, the contract's 10-30 s)
+        # widened once (fp64), then whole passes over the samples until >= 10 s of oracle
+        # time (bounded CPU work, the contract's 10-30 s)
         inputs = {(str(dt), n): np.ascontiguousarray(xin[dt][: (sample // n) * n].view(-1, n).cpu().double().numpy())
                   for dt, n in pairs}
         t, e, passes = 0.0, 0, 0
@@ -660,7 +854,7 @@ def main():
         del inputs
         cpu_baseline = {"value": round(4.0 * e / t / 1e9, 4), "unit": "GB/s", "cores": threads, "kind": "oracle",
                         "cpu_model": cpu_model(), "gel_per_s": round(e / t / 1e9, 4),
-                        "sample": f"first {sample >> 20}Mi elements of each of the 18 (dtype, n) C3 inputs, "
+                        "sample": f"first {sample >> 20}Mi elements of each of the {len(pairs)} (dtype, n) inputs, "
                                   f"{passes} passes ({e} elements), fp64 listing, {t:.1f} s; widening excluded"}
 
     if rank == 0:
@@ -672,7 +866,12 @@ def main():
         if c5:
             metric = ("C5: FWHT HBM GB/s, bf16 n=2^15, 2^33 elements row-sharded across the GPUs "
                       "(whole-job bytes / max-over-ranks time; strong scaling)")
-        if args.workload == "small":
+        if wl == "c2":
+            metric = "C2: FWHT HBM GB/s, bf16 n=128, m=2^20 rows per GPU (Llama-3 8B Q/K head_dim rotation)"
+        if wl == "c4":
+            metric = ("C4: FWHT HBM GB/s, fp16 n=4096, m=16384 rows per GPU (QuaRot Llama-2 7B online rotation), "
+                      "L2 scrubbed before every launch")
+        if wl == "small":
             metric = "FWHT HBM GB/s vs n=2^1..2^6 (bf16/fp16), rows shorter than the paper's 2^7 (NEXT-2)"
         if qkq:
             metric = ("FWHT + FP8-E4M3 quantization of the Q and K heads of fused QKV activations [T, 3, H, n] "
@@ -682,11 +881,14 @@ def main():
                       "HBM GB/s vs n=2^7..2^15")
         if args.ns:
             metric = metric.replace("n=2^7..2^15", f"n in {{{args.ns}}}")
+        if args.inplace and not rotate:
+            metric += " [in place]"
         line = {
             "metric": metric, "value": round(value, 1), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(t_max / args.steps, 4), "higher_is_better": True,
             "scaling": "strong" if c5 else "weak", "vs_baseline": None,
-            "dtype": "fp32" if f32 else ("bf16 (fp32 last-stage accumulate)" if c5 else
+            "dtype": "fp32" if f32 else ("bf16 (fp32 last-stage accumulate)" if wl in ("c5", "c2") else
+                                         "fp16 (fp32 last-stage accumulate)" if wl == "c4" else
                                          "fp16+bf16 (fp32 last-stage accumulate)"),
             "data": "synthetic (counter-based N(0,1), synthetic/)", "config": config_block(args, world),
             "pct_of_8TBps": round(100.0 * value / world / NOMINAL_HBM_GBS, 2),
@@ -697,9 +899,13 @@ def main():
             "gpu_launches": int(args.steps * sum(hc.launches_per_call(elems_of[(dt, n)] // n, n, dt) for dt, n in pairs)),
             "clocks": clocks, "remeasured_for_clocks": remeasured, "check": check,
         }
+        if args.misshard:
+            line["negative_control"] = "--misshard: rank %d generated its rows one base row off" % (world - 1)
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()
+    if check is not None and not check["pass"]:
+        sys.exit(3)
 
 
 if __name__ == "__main__":

@@ -79,7 +79,7 @@ typedef enum {
   HADACORE_ERR_MISALIGNED = 4,  /* in or out is not 16-byte aligned */
   HADACORE_ERR_OVERLAP = 5,     /* in != out and the two byte ranges overlap */
   HADACORE_ERR_DTYPE = 6,       /* unknown dtype */
-  HADACORE_ERR_SCALE = 7,       /* scale is NaN or +-Inf */
+  HADACORE_ERR_SCALE = 7,       /* scale is NaN, +-Inf, zero or negative (scale > 0) */
   HADACORE_ERR_CUDA = 8,        /* CUDA error (no device, launch failure, copy failure) */
   HADACORE_ERR_WORKSPACE = 9    /* hadacore_fwht_host: workspace NULL or too small */
 } hadacore_status_t;

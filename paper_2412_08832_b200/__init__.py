@@ -12,7 +12,8 @@ library is missing or no GPU is present, calls raise.
 ``x`` is a CUDA tensor of dtype float16 or bfloat16 whose last dimension n is a
 power of two in [2, 32768] (the paper's 2^7..2^15, plus n = 2..64: SURVEY.md 8(f)
 NEXT-2); all leading dimensions are rows (m = numel / n).  The strided entry
-point takes n = 2^7..2^15.
+points take n = 2^3..2^15 (rows of >= 16 bytes: TMA boxes).  ``scale`` must be
+finite and > 0.
 """
 from __future__ import annotations
 
@@ -195,8 +196,10 @@ def hadacore_fwht_quant(x: torch.Tensor, qtype: str = "e4m3", scale: float | Non
         row_scale = torch.empty(x.shape[:-1], dtype=torch.float32, device=x.device)
     if out.dtype != qdt or tuple(out.shape) != tuple(qshape) or not out.is_contiguous() or out.device != x.device:
         raise HadacoreError(ARG_ERROR, f"out must be a contiguous {qdt} tensor of shape {tuple(qshape)} on x's device")
-    if row_scale.dtype != torch.float32 or row_scale.numel() != m or not row_scale.is_contiguous():
-        raise HadacoreError(ARG_ERROR, "row_scale must be a contiguous float32 tensor with one entry per row")
+    if row_scale.dtype != torch.float32 or row_scale.numel() != m or not row_scale.is_contiguous() \
+            or row_scale.device != x.device:
+        raise HadacoreError(ARG_ERROR, "row_scale must be a contiguous float32 tensor with one entry per row on "
+                                       "x's device")
     if scale is None:
         scale = 1.0 / math.sqrt(n) if n > 0 else 1.0
     with torch.cuda.device(x.device):
@@ -239,8 +242,8 @@ def hadacore_fwht_strided(x: torch.Tensor, out: torch.Tensor | None = None, scal
         raise HadacoreError(ARG_ERROR, "x must be a CUDA view with a contiguous last dimension")
     if out is None:
         out = torch.empty(x.shape, dtype=x.dtype, device=x.device)
-    if out.shape != x.shape or out.dtype != x.dtype or out.stride(-1) != 1:
-        raise HadacoreError(ARG_ERROR, "out must have x's shape and dtype and a contiguous last dimension")
+    if out.shape != x.shape or out.dtype != x.dtype or out.stride(-1) != 1 or out.device != x.device:
+        raise HadacoreError(ARG_ERROR, "out must have x's shape, dtype and device and a contiguous last dimension")
 
     mo, mi, so, si = _row_grid(x, n)
     if out.is_contiguous():  # rows in (i, j) order: any grid maps onto it
@@ -311,8 +314,9 @@ def hadacore_fwht_quant_strided(x: torch.Tensor, qtype: str = "e4m3", scale: flo
     rs = row_scale if row_scale is not None else torch.empty(x.shape[:-1], dtype=torch.float32, device=x.device)
     if q.dtype != qdt or q.numel() != m * qshape[-1] or not q.is_contiguous() or q.device != x.device:
         raise HadacoreError(ARG_ERROR, f"out must be a contiguous {qdt} tensor of {m * qshape[-1]} elements on x's device")
-    if rs.dtype != torch.float32 or rs.numel() != m or not rs.is_contiguous():
-        raise HadacoreError(ARG_ERROR, "row_scale must be a contiguous float32 tensor with one entry per row")
+    if rs.dtype != torch.float32 or rs.numel() != m or not rs.is_contiguous() or rs.device != x.device:
+        raise HadacoreError(ARG_ERROR, "row_scale must be a contiguous float32 tensor with one entry per row on "
+                                       "x's device")
     mo, mi, so, si = _row_grid(x, n)
     if scale is None:
         scale = 1.0 / math.sqrt(n) if n > 0 else 1.0

@@ -437,11 +437,16 @@ hadacore_status_t dispatch_n(const void* in, void* out, uint8_t* q, float* rs, c
 
 Layout contiguous(int64_t m, int64_t n) { return Layout{m, 1, n, n, n, n}; }
 
-// hadacore_fwht / hadacore_fwht_host: n = 2..2^15 (n < 128: NEXT-2, fwht_small_kernel);
-// the strided and fused-quantization entry points: the paper's range 2^7..2^15.
+// hadacore_fwht / hadacore_fwht_host / hadacore_fwht_quant: n = 2..2^15 (n < 128: NEXT-2,
+// fwht_small_kernel); the strided entry points: n = 8..2^15 (rows of >= 16 bytes, TMA).
 bool valid_n(int64_t n) { return n >= 2 && n <= 32768 && (n & (n - 1)) == 0; }
 
 size_t elem_size(int dtype) { return dtype == HADACORE_F32 ? 4 : 2; }
+
+// SPEC S:57 (TransformOptions): scale > 0 and finite.  A zero scale would also break
+// the fused quantization's contract (row_scale = 1 and zero codes for y == 0): its fast
+// path decides on the pre-scale row maximum.
+bool valid_scale(float scale) { return std::isfinite(scale) && scale > 0.f; }
 
 template <int N>
 hadacore_status_t launch_f32(const void* in, void* out, int64_t m, float scale, cudaStream_t stream) {
@@ -585,7 +590,7 @@ hadacore_status_t validate(const void* in, const void* out, int64_t m, int64_t n
   if (dtype != HADACORE_F16 && dtype != HADACORE_BF16 && dtype != HADACORE_F32) return HADACORE_ERR_DTYPE;
   if (!valid_n(n)) return HADACORE_ERR_INVALID_N;
   if (m < 0 || m > INT64_MAX / (int64_t(elem_size(dtype)) * n)) return HADACORE_ERR_INVALID_M;
-  if (!std::isfinite(scale)) return HADACORE_ERR_SCALE;
+  if (!valid_scale(scale)) return HADACORE_ERR_SCALE;
   if (m == 0) return HADACORE_OK;
   if (!in || !out) return HADACORE_ERR_NULL;
   if (device_buffers && ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 15u))
@@ -674,7 +679,7 @@ extern "C" hadacore_status_t hadacore_fwht_strided(const void* in, void* out, in
   if (!valid_n(n) || n < 8) return HADACORE_ERR_INVALID_N;  // row grids: rows of >= 16 bytes (TMA)
   if (m_outer < 0 || m_inner < 0 || m_outer > (int64_t(1) << 31) || m_inner > (int64_t(1) << 31))
     return HADACORE_ERR_INVALID_M;
-  if (!std::isfinite(scale)) return HADACORE_ERR_SCALE;
+  if (!valid_scale(scale)) return HADACORE_ERR_SCALE;
   if (m_outer == 0 || m_inner == 0) return HADACORE_OK;
   if (!in || !out) return HADACORE_ERR_NULL;
   const Layout L{m_outer, m_inner, in_stride_outer, m_inner > 1 ? in_stride_inner : n, out_stride_outer,
@@ -707,7 +712,7 @@ extern "C" hadacore_status_t hadacore_fwht_quant_strided(const void* in, void* o
   if (!valid_n(n) || n < 8) return HADACORE_ERR_INVALID_N;  // row grids: rows of >= 16 bytes (TMA)
   if (m_outer < 0 || m_inner < 0 || m_outer > (int64_t(1) << 31) || m_inner > (int64_t(1) << 31))
     return HADACORE_ERR_INVALID_M;
-  if (!std::isfinite(scale)) return HADACORE_ERR_SCALE;
+  if (!valid_scale(scale)) return HADACORE_ERR_SCALE;
   if (m_outer == 0 || m_inner == 0) return HADACORE_OK;
   if (!in || !out_q || !row_scale) return HADACORE_ERR_NULL;
   const int64_t si = m_inner > 1 ? in_stride_inner : n;
@@ -831,7 +836,9 @@ int log2_pow2(int64_t n) {
 }
 int lab_grid(int64_t work_items, int per_block) {
   const int64_t b = (work_items + per_block - 1) / per_block;
-  const int64_t cap = int64_t(sm_count(0)) * 16;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) dev = 0;
+  const int64_t cap = int64_t(sm_count(dev)) * 16;  // the current device's SMs
   return int(b < 1 ? 1 : (b < cap ? b : cap));
 }
 }  // namespace
@@ -885,7 +892,7 @@ extern "C" const char* hadacore_status_string(hadacore_status_t s) {
     case HADACORE_ERR_MISALIGNED: return "in/out must be 16-byte aligned";
     case HADACORE_ERR_OVERLAP: return "in and out partially overlap (only in == out is allowed)";
     case HADACORE_ERR_DTYPE: return "unsupported dtype / qtype for this entry point";
-    case HADACORE_ERR_SCALE: return "scale must be finite";
+    case HADACORE_ERR_SCALE: return "scale must be finite and > 0";
     case HADACORE_ERR_CUDA: return "CUDA error (see cudaGetLastError)";
     case HADACORE_ERR_WORKSPACE: return "workspace NULL, misaligned or smaller than two rows";
   }

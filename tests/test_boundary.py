@@ -79,6 +79,10 @@ def test_validation_codes(lib):
     assert call(lib, a, b, 4, 256, dtype=-1) == DTYPE
     assert call(lib, a, b, 4, 256, scale=float("nan")) == SCALE
     assert call(lib, a, b, 4, 256, scale=float("inf")) == SCALE
+    assert call(lib, a, b, 4, 256, scale=0.0) == SCALE              # scale > 0
+    assert call(lib, a, b, 4, 256, scale=-0.0) == SCALE
+    assert call(lib, a, b, 4, 256, scale=-0.5) == SCALE
+    assert call(lib, a, b, 4, 64, scale=-1.0) == SCALE
     assert call(lib, None, b, 4, 256) == NULL
     assert call(lib, a, None, 4, 256) == NULL
     assert call(lib, a + 8, b, 4, 256) == MISALIGNED
@@ -98,6 +102,7 @@ def test_host_entry_validation(lib):
     assert f(a, b, 4, 256, 0, 1.0, ws, 1000, None) == WORKSPACE     # < two rows
     assert f(a, b, 4, 256, 0, 1.0, ws + 4, 1 << 20, None) == WORKSPACE
     assert f(a, a + 2, 4, 256, 0, 1.0, ws, 1 << 20, None) == OVERLAP
+    assert f(a, b, 4, 256, 0, 0.0, ws, 1 << 20, None) == SCALE
     assert f(None, None, 0, 256, 0, 1.0, None, 0, None) == OK
 
 
@@ -111,6 +116,9 @@ def test_quant_entry_validation(lib):
     assert f(a, q, rs, 4, 1, 0, 0, 1.0, None) == INVALID_N       # fused quantization: n = 2..2^15
     assert f(a, q, rs, 4, 65536, 0, 0, 1.0, None) == INVALID_N
     assert f(a, q, rs, 4, 256, 0, 1, float("nan"), None) == SCALE
+    assert f(a, q, rs, 4, 256, 0, 0, 0.0, None) == SCALE            # scale > 0
+    assert f(a, q, rs, 4, 256, 0, 2, -1.0, None) == SCALE
+    assert f(a, q, rs, 4, 16, 1, 0, -0.25, None) == SCALE
     assert f(a, None, rs, 4, 256, 0, 0, 1.0, None) == NULL
     assert f(a, q, None, 4, 256, 0, 0, 1.0, None) == NULL
     assert f(a, q + 8, rs, 4, 256, 0, 0, 1.0, None) == MISALIGNED
@@ -172,6 +180,8 @@ def test_strided_entry_validation(lib):
     assert f(a, a + 256, 4, 3, 384, 128, 384, 128, 128, 0, 1.0, None) == OVERLAP    # extents overlap
     assert f(a + 2, b, 4, 3, 384, 128, 384, 128, 128, 0, 1.0, None) == MISALIGNED
     assert f(None, None, 0, 3, 384, 128, 384, 128, 128, 0, 1.0, None) == OK
+    assert f(a, b, 4, 3, 384, 128, 384, 128, 128, 0, 0.0, None) == SCALE
+    assert f(a, b, 4, 3, 384, 128, 384, 128, 128, 0, -2.0, None) == SCALE
 
 
 def test_lab_entry_validation(lib):
@@ -204,6 +214,8 @@ def test_quant_strided_entry_validation(lib):
     assert f(a, q, rs, 4, 3, 384, 128, 4, 0, 0, 1.0, None) == INVALID_N      # n >= 8 (16-byte TMA rows)
     assert f(a, q, rs, 4, 3, 384, 64, 128, 0, 0, 1.0, None) == INVALID_M     # inner rows overlap
     assert f(a, q, rs, 4, 3, 384, 128, 128, 0, 0, float("inf"), None) == SCALE
+    assert f(a, q, rs, 4, 3, 384, 128, 128, 0, 0, 0.0, None) == SCALE
+    assert f(a, q, rs, 4, 3, 384, 128, 128, 0, 0, -1.0, None) == SCALE
     assert f(a, None, rs, 4, 3, 384, 128, 128, 0, 0, 1.0, None) == NULL
     assert f(a + 8, q, rs, 4, 3, 384, 128, 128, 0, 0, 1.0, None) == MISALIGNED
     assert f(a, a + 256, rs, 4, 3, 384, 128, 128, 0, 0, 1.0, None) == OVERLAP
