@@ -103,32 +103,79 @@ def ncu_traffic(workload: str = "fwht"):
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons, sampled while the timed region runs."""
+    """SM clocks + clock-event (throttle) reasons sampled while the timed region runs: NVML
+    polled every ~2 ms from a thread (a 3 ms step still gets samples), falling back to
+    `nvidia-smi -lms 20` when NVML is unavailable."""
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, index: int):
         self.index = index
-        self.rows = []
+        self.rows = []  # (time, sm_mhz, sm_max_mhz, reasons)
         self.proc = None
+        self.stop = threading.Event()
         self.t0 = self.t1 = None
+        self.source = None
 
     def __enter__(self):
         try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.physical_index())
+            bits = {"hw_slowdown": pynvml.nvmlClocksEventReasonHwSlowdown,
+                    "hw_thermal_slowdown": pynvml.nvmlClocksEventReasonHwThermalSlowdown,
+                    "sw_thermal_slowdown": pynvml.nvmlClocksEventReasonSwThermalSlowdown,
+                    "sw_power_cap": pynvml.nvmlClocksEventReasonSwPowerCap}
+            smax = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+
+            def poll():
+                while not self.stop.is_set():
+                    try:
+                        sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                        r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                        self.rows.append((time.time(), float(sm), float(smax),
+                                          {nm for nm, b in bits.items() if r & b}))
+                    except Exception:
+                        pass
+                    time.sleep(0.002)
+            self.reader = threading.Thread(target=poll, daemon=True)
+            self.reader.start()
+            self.source = "NVML, 2 ms polling"
+            time.sleep(0.05)
+            return self
+        except Exception:
+            pass
+        try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                                          "-lms", "20", "-i", str(self.index)], stdout=subprocess.PIPE,
+                                          "-lms", "20", "-i", str(self.physical_index())], stdout=subprocess.PIPE,
                                          stderr=subprocess.DEVNULL, text=True)
             self.reader = threading.Thread(target=self._read, daemon=True)
             self.reader.start()
+            self.source = "nvidia-smi -lms 20"
             time.sleep(0.3)
         except Exception:
             self.proc = None
         return self
 
+    def physical_index(self):
+        vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+        if vis:
+            try:
+                return int(vis.split(",")[self.index])
+            except (ValueError, IndexError):
+                pass
+        return self.index
+
     def _read(self):
         for line in self.proc.stdout:
-            self.rows.append((time.time(), line.strip()))
+            f = [v.strip() for v in line.strip().split(",")]
+            try:
+                self.rows.append((time.time(), float(f[0]), float(f[1]),
+                                  {nm for nm, v in zip(self.NAMES, f[4:8]) if v.lower() == "active"}))
+            except Exception:
+                continue
 
     def mark_start(self):
         self.t0 = time.time()
@@ -137,6 +184,7 @@ class ClockSampler:
         self.t1 = time.time()
 
     def __exit__(self, *a):
+        self.stop.set()
         if self.proc:
             time.sleep(0.05)
             self.proc.terminate()
@@ -147,23 +195,14 @@ class ClockSampler:
 
     def summary(self):
         if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
-        inside = [r for t, r in self.rows if self.t0 is not None and self.t0 <= t <= (self.t1 or t)]
-        use = inside if inside else [r for _, r in self.rows]
-        sm, smax, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for r in use:
-            f = [v.strip() for v in r.split(",")]
-            try:
-                sm.append(float(f[0]))
-                smax.append(float(f[1]))
-            except Exception:
-                continue
-            for nm, v in zip(names, f[4:8]):
-                if v.lower() == "active":
-                    reasons.add(nm)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
-                "reasons": sorted(reasons), "samples": len(use), "samples_in_timed_region": len(inside)}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["clock sampling unavailable"], "samples": 0}
+        inside = [r for r in self.rows if self.t0 is not None and self.t0 <= r[0] <= (self.t1 or r[0])]
+        use = inside if inside else self.rows
+        sm = [r[1] for r in use]
+        reasons = set().union(*[r[3] for r in use])
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(r[2] for r in use),
+                "reasons": sorted(reasons), "samples": len(use), "samples_in_timed_region": len(inside),
+                "source": self.source}
 
 
 def dist_setup(args):

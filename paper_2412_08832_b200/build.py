@@ -32,15 +32,31 @@ def needs_build() -> bool:
     return any(os.path.getmtime(d) > t for d in DEPS)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not needs_build():
-        return LIB
-    tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "-shared",
-           "-Xptxas", "-v" if verbose else "-O3", "-I", os.path.join(ROOT, "include"),
-           "-o", tmp, *SOURCES]
-    subprocess.check_call(cmd)
-    os.replace(tmp, LIB)
+# Negative-control library (tests/test_gpu_edge.py): the same source with one sign of the
+# H_16 constant flipped (-DHC_NEGCTL); the parity tests must FAIL on it.  Test
+# infrastructure only -- the Python binding never loads it.
+LIB_NEGCTL = os.path.join(HERE, "libhadacore_negctl.so")
+
+
+def _cmd(out: str, defines=(), verbose: bool = False):
+    return [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "-shared",
+            "-Xptxas", "-v" if verbose else "-O3", "-I", os.path.join(ROOT, "include"), *defines,
+            "-o", out, *SOURCES]
+
+
+def build(force: bool = False, verbose: bool = False, negctl: bool = True) -> str:
+    """Build libhadacore.so (and, with negctl, the negative-control library in parallel)."""
+    jobs = []
+    if force or needs_build():
+        jobs.append((LIB, _cmd(LIB + f".tmp{os.getpid()}", (), verbose)))
+    if negctl and (force or not os.path.exists(LIB_NEGCTL) or
+                   any(os.path.getmtime(d) > os.path.getmtime(LIB_NEGCTL) for d in DEPS)):
+        jobs.append((LIB_NEGCTL, _cmd(LIB_NEGCTL + f".tmp{os.getpid()}", ("-DHC_NEGCTL",), False)))
+    procs = [(dst, cmd[cmd.index("-o") + 1], subprocess.Popen(cmd)) for dst, cmd in jobs]
+    for dst, tmp, p in procs:
+        if p.wait() != 0:
+            raise subprocess.CalledProcessError(p.returncode, "nvcc " + os.path.basename(dst))
+        os.replace(tmp, dst)
     return LIB
 
 

@@ -299,6 +299,9 @@ __device__ __forceinline__ void mma_pk(const uint32_t a[4], uint32_t b0, uint32_
 // (unnormalized +-1) if (hmask >> q) & 1, else I_2.
 __device__ __forceinline__ float kron_entry(uint32_t hmask, int i, int k) {
   int sgn = 0;
+#ifdef HC_NEGCTL  // negative-control build (tests/test_gpu_edge.py): one sign of H_16 flipped
+  if (hmask == 0xFu && i == 3 && k == 5) sgn = 1;
+#endif
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     const int bi = (i >> q) & 1, bk = (k >> q) & 1;

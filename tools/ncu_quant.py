@@ -1,7 +1,7 @@
 """One fused FWHT+quantization launch per (dtype, n) at 2^28 elements after one warm-up
 pass (ncu captures: -k regex:fwht -s <2*len(ns)> -c <2*len(ns)>).
 
-    python tools/ncu_quant.py [ns] [e4m3|int8]"""
+    python tools/ncu_quant.py [ns] [e4m3|int8|int4]"""
 import os
 import sys
 
@@ -20,5 +20,6 @@ for _ in range(2):
     for dt in (torch.float16, torch.bfloat16):
         for n in ns:
             x = src.view(torch.int16).view(dt).view(-1, n)
-            hc.hadacore_fwht_quant(x, qtype=qtype, out=q.view(-1, n), row_scale=sc[: x.shape[0]])
+            hc.hadacore_fwht_quant(x, qtype=qtype, out=q[: elems // (2 if qtype == "int4" else 1)].view(
+                -1, n // 2 if qtype == "int4" else n), row_scale=sc[: x.shape[0]])
 torch.cuda.synchronize()
