@@ -375,6 +375,24 @@ __device__ __forceinline__ void stage_da_f32(const uint32_t x[4], const uint32_t
   mma_f32<DT>(x, bc0[0], bc0[1], d);      // output columns 0..7  -> regs R0 (rows g), R1 (rows g+8)
   mma_f32<DT>(x, bc1[0], bc1[1], d + 4);  // output columns 8..15 -> R2, R3
 }
+// Packed fp32 butterfly on two adjacent pairs (SASS FADD2, sm_100): (a0, a1), (b0, b1) <-
+// (a + b, a - b) element-wise, IEEE round-to-nearest like two scalar FADDs -- half the
+// issue slots of the scalar butterflies (P:50-64 listing's x + y, x - y).
+__device__ __forceinline__ void bfly2(float& a0, float& a1, float& b0, float& b1) {
+#ifdef HC_SCALAR_BFLY  // A/B builds: scalar FADDs
+  const float s0 = a0 + b0, s1 = a1 + b1, d0 = a0 - b0, d1 = a1 - b1;
+  a0 = s0; a1 = s1; b0 = d0; b1 = d1;
+#else
+  asm("{.reg .b64 a, b, s, d;\n mov.b64 a, {%0,%1};\n mov.b64 b, {%2,%3};\n add.rn.f32x2 s, a, b;\n"
+      " sub.rn.f32x2 d, a, b;\n mov.b64 {%0,%1}, s;\n mov.b64 {%2,%3}, d;}"
+      : "+f"(a0), "+f"(a1), "+f"(b0), "+f"(b1));
+#endif
+}
+// fp32 butterflies between two 8-value fragments (a chunk bit held across a lane's fragments)
+__device__ __forceinline__ void bfly8(float a[8], float b[8]) {
+#pragma unroll
+  for (int e = 0; e < 8; e += 2) bfly2(a[e], a[e + 1], b[e], b[e + 1]);
+}
 // Two chunk-bit groups at once (n >= 8192): H_16 over the A fragment's column bits as a
 // data-as-A stage (layout kept), then H_2 over the fragment's row-half bit (the ldmatrix
 // matrix index bit j0: d[0..1], d[4..5] are rows g, d[2..3], d[6..7] rows g + 8) as fp32
@@ -384,14 +402,8 @@ template <int DT>
 __device__ __forceinline__ void stage_da_j0_f32(const uint32_t x[4], const uint32_t bc0[2], const uint32_t bc1[2],
                                                 float d[8]) {
   stage_da_f32<DT>(x, bc0, bc1, d);
-#pragma unroll
-  for (int h = 0; h < 8; h += 4)
-#pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      const float p0 = d[h + e], p1 = d[h + 2 + e];
-      d[h + e] = p0 + p1;
-      d[h + 2 + e] = p0 - p1;
-    }
+  bfly2(d[0], d[1], d[2], d[3]);
+  bfly2(d[4], d[5], d[6], d[7]);
 }
 #ifdef HC_J0_MMA
 constexpr bool kJ0Mma = true;
@@ -400,10 +412,22 @@ constexpr bool kJ0Mma = false;
 #endif
 
 // fp32 epilogue: * s_res (exact normalization remainder), one RNE rounding to 16 bits.
+// The multiplies are packed (mul.rn.f32x2, SASS FMUL2: IEEE-identical to two FMULs).
 template <int DT>
 __device__ __forceinline__ void scale_pack(const float d[8], float s_res, uint32_t y[4]) {
 #pragma unroll
-  for (int i = 0; i < 4; ++i) y[i] = pack2<DT>(d[2 * i] * s_res, d[2 * i + 1] * s_res);
+  for (int i = 0; i < 4; ++i) {
+    float a = d[2 * i], b = d[2 * i + 1];
+#ifndef HC_SCALAR_BFLY
+    asm("{.reg .b64 t, s;\n mov.b64 t, {%0,%1};\n mov.b64 s, {%2,%2};\n mul.rn.f32x2 t, t, s;\n mov.b64 {%0,%1}, t;}"
+        : "+f"(a), "+f"(b)
+        : "f"(s_res));
+#else
+    a *= s_res;
+    b *= s_res;
+#endif
+    y[i] = pack2<DT>(a, b);
+  }
 }
 
 // ------------------------------------------------------------------ SIMT ablation
@@ -1370,14 +1394,7 @@ __global__ void __launch_bounds__((NT + 1) * 32, CTAS)
           for (int b = 0; b < PL::nx; ++b)
 #pragma unroll
             for (int xi = 0; xi < (1 << PL::nx); ++xi)
-              if (!((xi >> b) & 1)) {
-#pragma unroll
-                for (int e = 0; e < 8; ++e) {
-                  const float p0 = dd[xi][e], p1 = dd[xi | (1 << b)][e];
-                  dd[xi][e] = p0 + p1;
-                  dd[xi | (1 << b)][e] = p0 - p1;
-                }
-              }
+              if (!((xi >> b) & 1)) bfly8(dd[xi], dd[xi | (1 << b)]);
 #pragma unroll
           for (int xi = 0; xi < (1 << PL::nx); ++xi) {
             uint32_t z[4];
@@ -1552,14 +1569,7 @@ __global__ void __launch_bounds__((NT + 1) * 32, CTAS)
         for (int b = 0; b < PL::nx; ++b)
 #pragma unroll
           for (int xi = 0; xi < (1 << PL::nx); ++xi)
-            if (!((xi >> b) & 1)) {
-#pragma unroll
-              for (int e = 0; e < 8; ++e) {
-                const float p0 = d[xi][e], p1 = d[xi | (1 << b)][e];
-                d[xi][e] = p0 + p1;
-                d[xi | (1 << b)][e] = p0 - p1;
-              }
-            }
+            if (!((xi >> b) & 1)) bfly8(d[xi], d[xi | (1 << b)]);
 #pragma unroll
         for (int xi = 0; xi < (1 << PL::nx); ++xi) {
           uint32_t z[4];

@@ -122,12 +122,39 @@ template <int N> struct TunedSQ : TunedSQ0<N> {};
 struct TunedSmallM { static constexpr int nt = 4, tkb = 2, st = 2, u = 1, ctas = 1; };
 constexpr int QT_SMALLM = -2;  // kernels treat every QT < 0 as the plain transform
 
+// Mid-size problems (n = 512..4096, contiguous, at most HC_MIDM_MB MiB of input, i.e. up to
+// 2^26 elements -- BASELINE C4 is 2^26): the whole launch is a few tiles per SM, so the ramp
+// (first loads) and the tail (last tiles' phase 1 -> phase 2 -> store chain) dominate; 8 KiB
+// tiles and 2 CTAs of 8 consumer warps per SM start more independent pipelines.  Selected at
+// run time as the QT_MIDM instantiation.  Paired sweep (tools/midsize.py, 8 variants x n x
+// 2^22..2^26, profiles/r02_midsize.md): n = 4096 at 2^24 elements 6243 -> 6494 GB/s warm
+// (n = 256: 6772); n = 8192..32768 were no better and keep the main table.  HC_MIDM_* macros
+// override the table for A/B builds (HC_MIDM_MB=0 disables it).
+#ifndef HC_MIDM_MB
+#define HC_MIDM_MB 128
+#endif
+#ifndef HC_MIDM_MAXN
+#define HC_MIDM_MAXN 4096
+#endif
+template <int N> struct TunedMidM0 { static constexpr int nt = 8, tkb = 8, st = 4, u = 1, ctas = 2; };
+#ifdef HC_MIDM_NT
+template <int N> struct TunedMidM {
+  static constexpr int nt = HC_MIDM_NT, tkb = HC_MIDM_TKB, st = HC_MIDM_ST, u = 1, ctas = HC_MIDM_CTAS;
+};
+#else
+template <int N> struct TunedMidM : TunedMidM0<N> {};
+#endif
+constexpr int QT_MIDM = -3;
+
 #ifdef HC_TUNE  // tools/tune.py: one configuration for every n, from -D macros
 template <int N, int QT>
 struct Knobs { static constexpr int nt = HC_NT, tkb = HC_TILE_KB, st = HC_STAGES, u = HC_U, ctas = HC_CTAS; };
 #else
 template <int N, int QT>
-struct Knobs : std::conditional_t<(QT >= 0), TunedQ<N>, std::conditional_t<(QT == QT_SMALLM), TunedSmallM, Tuned<N>>> {};
+struct Knobs
+    : std::conditional_t<(QT >= 0), TunedQ<N>,
+                         std::conditional_t<(QT == QT_SMALLM), TunedSmallM,
+                                            std::conditional_t<(QT == QT_MIDM), TunedMidM<N>, Tuned<N>>>> {};
 #endif
 
 template <int N, int QT = -1>
@@ -258,6 +285,10 @@ hadacore_status_t launch(const void* in, void* out, uint8_t* out_q, float* row_s
   if constexpr (N <= 256 && QT == QT_NONE) {
     if (L.m_inner == 1 && L.in_so == N && L.out_so == N && L.m_outer * N * 2 <= (int64_t(4) << 20))
       return launch<N, DT, QT_SMALLM>(in, out, out_q, row_scale, L, scale, stream);
+  }
+  if constexpr (N > 256 && N <= HC_MIDM_MAXN && QT == QT_NONE && HC_MIDM_MB > 0) {
+    if (L.m_inner == 1 && L.in_so == N && L.out_so == N && L.m_outer * N * 2 <= (int64_t(HC_MIDM_MB) << 20))
+      return launch<N, DT, QT_MIDM>(in, out, out_q, row_scale, L, scale, stream);
   }
 #endif
   using C = Cfg<N, QT>;

@@ -138,8 +138,11 @@ def test_r14_subnormal_rows_derived_bound(hc, n, dtype):
     err = np.linalg.norm(y - ref, axis=1)
     bound = roundings(n) / 2.0 * (u * math.sqrt(n) + fi.eps * np.linalg.norm(xs, axis=1))
     assert np.all(err <= bound), (err / bound).max()
-    # and the result is not flushed to zero
-    assert np.all(np.linalg.norm(y, axis=1) >= 0.5 * np.linalg.norm(ref, axis=1))
+    # and the result is not flushed to zero: rows whose exact result is well above the
+    # bound keep their magnitude (rows at the spacing level may legitimately round to 0)
+    big = np.linalg.norm(ref, axis=1) > 4 * bound
+    assert big.sum() >= 4
+    assert np.all(np.linalg.norm(y[big], axis=1) >= 0.5 * np.linalg.norm(ref[big], axis=1))
 
 
 # ---------------------------------------------------------------- canary borders

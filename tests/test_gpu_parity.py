@@ -349,3 +349,22 @@ def test_torch_op_quant_on_strided_view(hc):
     q, s = torch.ops.hadacore.fwht_quant(qkv[:, 0:2], "e4m3", None)
     q2, s2 = hc.hadacore_fwht_quant(qkv[:, 0:2].contiguous(), "e4m3")
     assert torch.equal(q.view(torch.uint8), q2.view(torch.uint8)) and torch.equal(s, s2)
+
+
+@pytest.mark.parametrize("dtype", DTYPES, ids=["fp16", "bf16"])
+@pytest.mark.parametrize("n", [512, 1024, 2048, 4096])
+def test_midsize_and_main_configs_agree(hc, n, dtype):
+    """n = 512..4096 launches of <= 128 MiB run the mid-size instantiation (8 KiB tiles, 2 CTAs
+    per SM; hadacore.cu TunedMidM), larger ones the main table (16 KiB tiles).  A launch just
+    above the threshold (main config, ragged tail) matches the oracle on sampled rows, and its
+    rows are bitwise equal to the same rows transformed by small launches (mid-size config):
+    results do not depend on the launch configuration."""
+    m = (128 << 20) // (2 * n) + 3 * (16384 // (2 * n)) + 1
+    x = torch.empty(m, n, dtype=dtype, device="cuda")
+    synthetic.generate(m, n, dtype, synthetic.seed_for(2, dtype), out=x)
+    y = hc.hadacore_fwht(x)
+    rows = sorted(set([0, 1, m // 2, m - 2, m - 1] + torch.randint(0, m, (200,), generator=torch.Generator().manual_seed(n)).tolist()))
+    assert rel_l2_rows(widen(y[rows]), oracle.fwht(widen(x[rows]))).max() <= TOL[dtype]
+    for r0 in (0, m // 2 - 37, m - 101):
+        ys = hc.hadacore_fwht(x[r0:r0 + 101].contiguous())
+        assert torch.equal(ys.view(torch.int16), y[r0:r0 + 101].view(torch.int16)), r0
