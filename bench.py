@@ -742,6 +742,22 @@ def main():
         remeasured = True
     # per-launch breakdown: a separate pass after the timed region
     _, per = timed_region(max(3, min(args.steps, 10)), True)
+    # per-(dtype, n) rate: back-to-back launches of one (dtype, n) between two events (the
+    # per-launch events above break programmatic dependent launch, so they understate a
+    # kernel's rate inside a run of launches, most for the shortest launches)
+    per_pair_ms = {}
+    if not scrub:
+        reps = max(3, min(args.steps, 10))
+        for dt, n in pairs:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            launch(dt, n)
+            torch.cuda.synchronize()
+            e0.record(stream)
+            for _ in range(reps):
+                launch(dt, n)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            per_pair_ms[(dt, n)] = e0.elapsed_time(e1) / reps
 
     # output checks outside the timed regions, on every rank:
     # (1) a property that holds at any size: the normalized transform preserves
@@ -823,7 +839,7 @@ def main():
     per_n = {}
     for k, (dt, n) in enumerate(pairs):
         ts = sorted(per[k::len(pairs)])
-        med = ts[len(ts) // 2]
+        med = per_pair_ms.get((dt, n), ts[len(ts) // 2])
         b_n = 2.0 * esize * elems_of[(dt, n)] if not quant else (2.0 + qb) * args.elems + 4.0 * (args.elems // n)
         if qkq:
             b_n = 3.0 * elems_of[(dt, n)] + 4.0 * elems_of[(dt, n)] / n
@@ -933,7 +949,10 @@ def main():
             "pct_of_8TBps": round(100.0 * value / world / NOMINAL_HBM_GBS, 2),
             # north_star: "reported ... both as GB/s and elements/s" (whole job, all ranks)
             "elements_per_s": float(f"{(C5_ELEMS * args.steps if c5 else sum(elems_of[p] for p in pairs) * args.steps * world) / (t_max * 1e-3):.4g}"),
-            "per_n_GBps": per_n, "launch_us_p10_p50_p90": launch_pct, "inplace": bool(args.inplace),
+            "per_n_GBps": per_n,
+            "per_n_source": ("sum of per-launch events (L2 scrubbed between launches)" if scrub else
+                             "back-to-back launches of each (dtype, n), CUDA events around the group"),
+            "launch_us_p10_p50_p90": launch_pct, "inplace": bool(args.inplace),
             "roofline": roofline, "cpu_baseline": cpu_baseline, "e2e": e2e,
             "gpu_launches": int(args.steps * sum(hc.launches_per_call(elems_of[(dt, n)] // n, n, dt) for dt, n in pairs)),
             "clocks": clocks, "remeasured_for_clocks": remeasured, "check": check,

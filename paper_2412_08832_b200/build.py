@@ -14,7 +14,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libhadacore.so")
 SOURCES = [os.path.join(CSRC, "hadacore.cu")]
-DEPS = SOURCES + [os.path.join(CSRC, "fwht_kernel.cuh"), os.path.join(CSRC, "fwht_small.cuh"), os.path.join(CSRC, "quant_lab.cuh"), os.path.join(CSRC, "fwht_f32.cuh"), os.path.join(ROOT, "include", "hadacore.h")]
+DEPS = SOURCES + [os.path.join(CSRC, "fwht_kernel.cuh"), os.path.join(CSRC, "fwht_small.cuh"), os.path.join(CSRC, "quant_lab.cuh"), os.path.join(CSRC, "fwht_f32.cuh"), os.path.join(CSRC, "fwht_quant_tc.cuh"), os.path.join(ROOT, "include", "hadacore.h")]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -20,6 +20,7 @@
 #include "fwht_small.cuh"
 #include "fwht_f32.cuh"
 #include "quant_lab.cuh"
+#include "fwht_quant_tc.cuh"
 
 namespace hadacore {
 namespace {
@@ -278,9 +279,85 @@ bool ensure_smem_attr(Kern kern, int smem, std::atomic<uint64_t>& done, int dev)
   return true;
 }
 
+// Fused quantization on tcgen05 + TMEM (fwht_quant_tc.cuh) for rows of n >= HC_QTC_MINN
+// (contiguous or row grids): NA phase-A warps, NE epilogue warps, ST 64 KiB stages
+// (DESIGN.md §5).
+// HC_QTC_MINN = 0 disables it (A/B builds: the fwht_rows_kernel epilogue for every n).
+#ifndef HC_QTC_MINN
+#define HC_QTC_MINN 16384  // per-(qtype, n) A/B: profiles/r02_quant_tc_ab.txt
+#endif
+#ifndef HC_QTC_NA
+#define HC_QTC_NA 12
+#endif
+#ifndef HC_QTC_NE
+#define HC_QTC_NE 4
+#endif
+#ifndef HC_QTC_ST
+#define HC_QTC_ST 3
+#endif
+
+// 5-D view (64 elements, chunk [512 B], inner row, outer row, 64-element segment [128 B])
+// of a row grid; box (64, C, bi, bo, 2) with bi * bo = 128 / C rows, SWIZZLE_128B: half a
+// segment-major tile of 128 chunk lines per segment (fwht_quant_tc_kernel loads two).
+bool encode_tc_map(CUtensorMap* map, const void* base, const Layout& L, int n, const RowGrid& g) {
+  PFN_cuTensorMapEncodeTiled_v12000 enc = tensor_map_encoder();
+  if (!enc) return false;
+  const int C = n / 256;
+  cuuint64_t dims[5] = {64, cuuint64_t(C), cuuint64_t(L.m_inner), cuuint64_t(L.m_outer), 4};
+  cuuint64_t strides[4] = {512, cuuint64_t(2) * cuuint64_t(L.in_si), cuuint64_t(2) * cuuint64_t(L.in_so), 128};
+  cuuint32_t box[5] = {64, cuuint32_t(C), cuuint32_t(1u << g.lbi), cuuint32_t(g.bo), 2};  // half a tile
+  cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT16, 5, const_cast<void*>(base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// 4-D view (128 bytes, 128-byte line of a row's codes, inner row, outer row) of the codes
+// out_q (contiguous rows in (i, j) order); box (128, lines per row, bi, bo), SWIZZLE_128B:
+// fwht_quant_tc_kernel stages a tile's codes swizzled and stores them with one TMA copy.
+bool encode_tc_qmap(CUtensorMap* map, void* q, const Layout& L, int code_bytes, const RowGrid& g) {
+  PFN_cuTensorMapEncodeTiled_v12000 enc = tensor_map_encoder();
+  if (!enc) return false;
+  const int lines = code_bytes / 128;
+  cuuint64_t dims[4] = {128, cuuint64_t(lines), cuuint64_t(L.m_inner), cuuint64_t(L.m_outer)};
+  cuuint64_t strides[3] = {128, cuuint64_t(code_bytes), cuuint64_t(code_bytes) * cuuint64_t(L.m_inner)};
+  cuuint32_t box[4] = {128, cuuint32_t(lines), cuuint32_t(1u << g.lbi), cuuint32_t(g.bo)};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, q, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int N, int DT, int QT>
+hadacore_status_t launch_qtc(const void* in, uint8_t* out_q, float* row_scale, const Layout& L, float scale,
+                             cudaStream_t stream) {
+  constexpr int NA = HC_QTC_NA, NE = HC_QTC_NE, ST = HC_QTC_ST;
+  constexpr int smem = tc_smem_bytes<ST, NE>();
+  static_assert(smem <= 227 * 1024, "shared memory");
+  static std::atomic<uint64_t> attr_done{0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return HADACORE_ERR_CUDA;
+  auto kern = fwht_quant_tc_kernel<N, DT, QT, ST, NA, NE>;
+  if (!ensure_smem_attr(kern, smem, attr_done, dev)) return HADACORE_ERR_CUDA;
+  const RowGrid g = make_grid(L, 128 / (N / 256));
+  const int64_t max_ctas = kClc ? int64_t(INT32_MAX) : int64_t(sm_count(dev));
+  const int grid = int(g.num_tiles < max_ctas ? g.num_tiles : max_ctas);
+  CUtensorMap tin, tq;
+  if (!encode_tc_map(&tin, in, L, N, g) || !encode_tc_qmap(&tq, out_q, L, QT == QT_INT4 ? N / 2 : N, g))
+    return HADACORE_ERR_CUDA;
+  // phase A's constants carry 2^-stage_shift(mask_a); H_128 is +-1
+  const float s_res = std::ldexp(scale, stage_shift(PlanL<log2_n<N>() - 8>::mask_a));
+  if (launch_pdl(kern, grid, (NE + NA + 2) * 32, smem, stream, tin, tq, row_scale, g, s_res) != cudaSuccess)
+    return HADACORE_ERR_CUDA;
+  return cudaPeekAtLastError() == cudaSuccess ? HADACORE_OK : HADACORE_ERR_CUDA;
+}
+
 template <int N, int DT, int QT>
 hadacore_status_t launch(const void* in, void* out, uint8_t* out_q, float* row_scale, const Layout& L, float scale,
                          cudaStream_t stream) {
+  if constexpr (QT >= 0 && N >= 4096 && HC_QTC_MINN > 0 && N >= HC_QTC_MINN) {
+    return launch_qtc<N, DT, QT>(in, out_q, row_scale, L, scale, stream);
+  }
 #ifndef HC_TUNE
   if constexpr (N <= 256 && QT == QT_NONE) {
     if (L.m_inner == 1 && L.in_so == N && L.out_so == N && L.m_outer * N * 2 <= (int64_t(4) << 20))
