@@ -747,7 +747,7 @@ def main():
     # kernel's rate inside a run of launches, most for the shortest launches)
     per_pair_ms = {}
     if not scrub:
-        reps = max(3, min(args.steps, 10))
+        reps = max(3, min(args.steps, 20))
         for dt, n in pairs:
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             launch(dt, n)

@@ -1,6 +1,8 @@
 """Summarize an ncu --set full capture of the fwht kernels (run here, no GPU needed).
 
     python tools/ncu_summary.py gpurun_out/prof.ncu-rep profiles/r01_ncu_full.md [--traffic profiles/ncu_traffic.json]
+        [--alg-bytes B]   (algorithmic bytes per element: 4 for the 16-bit transform (default), 3 for
+                           E4M3/INT8 fused quantization, 2.5 for INT4; the 4-byte row scales are added)
 
 Writes a markdown table per launch: n, dtype, duration, DRAM read/write bytes,
 DRAM throughput %, issue %, warps active %, HMMA pipe %, shared bank conflicts,
@@ -24,6 +26,7 @@ KEYS = {
     "inst": "smsp__inst_executed.sum",
     "bank_conf": "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
     "regs": "launch__registers_per_thread",
+    "tensor_pct": "TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
 }
 
 
@@ -35,11 +38,12 @@ def unit_scale(unit):
 def main():
     rep, out_md = sys.argv[1], sys.argv[2]
     traffic_path = sys.argv[sys.argv.index("--traffic") + 1] if "--traffic" in sys.argv else None
+    alg_b = float(sys.argv[sys.argv.index("--alg-bytes") + 1]) if "--alg-bytes" in sys.argv else None
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True, check=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     hdr, units, data = rows[0], rows[1], rows[2:]
     lines = ["| kernel | n | dtype | time µs | DRAM rd MB | DRAM wr MB | (rd+wr)/algorithmic | DRAM % | issue % | "
-             "warps % | HMMA % | smem bank confl. | regs | top stalls |", "|" + "---|" * 14]
+             "warps % | HMMA % | tensor pipe % | smem bank confl. | regs | top stalls |", "|" + "---|" * 15]
     traffic = []
     for d in data:
         name = d[hdr.index("Kernel Name")]
@@ -66,15 +70,16 @@ def main():
                     except ValueError:
                         pass
         stalls.sort(reverse=True)
-        alg = (8.0 if dt == "fp32" else 4.0) * (1 << 28)
+        alg = (alg_b * (1 << 28) + 4.0 * (1 << 28) / max(n, 1)) if alg_b else (8.0 if dt == "fp32" else 4.0) * (1 << 28)
         ratio = (v.get("rd", 0) + v.get("wr", 0)) / alg
         lines.append(f"| {kern} | {n} | {dt} | {v.get('dur_us', 0):.1f} | {v.get('rd', 0)/1e6:.1f} | {v.get('wr', 0)/1e6:.1f} | "
                      f"{ratio:.3f} | {v.get('dram_pct', 0):.1f} | {v.get('issue_pct', 0):.1f} | {v.get('warps_pct', 0):.1f} | "
-                     f"{v.get('hmma_pct', 0):.1f} | {v.get('bank_conf', 0):.0f} | {v.get('regs', 0):.0f} | "
+                     f"{v.get('hmma_pct', 0):.1f} | {v.get('tensor_pct', float('nan')):.1f} | {v.get('bank_conf', 0):.0f} | {v.get('regs', 0):.0f} | "
                      + ", ".join(f"{nm} {x:.2f}" for x, nm in stalls[:3]) + " |")
         traffic.append({"n": n, "dtype": dt, "dram_bytes": v.get("rd", 0) + v.get("wr", 0), "duration_us": v.get("dur_us")})
-    open(out_md, "w").write(f"# ncu --set full summary of `{rep}`\n\nAlgorithmic bytes per launch = 4 B x 2^28 = "
-                            f"{4 * (1 << 28)} (16-bit; 8 B x 2^28 for fp32; read + write once).\n\n"
+    alg_note = (f"{alg_b} B x 2^28 + 4 B per row (fused quantization: 2 B read + codes + row scales)" if alg_b else
+                f"4 B x 2^28 = {4 * (1 << 28)} (16-bit; 8 B x 2^28 for fp32; read + write once)")
+    open(out_md, "w").write(f"# ncu --set full summary of `{rep}`\n\nAlgorithmic bytes per launch = {alg_note}.\n\n"
                             + "\n".join(lines) + "\n")
     print("\n".join(lines))
     if traffic_path:
