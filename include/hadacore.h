@@ -98,7 +98,8 @@ hadacore_status_t hadacore_fwht(const void* in, void* out, int64_t m, int64_t n,
  * blocks (<= 32 MiB) host->device into `workspace`, transforms them in place with the
  * same kernel, and copies them device->host into `out_host`, pipelined over up to
  * four workspace slots and internal streams so both copy directions overlap the
- * kernels.  Returns after the last
+ * kernels (the four non-blocking streams and one event are created on the first call
+ * of each host thread on each device and kept for the process).  Returns after the last
  * device->host copy has completed (synchronises `stream`).
  *   in_host / out_host: m x n row-major 16-bit matrices in host memory (pinned
  *     memory gives full PCIe bandwidth; pageable works but is slower).  May be equal.

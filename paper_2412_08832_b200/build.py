@@ -36,6 +36,10 @@ def needs_build() -> bool:
 # H_16 constant flipped (-DHC_NEGCTL); the parity tests must FAIL on it.  Test
 # infrastructure only -- the Python binding never loads it.
 LIB_NEGCTL = os.path.join(HERE, "libhadacore_negctl.so")
+# Timing-perturbation library (tests/test_gpu_jitter.py): -DHC_JITTER inserts random
+# nanosleeps at the barrier points of the cluster / warp-specialized kernels; its results
+# must be bitwise those of the product library.  Test infrastructure only.
+LIB_JITTER = os.path.join(HERE, "libhadacore_jitter.so")
 
 
 def _cmd(out: str, defines=(), verbose: bool = False):
@@ -52,6 +56,9 @@ def build(force: bool = False, verbose: bool = False, negctl: bool = True) -> st
     if negctl and (force or not os.path.exists(LIB_NEGCTL) or
                    any(os.path.getmtime(d) > os.path.getmtime(LIB_NEGCTL) for d in DEPS)):
         jobs.append((LIB_NEGCTL, _cmd(LIB_NEGCTL + f".tmp{os.getpid()}", ("-DHC_NEGCTL",), False)))
+    if negctl and (force or not os.path.exists(LIB_JITTER) or
+                   any(os.path.getmtime(d) > os.path.getmtime(LIB_JITTER) for d in DEPS)):
+        jobs.append((LIB_JITTER, _cmd(LIB_JITTER + f".tmp{os.getpid()}", ("-DHC_JITTER",), False)))
     procs = [(dst, cmd[cmd.index("-o") + 1], subprocess.Popen(cmd)) for dst, cmd in jobs]
     for dst, tmp, p in procs:
         if p.wait() != 0:

@@ -365,12 +365,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((NT + 1) * 32, 1)
       for (int64_t r = cid; r < m; r += nclusters, ++it) {
         const int s = it % STAGES;
         mbar_wait(&done[s], (it / STAGES) & 1);
+        jitter(1, it);
         // smem [0, NH/2) = y_lo at this CTA's positions, [NH/2, NH) = y_hi at them
         bulk_s2g(out + r * 2 * NH + rank * (NH / 2), smem + s * TILE_BYTES, TILE_BYTES / 2);
         bulk_s2g(out + r * 2 * NH + NH + rank * (NH / 2), smem + s * TILE_BYTES + TILE_BYTES / 2, TILE_BYTES / 2);
         bulk_commit();
         if (r_load < m) {
           bulk_wait_read<0>();
+          jitter(2, it);
           mbar_arrive_expect_tx(&full[s], TILE_BYTES);
           bulk_g2s(smem + s * TILE_BYTES, src(r_load), TILE_BYTES, &full[s], pol);
           r_load += nclusters;
@@ -434,8 +436,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((NT + 1) * 32, 1)
       // release at cluster scope, cumulative over the group's writes it synchronized with
       const uint32_t tb_addr = smem_addr(tb);
       named_bar_sync(1 + grp, NTG * 32);
-      if (tid == 0) mbar_arrive_remote(mapa_shared(smem_addr(&ready[s]), peer));
+      if (tid == 0) {
+        jitter(3, it);
+        mbar_arrive_remote(mapa_shared(smem_addr(&ready[s]), peer));
+      }
       mbar_wait_cluster(&ready[s], ph);  // the partner's half is final
+      jitter(4, it);
       // positions [rank * NH/2, (rank+1) * NH/2) of both halves are this CTA's: it reads
       // the partner's half only there (32 KiB over DSMEM), and produces both outputs
       // y_lo = a + b and y_hi = a - b for them
@@ -452,7 +458,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((NT + 1) * 32, 1)
 #pragma unroll
       for (int k2 = 0; k2 < PER_THREAD; ++k2) own[k2] = *reinterpret_cast<const float4*>(tb + 4 * (q0 + tid + k2 * NTG * 32));
       named_bar_sync(1 + grp, NTG * 32);  // the whole group has read the partner's half
-      if (tid == 0) mbar_arrive_remote(mapa_shared(smem_addr(&consumed[s]), peer));
+      if (tid == 0) {
+        jitter(5, it);
+        mbar_arrive_remote(mapa_shared(smem_addr(&consumed[s]), peer));
+      }
       mbar_wait_cluster(&consumed[s], ph);  // the partner is done reading ours
 #pragma unroll
       for (int k2 = 0; k2 < PER_THREAD; ++k2) {

@@ -123,6 +123,22 @@ __device__ __forceinline__ void trace(int it, int ev) {
 __device__ __forceinline__ void trace(int, int) {}
 #endif
 
+// HC_JITTER (test build libhadacore_jitter.so, tests/test_gpu_jitter.py): random
+// nanosleeps at the synchronization points of the multi-role / multi-CTA kernels, so
+// that the barrier protocols are exercised under perturbed timing; results must stay
+// bitwise identical to the product build.
+#ifdef HC_JITTER
+__device__ __forceinline__ void jitter(uint32_t site, uint32_t it) {
+  uint32_t h = (blockIdx.x * 0x9E3779B1u) ^ (threadIdx.x * 0x85EBCA77u) ^ (it * 0xC2B2AE3Du) ^ (site * 0x27D4EB2Fu);
+  h ^= h >> 15;
+  h *= 0x2C1B3C6Du;
+  h ^= h >> 12;
+  if ((h & 3u) == 0u) __nanosleep((h >> 8) & 4095u);  // a quarter of the time, up to ~4 us
+}
+#else
+__device__ __forceinline__ void jitter(uint32_t, uint32_t) {}
+#endif
+
 // Programmatic dependent launch: let the next kernel be scheduled early, and wait
 // for the previous kernel's completion (and memory flush) before touching memory.
 __device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }

@@ -261,6 +261,7 @@ __global__ void __launch_bounds__((NE + NA + 2) * 32, 1)
         const int t = ctl->stage_tile[s];
         if (t < 0) break;
         mbar_wait(&ufree[s], ph);  // the MMAs have read the stage: its upper half is free
+        jitter(10, it);
         int64_t nt = -1;
         if (!ended) {
           if (tile < 0 || tile >= num_tiles) {
@@ -278,6 +279,7 @@ __global__ void __launch_bounds__((NE + NA + 2) * 32, 1)
           }
         }
         mbar_wait(&cready[s], ph);  // the codes of tile t are staged in the lower half
+        jitter(11, it);
         const TileRows tr(g, t);
         tma_store_4d(&tm_q, 0, 0, int(tr.j0), int(tr.i0), smem + s * kTcTile);
         bulk_commit();
@@ -298,6 +300,7 @@ __global__ void __launch_bounds__((NE + NA + 2) * 32, 1)
         trace(it, 7);
         const int tile = ctl->stage_tile[s];
         mbar_wait(&tempty[b], ((it >> 1) & 1) ^ 1);  // the epilogue has drained buffer b
+        jitter(12, it);
         trace(it, 3);
         if (tile < 0) {
           buf_tile[b] = -1;
@@ -390,6 +393,7 @@ __global__ void __launch_bounds__((NE + NA + 2) * 32, 1)
         }
       }
       fence_proxy_async_smem();  // our 16-bit image is read next by the tensor core (async proxy)
+      jitter(13, it);
       __syncwarp();
       if (lane == 0) mbar_arrive(&adone[s]);
       if (wa == 0 && lane == 0) trace(it, 2);
@@ -436,6 +440,7 @@ __global__ void __launch_bounds__((NE + NA + 2) * 32, 1)
 #pragma unroll
       for (int o = 8; o >= 1; o >>= 1) au = max(au, __shfl_xor_sync(0xffffffffu, au, o));
       if ((lane & 15) == 0) red[b * NE * 2 + warp * 2 + (lane >> 4)] = __uint_as_float(au);
+      jitter(14, it);
       named_bar_sync(1, NE * 32);
       if (warp == 0 && lane == 0) trace(it, 5);
       float am = 0.f;
@@ -514,6 +519,7 @@ __global__ void __launch_bounds__((NE + NA + 2) * 32, 1)
       }
       tc_fence_before();
       fence_proxy_async_smem();  // the staged codes are read next by the TMA store (async proxy)
+      jitter(15, it);
       __syncwarp();
       if (lane == 0) {
         mbar_arrive(&tempty[b]);

@@ -895,14 +895,27 @@ extern "C" hadacore_status_t hadacore_fwht_host(const void* in_host, void* out_h
     rows_per_slot = workspace_bytes / row_bytes >= size_t(align_rows) ? align_rows : 1;
   }
   cudaStream_t user = reinterpret_cast<cudaStream_t>(stream);
-  cudaStream_t st[kMaxSlots] = {};
-  cudaEvent_t ev = nullptr;
+  // internal streams and event: created once per (host thread, device) and kept (ADVICE /
+  // creating and destroying 4 streams + 1 event per call cost a few tens of us)
+  struct HostPipe {
+    cudaStream_t st[kMaxSlots];
+    cudaEvent_t ev;
+    bool ready;
+  };
+  thread_local HostPipe pipes[kMaxDevices] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return HADACORE_ERR_CUDA;
+  HostPipe& hp = pipes[dev];
+  if (!hp.ready) {
+    for (int i = 0; i < kMaxSlots; ++i)
+      if (cudaStreamCreateWithFlags(&hp.st[i], cudaStreamNonBlocking) != cudaSuccess) return HADACORE_ERR_CUDA;
+    if (cudaEventCreateWithFlags(&hp.ev, cudaEventDisableTiming) != cudaSuccess) return HADACORE_ERR_CUDA;
+    hp.ready = true;
+  }
+  cudaStream_t* st = hp.st;
+  cudaEvent_t ev = hp.ev;
   hadacore_status_t rc = HADACORE_OK;
-  for (int i = 0; i < slots && rc == HADACORE_OK; ++i)
-    if (cudaStreamCreateWithFlags(&st[i], cudaStreamNonBlocking) != cudaSuccess) rc = HADACORE_ERR_CUDA;
-  if (rc == HADACORE_OK && cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess)
-    rc = HADACORE_ERR_CUDA;
-  if (rc == HADACORE_OK) {
+  {
     // order after everything already queued on the caller's stream
     if (cudaEventRecord(ev, user) != cudaSuccess) rc = HADACORE_ERR_CUDA;
     for (int i = 0; i < slots && rc == HADACORE_OK; ++i)
@@ -926,11 +939,7 @@ extern "C" hadacore_status_t hadacore_fwht_host(const void* in_host, void* out_h
       rc = HADACORE_ERR_CUDA;
   }
   for (int i = 0; i < slots; ++i)
-    if (st[i]) {
-      if (cudaStreamSynchronize(st[i]) != cudaSuccess) rc = HADACORE_ERR_CUDA;
-      cudaStreamDestroy(st[i]);
-    }
-  if (ev) cudaEventDestroy(ev);
+    if (cudaStreamSynchronize(st[i]) != cudaSuccess) rc = HADACORE_ERR_CUDA;
   return rc;
 }
 

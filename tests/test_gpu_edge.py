@@ -195,6 +195,8 @@ def negctl_lib(hc):
     vp, i64 = ctypes.c_void_p, ctypes.c_int64
     lib.hadacore_fwht.argtypes = [vp, vp, i64, i64, ctypes.c_int, ctypes.c_float, vp]
     lib.hadacore_fwht.restype = ctypes.c_int
+    lib.hadacore_fwht_quant.argtypes = [vp, vp, vp, i64, i64, ctypes.c_int, ctypes.c_int, ctypes.c_float, vp]
+    lib.hadacore_fwht_quant.restype = ctypes.c_int
     return lib
 
 
@@ -214,3 +216,26 @@ def test_negative_control_fails_parity(hc, negctl_lib, n, dtype):
     assert rc == 0
     assert rel_l2_rows(widen(good), ref).max() <= TOL[dtype]
     assert rel_l2_rows(widen(bad), ref).max() > 10 * TOL[dtype]
+
+
+@pytest.mark.parametrize("n", [2048, 16384, 32768])
+def test_negative_control_fails_quant_parity(hc, negctl_lib, n):
+    """The fused quantization's parity check (dequantized outputs vs the oracle's transform) passes
+    on the product library and fails on the sign-flipped build, for the register-epilogue kernel
+    (n = 2048) and the tcgen05 kernel, whose H_128 B operand carries the flipped sign (n >= 16384)."""
+    m = 8
+    x = synthetic.generate(m, n, torch.bfloat16, 4848).cuda()
+    ref = oracle.fwht(widen(x))
+    q, s = hc.hadacore_fwht_quant(x, "int8")
+    qb = torch.empty_like(q)
+    sb = torch.empty_like(s)
+    rc = negctl_lib.hadacore_fwht_quant(x.data_ptr(), qb.data_ptr(), sb.data_ptr(), m, n, 1, 1, 1.0 / math.sqrt(n),
+                                        torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    assert rc == 0
+    # error in units of the row's code step: the product build is within half a step plus the
+    # bf16 transform error; one flipped sign of H_16 / H_128 moves whole outputs by several steps
+    good = np.abs(widen(q.float()) * widen(s)[:, None] - ref) / widen(s)[:, None]
+    bad = np.abs(widen(qb.float()) * widen(sb)[:, None] - ref) / widen(sb)[:, None]
+    assert good.max() <= 1.0
+    assert bad.max() > 3.0
