@@ -466,6 +466,9 @@ __device__ __forceinline__ void unpack8(const uint32_t x[4], float v[8]) {
     }
   }
 }
+// HC_SIMT_SCALAR: the round-1 scalar form (one SHFL + one FFMA per value and lane bit);
+// default: packed f32x2 math -- in-register bits as FADD2 butterfly pairs, lane bits as
+// two SHFL + one FFMA2 per value pair (SURVEY.md 7 variant V-B)
 __device__ __forceinline__ void simt_butterflies(float v[8], uint32_t mask8) {
   const int lane = threadIdx.x & 31;
   constexpr int reg_bit[8] = {0, -1, -1, 2, -1, -1, -1, 1};   // b -> bit of the value index
@@ -475,6 +478,7 @@ __device__ __forceinline__ void simt_butterflies(float v[8], uint32_t mask8) {
     if (!((mask8 >> b) & 1u)) continue;
     if (reg_bit[b] >= 0) {
       const int st = 1 << reg_bit[b];
+#ifdef HC_SIMT_SCALAR
 #pragma unroll
       for (int i = 0; i < 8; ++i)
         if (!(i & st)) {
@@ -482,21 +486,46 @@ __device__ __forceinline__ void simt_butterflies(float v[8], uint32_t mask8) {
           v[i] = p0 + p1;
           v[i | st] = p0 - p1;
         }
+#else
+#pragma unroll
+      for (int k = 0; k < 4; k += 2) {  // the k-th index with bit st clear: (k / st) * 2 st + k % st
+        const int i0 = (k / st) * 2 * st + k % st, i1 = ((k + 1) / st) * 2 * st + (k + 1) % st;
+        bfly2(v[i0], v[i1], v[i0 | st], v[i1 | st]);
+      }
+#endif
     } else {
       const int lb = 1 << lane_bit[b];
       const float sg = (lane & lb) ? -1.f : 1.f;
+#ifdef HC_SIMT_SCALAR
 #pragma unroll
       for (int i = 0; i < 8; ++i) v[i] = fmaf(v[i], sg, __shfl_xor_sync(0xffffffffu, v[i], lb));
+#else
+#pragma unroll
+      for (int i = 0; i < 8; i += 2) {
+        const float q0 = __shfl_xor_sync(0xffffffffu, v[i], lb), q1 = __shfl_xor_sync(0xffffffffu, v[i + 1], lb);
+        float a = v[i], c = v[i + 1];
+        asm("{.reg .b64 t, s, u;\n mov.b64 t, {%0,%1};\n mov.b64 s, {%2,%2};\n mov.b64 u, {%3,%4};\n"
+            " fma.rn.f32x2 t, t, s, u;\n mov.b64 {%0,%1}, t;}"
+            : "+f"(a), "+f"(c)
+            : "f"(sg), "f"(q0), "f"(q1));
+        v[i] = a;
+        v[i + 1] = c;
+      }
+#endif
     }
   }
 }
+__device__ __forceinline__ void mul2(float& a, float& b, float m);
 template <int DT>
 __device__ __forceinline__ void simt_fwht_pack(const uint32_t x[4], uint32_t mask8, float mul, uint32_t z[4]) {
   float v[8];
   unpack8<DT>(x, v);
   simt_butterflies(v, mask8);
 #pragma unroll
-  for (int j = 0; j < 4; ++j) z[j] = pack2<DT>(v[2 * j] * mul, v[2 * j + 1] * mul);
+  for (int j = 0; j < 4; ++j) {
+    mul2(v[2 * j], v[2 * j + 1], mul);
+    z[j] = pack2<DT>(v[2 * j], v[2 * j + 1]);
+  }
 }
 
 // ------------------------------------------------------------------ fused quantization
