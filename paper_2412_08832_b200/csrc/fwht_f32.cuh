@@ -483,6 +483,168 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((NT + 1) * 32, 1)
   cluster_sync_all();  // no CTA leaves while its partner may still touch its shared memory
 }
 
+// ---------------------------------------------------------------- n = 2^15, top bit first
+// (round 2; VERDICT r1 "fp32 at n = 2^15": the pair kernel above exchanges the halves AFTER
+// they are transformed, a synchronous cross-SM handshake per row that left 23 % of its stall
+// samples waiting on the partner).  The factors of H_2^15 = (H_2 (x) I) (I (x) H_2^14)
+// commute, so the top-bit butterfly can come FIRST: CTA h of a 2-CTA cluster
+// computes u_h = x_lo + (1 - 2h) x_hi and then y_h = scale * H_2^14 u_h, the output half h.
+// Each CTA needs both input halves: CTA h loads 16 KiB pieces of half h with a MULTICAST bulk
+// copy that lands in both CTAs' shared memory (HBM and L2 read each byte once), so the only
+// cross-CTA traffic is the input itself, pipelined through an S-slot ring; a slot is refilled
+// when the consumers of BOTH CTAs have released it (an empty mbarrier with one local and one
+// remote arrival per use) -- an asynchronous, ring-deep dependency instead of a per-row
+// handshake.  The combine u = x_lo +- x_hi is fused into phase 0 (bits 0..4); phases 1, 2
+// (bits 5..9, 10..13, scale applied in the last) run on the CTA's 64 KiB row buffer as in
+// fwht_f32_fast_kernel; then one bulk store of y_h.  One consumer group consumes the pieces
+// strictly in sequence (two groups sharing the slots could wait on a slot two fills ahead,
+// which a parity wait cannot tell apart -- the first version hung); rows alternate two 64 KiB
+// row buffers so a row's store overlaps the next row's combine.  Smem: NRB x 64 KiB + S x 32 KiB.
+// MEASURED SLOWER than the pair kernel (HC_F32_MC builds: 3.57 TB/s with 3 slots and two row
+// buffers, 3.2 with 4-5 slots and one, vs 4.78; profiles/r02_f32_mc_ab.txt): the shared-memory
+// budget leaves less than one row of input in flight (3 x 16 KiB of a CTA's own half), so each
+// row's last piece is loaded only once the combine has started, and the two CTAs advance in
+// lockstep through the shared slots.  Kept as a build option for the record.
+__device__ __forceinline__ void bulk_g2s_mc2(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                             uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster.L2::cache_hint"
+      " [%0], [%1], %2, [%3], %4, %5;" ::"r"(smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar)), "h"(uint16_t(3)), "l"(policy)
+      : "memory");
+}
+
+template <int S, int NT, int NRB>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((NT + 1) * 32, 1)
+    fwht_f32_mc_kernel(const float* __restrict__ in, float* __restrict__ out, int64_t m, float scale) {
+  constexpr int NH = 16384;                 // elements per half row (per CTA)
+  constexpr int PIECE = 4096;               // floats per multicast piece (16 KiB)
+  constexpr int NPIECE = NH / PIECE;        // pieces per half row
+  constexpr int ROWBUF = NH * 4;            // 64 KiB
+  constexpr int SLOT = 2 * PIECE * 4;       // lo piece + hi piece, 32 KiB
+  constexpr int PAR = NT * 32 / (PIECE / 32);  // pieces combined at once (one 32-float item per thread)
+  static_assert(PAR >= 1 && NPIECE % PAR == 0 && PAR * (PIECE / 32) == NT * 32, "item split");
+  static_assert(S >= PAR, "slots");
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t* const slots = smem + NRB * ROWBUF;
+  uint64_t* full = reinterpret_cast<uint64_t*>(slots + S * SLOT);
+  uint64_t* empty = full + S;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank(), peer = rank ^ 1u;
+  const int64_t cid = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
+
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < S; ++k) {
+      mbar_init(&full[k], 1);
+      mbar_init(&empty[k], 2);  // this CTA's consumers + the partner's
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    fence_proxy_async_smem();
+  }
+  cluster_sync_all();  // both CTAs' barriers exist before any multicast or remote arrival
+  pdl_launch_dependents();
+
+  if (warp == NT) {
+    // ---------------- producer: this CTA's half of every piece, multicast to both CTAs
+    if (lane == 0) {
+      pdl_wait();
+      const uint64_t pol = policy_evict_first();
+      int u = 0;  // piece sequence number (both CTAs walk the same sequence)
+      for (int64_t r = cid; r < m; r += nclusters) {
+#pragma unroll 1
+        for (int p = 0; p < NPIECE; ++p, ++u) {
+          const int k = u % S;
+          mbar_wait_cluster(&empty[k], ((u / S) & 1) ^ 1);  // both CTAs have released slot k
+          jitter(6, u);
+          mbar_arrive_expect_tx(&full[k], SLOT);            // own half + the partner's
+          bulk_g2s_mc2(slots + k * SLOT + rank * (SLOT / 2), in + r * 2 * NH + int64_t(rank) * NH + p * PIECE,
+                       SLOT / 2, &full[k], pol);
+        }
+      }
+    }
+  } else {
+    // ---------------- consumers (one group, pieces consumed strictly in sequence, so a
+    // parity wait is never two phases ahead of its slot); rows alternate two row buffers
+    const int tid = threadIdx.x, half = tid / (PIECE / 32), item = tid % (PIECE / 32);
+    const uint32_t c = uint32_t(lane) & 7u;
+    float al[3];
+#pragma unroll
+    for (int b = 0; b < 3; ++b) al[b] = ((c >> b) & 1u) ? -1.f : 1.f;
+    const float hs = rank == 0 ? 1.f : -1.f;  // u_h = x_lo + hs * x_hi
+    int rows = 0;
+    for (int64_t r = cid; r < m; r += nclusters, ++rows) {
+      float* const rb = reinterpret_cast<float*>(smem + (rows % NRB) * ROWBUF);
+      if (rows >= NRB) {  // the store of NRB rows ago (same buffer) has read it
+        if (tid == 0) bulk_wait_read<NRB - 1>();
+        named_bar_sync(1, NT * 32);
+      }
+      // combine (top bit) + phase 0 (bits 0..4): PAR pieces at once, 32 floats per thread
+#pragma unroll 1
+      for (int p0 = 0; p0 < NPIECE; p0 += PAR) {
+        const int p = p0 + half, u = rows * NPIECE + p, ks = u % S;
+        mbar_wait(&full[ks], (u / S) & 1);
+        const float* lo = reinterpret_cast<const float*>(slots + ks * SLOT);
+        const float* hi = lo + PIECE;
+        float v[32];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int o = 4 * (item * 8 + int(uint32_t(j) ^ c));
+          const float4 a = *reinterpret_cast<const float4*>(lo + o);
+          const float4 b = *reinterpret_cast<const float4*>(hi + o);
+          v[4 * j] = fmaf(b.x, hs, a.x);
+          v[4 * j + 1] = fmaf(b.y, hs, a.y);
+          v[4 * j + 2] = fmaf(b.z, hs, a.z);
+          v[4 * j + 3] = fmaf(b.w, hs, a.w);
+        }
+        // the slots are read: release them to both producers
+        named_bar_sync(1, NT * 32);
+        if (item == 0) {
+          jitter(7, u);
+          mbar_arrive(&empty[ks]);
+          mbar_arrive_remote(mapa_shared(smem_addr(&empty[ks]), peer));
+        }
+#pragma unroll
+        for (int b = 0; b < 2; ++b)
+#pragma unroll
+          for (int e = 0; e < 32; ++e)
+            if (!(e & (1 << b))) {
+              const float q0 = v[e], q1 = v[e | (1 << b)];
+              v[e] = q0 + q1;
+              v[e | (1 << b)] = q0 - q1;
+            }
+#pragma unroll
+        for (int b = 0; b < 3; ++b)
+#pragma unroll
+          for (int e = 0; e < 32; ++e)
+            if (!(e & (4 << b))) {
+              const float q0 = v[e], q1 = v[e | (4 << b)];
+              v[e] = fmaf(q0, al[b], q1);
+              v[e | (4 << b)] = fmaf(q1, -al[b], q0);
+            }
+        float* const dst = rb + p * PIECE;
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          *reinterpret_cast<float4*>(dst + 4 * (item * 8 + int(uint32_t(j) ^ c))) =
+              make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+      }
+      named_bar_sync(1, NT * 32);
+      f32_phase<NH, 5, 5, false, NT>(rb, 1, tid, 1.f);
+      named_bar_sync(1, NT * 32);
+      f32_phase<NH, 10, 4, true, NT>(rb, 1, tid, scale);
+      fence_proxy_async_smem();  // the bulk store reads rb through the async proxy
+      named_bar_sync(1, NT * 32);
+      if (tid == 0) {
+        bulk_s2g(out + r * 2 * NH + int64_t(rank) * NH, rb, ROWBUF);
+        bulk_commit();
+      }
+    }
+    if (threadIdx.x == 0) bulk_wait_all();
+  }
+  __syncwarp();
+  cluster_sync_all();  // no CTA leaves while its partner may still multicast into it or arrive remotely
+}
+
 // n = 2^15 in fp32, second pass: rows are [a | b] with a, b = H_2^14-transformed halves;
 // out = scale * [a + b | a - b] (the remaining H_2 factor over the top index bit).
 __global__ void f32_half_butterfly_kernel(const float* __restrict__ in, float* __restrict__ out, int64_t m,

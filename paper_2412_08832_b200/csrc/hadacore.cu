@@ -600,7 +600,10 @@ hadacore_status_t launch_f32_fast(const void* in, void* out, int64_t m, float sc
 
 hadacore_status_t launch_f32_32k(const void* in, void* out, int64_t m, float scale, cudaStream_t stream) {
 #ifndef HC_F32_TWO_PASS
-  // one launch of 2-CTA clusters, a row per cluster (fwht_f32_pair_kernel)
+  // one launch of 2-CTA clusters, a row per cluster: fwht_f32_pair_kernel (DSMEM exchange of
+  // the transformed halves; default) or fwht_f32_mc_kernel (HC_F32_MC: top bit first,
+  // multicast input halves -- measured slower, 3.2-3.6 vs 4.8 TB/s: profiles/r02_f32_mc_ab.txt)
+#ifndef HC_F32_MC
 #ifndef HC_PAIR_NT
 #define HC_PAIR_NT 16
 #endif
@@ -609,10 +612,21 @@ hadacore_status_t launch_f32_32k(const void* in, void* out, int64_t m, float sca
 #endif
   constexpr int st = 3, nt = HC_PAIR_NT, groups = HC_PAIR_G;
   constexpr int smem = st * 65536 + 4 * st * 8;
+  auto kern = fwht_f32_pair_kernel<st, nt, groups>;
+#else
+#ifndef HC_MC_SLOTS
+#define HC_MC_SLOTS 5
+#endif
+#ifndef HC_MC_RB
+#define HC_MC_RB 1
+#endif
+  constexpr int st = HC_MC_SLOTS, nt = 8, nrb = HC_MC_RB;
+  constexpr int smem = nrb * 65536 + st * 32768 + 2 * st * 8;
+  auto kern = fwht_f32_mc_kernel<st, nt, nrb>;
+#endif
   static std::atomic<uint64_t> attr_done{0};
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return HADACORE_ERR_CUDA;
-  auto kern = fwht_f32_pair_kernel<st, nt, groups>;
   if (!ensure_smem_attr(kern, smem, attr_done, dev)) return HADACORE_ERR_CUDA;
   // co-resident clusters: a cluster's CTAs share a GPC, so not every SM pairs up --
   // a grid with more clusters than fit at once would run a second wave
