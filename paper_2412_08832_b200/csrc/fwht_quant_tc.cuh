@@ -132,8 +132,8 @@ __host__ __device__ constexpr int tc_smem_bytes() {
 // depth (64 KiB stages), NA phase-A warps, NE epilogue warps (4 or 8).  Warps [0, NE)
 // are the epilogue (warp % 4 = its TMEM lane quadrant), [NE, NE + NA) phase A, then the
 // TMA producer warp and the MMA warp.
-template <int N, int DT, int QT, int STAGES, int NA, int NE>
-__global__ void __launch_bounds__((NE + NA + 2) * 32, 1)
+template <int N, int DT, int QT, int STAGES, int NA, int NE, int EG>
+__global__ void __launch_bounds__((EG * NE + NA + 2) * 32, 1)
     fwht_quant_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ CUtensorMap tm_q,
                          float* __restrict__ row_scale, const RowGrid g, float s_res) {
   constexpr int C = N / 256, R = 128 / C, Q = log2_n<N>() - 8;
@@ -162,7 +162,7 @@ __global__ void __launch_bounds__((NE + NA + 2) * 32, 1)
   float* red = reinterpret_cast<float*>(tmem_slot + 2);    // [2][NE * 2] row-max partials
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int WP = NE + NA, WM = NE + NA + 1;  // producer and MMA warps
+  const int WP = EG * NE + NA, WM = EG * NE + NA + 1;  // producer and MMA warps
 
   if (threadIdx.x == 0) {
     mbar_init(&ctl->clc_bar, 1);
@@ -302,10 +302,15 @@ __global__ void __launch_bounds__((NE + NA + 2) * 32, 1)
         mbar_wait(&tempty[b], ((it >> 1) & 1) ^ 1);  // the epilogue has drained buffer b
         jitter(12, it);
         trace(it, 3);
-        if (tile < 0) {
-          buf_tile[b] = -1;
-          mbar_arrive(&tfull[b]);
-          mbar_arrive(&tfull[b]);
+        if (tile < 0) {  // end: every epilogue group sees a -1 tile (group e drains iteration it + e)
+#pragma unroll
+          for (int e = 0; e < EG; ++e) {
+            const int ie = it + e, be = ie & 1;
+            if (e > 0) mbar_wait(&tempty[be], ((ie >> 1) & 1) ^ 1);
+            buf_tile[be] = -1;
+            mbar_arrive(&tfull[be]);
+            mbar_arrive(&tfull[be]);
+          }
           break;
         }
         tc_fence_after();
@@ -330,9 +335,9 @@ __global__ void __launch_bounds__((NE + NA + 2) * 32, 1)
         mbar_arrive(&tfull[b]);
       }
     }
-  } else if (warp >= NE) {
+  } else if (warp >= EG * NE) {
     // ---------------- phase A: H_{n/256} across the chunks of the raw rows, in place
-    const int wa = warp - NE;
+    const int wa = warp - EG * NE;
     uint32_t Bc0[2], Bc1[2];
     make_const_b<DT>(PL::mask_a, 0, Bc0);
     make_const_b<DT>(PL::mask_a, 1, Bc1);
@@ -401,13 +406,15 @@ __global__ void __launch_bounds__((NE + NA + 2) * 32, 1)
     }
   } else {
     // ---------------- epilogue: TMEM lane quadrant warp % 4 = chunks 32q .. 32q + 31 of the tile
-    const int quad = warp & 3, ch = warp >> 2;  // ch: column half (NE = 8)
+    // EG groups of NE warps take alternate tiles (EG = 2: group g always drains TMEM buffer g)
+    const int eg = warp / NE, ew = warp % NE;
+    const int quad = ew & 3, ch = ew >> 2;  // ch: column half (NE = 8)
     const int mrow = 32 * quad + lane;           // chunk row of the tile = TMEM lane
     const int r = mrow / C, c = mrow % C;
     constexpr int NJ = NE == 4 ? 4 : 2;          // 32-column groups per thread and pass
     const int j0 = NE == 4 ? 0 : 2 * ch;
     const float q_qs = copysignf(qmax_of<QT>(), s_res), q_ss = fabsf(s_res) / qmax_of<QT>();
-    for (int it = 0;; ++it) {
+    for (int it = eg;; it += EG) {
       const int b = it & 1;
       mbar_wait(&tfull[b], (it >> 1) & 1);
       if (warp == 0 && lane == 0) trace(it, 4);
@@ -439,9 +446,9 @@ __global__ void __launch_bounds__((NE + NA + 2) * 32, 1)
       uint32_t au = __float_as_uint(a);
 #pragma unroll
       for (int o = 8; o >= 1; o >>= 1) au = max(au, __shfl_xor_sync(0xffffffffu, au, o));
-      if ((lane & 15) == 0) red[b * NE * 2 + warp * 2 + (lane >> 4)] = __uint_as_float(au);
+      if ((lane & 15) == 0) red[b * NE * 2 + ew * 2 + (lane >> 4)] = __uint_as_float(au);
       jitter(14, it);
-      named_bar_sync(1, NE * 32);
+      named_bar_sync(1 + eg, NE * 32);
       if (warp == 0 && lane == 0) trace(it, 5);
       float am = 0.f;
       {

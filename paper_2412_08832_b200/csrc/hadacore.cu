@@ -287,13 +287,16 @@ bool ensure_smem_attr(Kern kern, int smem, std::atomic<uint64_t>& done, int dev)
 #define HC_QTC_MINN 16384  // per-(qtype, n) A/B: profiles/r02_quant_tc_ab.txt
 #endif
 #ifndef HC_QTC_NA
-#define HC_QTC_NA 12
+#define HC_QTC_NA 8
 #endif
 #ifndef HC_QTC_NE
 #define HC_QTC_NE 4
 #endif
 #ifndef HC_QTC_ST
 #define HC_QTC_ST 3
+#endif
+#ifndef HC_QTC_EG
+#define HC_QTC_EG 2  // epilogue groups on alternate tiles (INT4 +4.5 %: profiles/r02_quant_tc_eg.txt)
 #endif
 
 // 5-D view (64 elements, chunk [512 B], inner row, outer row, 64-element segment [128 B])
@@ -331,13 +334,13 @@ bool encode_tc_qmap(CUtensorMap* map, void* q, const Layout& L, int code_bytes, 
 template <int N, int DT, int QT>
 hadacore_status_t launch_qtc(const void* in, uint8_t* out_q, float* row_scale, const Layout& L, float scale,
                              cudaStream_t stream) {
-  constexpr int NA = HC_QTC_NA, NE = HC_QTC_NE, ST = HC_QTC_ST;
+  constexpr int NA = HC_QTC_NA, NE = HC_QTC_NE, ST = HC_QTC_ST, EG = HC_QTC_EG;
   constexpr int smem = tc_smem_bytes<ST, NE>();
   static_assert(smem <= 227 * 1024, "shared memory");
   static std::atomic<uint64_t> attr_done{0};
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return HADACORE_ERR_CUDA;
-  auto kern = fwht_quant_tc_kernel<N, DT, QT, ST, NA, NE>;
+  auto kern = fwht_quant_tc_kernel<N, DT, QT, ST, NA, NE, EG>;
   if (!ensure_smem_attr(kern, smem, attr_done, dev)) return HADACORE_ERR_CUDA;
   const RowGrid g = make_grid(L, 128 / (N / 256));
   const int64_t max_ctas = kClc ? int64_t(INT32_MAX) : int64_t(sm_count(dev));
@@ -347,7 +350,7 @@ hadacore_status_t launch_qtc(const void* in, uint8_t* out_q, float* row_scale, c
     return HADACORE_ERR_CUDA;
   // phase A's constants carry 2^-stage_shift(mask_a); H_128 is +-1
   const float s_res = std::ldexp(scale, stage_shift(PlanL<log2_n<N>() - 8>::mask_a));
-  if (launch_pdl(kern, grid, (NE + NA + 2) * 32, smem, stream, tin, tq, row_scale, g, s_res) != cudaSuccess)
+  if (launch_pdl(kern, grid, (EG * NE + NA + 2) * 32, smem, stream, tin, tq, row_scale, g, s_res) != cudaSuccess)
     return HADACORE_ERR_CUDA;
   return cudaPeekAtLastError() == cudaSuccess ? HADACORE_OK : HADACORE_ERR_CUDA;
 }

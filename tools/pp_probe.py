@@ -4,7 +4,7 @@ import paper_2412_08832_b200 as hc
 elems = 1 << 28
 xs = {dt: torch.randn(elems, device='cuda').to(dt) for dt in (torch.float16, torch.bfloat16)}
 q = torch.empty(elems, dtype=torch.uint8, device='cuda')
-for n in (8192, 32768):
+for n in (16384, 32768):
     sc = torch.empty(elems // n, device='cuda')
     def L(dt):
         hc.hadacore_fwht_quant(xs[dt].view(-1, n), 'e4m3', out=q.view(torch.float8_e4m3fn).view(-1, n), row_scale=sc)
