@@ -582,7 +582,12 @@ hadacore_status_t launch_f32(const void* in, void* out, int64_t m, float scale, 
 // Full-speed fp32 path (NEXT-2, fwht_f32_fast_kernel): 8 consumer warps, 32 KiB
 // tiles in a 4-stage ring (64 KiB x 3 for n = 2^14); n = 2^15 = two 2^14 halves +
 // f32_half_butterfly_kernel.
-template <int N> struct TunedF { static constexpr int nt = 8, tkb = N >= 16384 ? 64 : 32, st = N >= 16384 ? 3 : 4; };
+#ifndef HC_F32_BIG_N
+#define HC_F32_BIG_N 8192  // smallest n with 64 KiB x 3 tiles (n = 8192: 6.33-6.58 -> 6.82-6.84 TB/s, profiles/r02_f32_tiles_ab.txt)
+#endif
+template <int N> struct TunedF {
+  static constexpr int nt = 8, tkb = N >= HC_F32_BIG_N ? 64 : 32, st = N >= HC_F32_BIG_N ? 3 : 4;
+};
 
 template <int N>
 hadacore_status_t launch_f32_fast(const void* in, void* out, int64_t m, float scale, cudaStream_t stream) {
