@@ -328,6 +328,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((NT + 1) * 32, 1)
   // G <= STAGES: a group never waits on a stage barrier two phases ahead of its
   // current phase (parity waits cannot tell those apart)
   static_assert(NT % G == 0 && G <= STAGES, "groups");
+  static_assert(PER_THREAD * NTG * 32 * 8 == NH, "the final factor's positions split evenly over a group");
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * TILE_BYTES);
   uint64_t* done = full + STAGES;
