@@ -746,8 +746,12 @@ def main():
     # per-launch events above break programmatic dependent launch, so they understate a
     # kernel's rate inside a run of launches, most for the shortest launches)
     per_pair_ms = {}
+    per_pair_clocks = None
     if not scrub:
         reps = max(3, min(args.steps, 20))
+        cs_pp = ClockSampler(torch.cuda.current_device() if world == 1 else local)
+        cs_pp.__enter__()
+        cs_pp.mark_start()
         for dt, n in pairs:
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             launch(dt, n)
@@ -758,6 +762,9 @@ def main():
             e1.record(stream)
             torch.cuda.synchronize()
             per_pair_ms[(dt, n)] = e0.elapsed_time(e1) / reps
+        cs_pp.mark_end()
+        cs_pp.__exit__(None, None, None)
+        per_pair_clocks = cs_pp.summary()
 
     # output checks outside the timed regions, on every rank:
     # (1) a property that holds at any size: the normalized transform preserves
@@ -951,7 +958,10 @@ def main():
             "elements_per_s": float(f"{(C5_ELEMS * args.steps if c5 else sum(elems_of[p] for p in pairs) * args.steps * world) / (t_max * 1e-3):.4g}"),
             "per_n_GBps": per_n,
             "per_n_source": ("sum of per-launch events (L2 scrubbed between launches)" if scrub else
-                             "back-to-back launches of each (dtype, n), CUDA events around the group"),
+                             "back-to-back launches of each (dtype, n), CUDA events around the group, after the "
+                             "timed region (its clocks: per_n_clocks; long fused-quantization runs reach the power "
+                             "cap there -- profiles/r02_quant_single_n.txt has single-n timed regions)"),
+            "per_n_clocks": per_pair_clocks,
             "launch_us_p10_p50_p90": launch_pct, "inplace": bool(args.inplace),
             "roofline": roofline, "cpu_baseline": cpu_baseline, "e2e": e2e,
             "gpu_launches": int(args.steps * sum(hc.launches_per_call(elems_of[(dt, n)] // n, n, dt) for dt, n in pairs)),
