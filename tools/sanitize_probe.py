@@ -1,6 +1,7 @@
 """Small invocations of every kernel family for compute-sanitizer (memcheck / racecheck / synccheck):
 fwht_kernel (n = 128, 256), fwht_rows_kernel (n = 512, 4096, 32768), strided rows, fused quantization
-(E4M3 / INT8 / INT4, both kernels), fwht_small_kernel (n = 2..64, ragged totals), the fp32 kernels
+(E4M3 / INT8 / INT4, the register epilogues and the tcgen05 kernel: n = 4096 INT4, 16384, 32768,
+contiguous and row grids, ragged last tiles), fwht_small_kernel (n = 2..64, ragged totals), the fp32 kernels
 (incl. the 2-CTA cluster n = 2^15) and the quant-lab kernels."""
 import os
 import sys
@@ -36,5 +37,13 @@ for n, m in ((2, 5), (64, 9), (2048, 3), (16384, 2), (32768, 3)):
     hc.hadacore_fwht(x)
     hc.fake_quant(x, "int4", per_tensor=True)
     hc.row_sq_error(x, x)
+for dt in (torch.float16, torch.bfloat16):  # the tcgen05 fused quantization: ragged tiles, row grids
+    for n, m in ((16384, 5), (32768, 2), (8192, 9)):
+        x = torch.randn(m, n, device=dev).to(dt)
+        for q in ("e4m3", "int8", "int4"):
+            hc.hadacore_fwht_quant(x, q)
+    qkv = torch.randn(3, 3, 2, 16384, device=dev).to(dt)
+    for q in ("e4m3", "int4"):
+        hc.hadacore_fwht_quant_strided(qkv[:, 0:2], q)
 torch.cuda.synchronize()
 print("sanitize probe done")
