@@ -39,7 +39,7 @@ __host__ __device__ constexpr uint32_t idesc(int M, int N) {
          (uint32_t(M >> 4) << 24);
 }
 
-template <bool BF, int MM = 128>
+template <bool BF, int MM = 128, int LANE_OFF = 0>
 __global__ void __launch_bounds__(128) probe(const uint16_t* X, const uint16_t* H, float* D, int reps,
                                              long long* cycles) {
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -78,7 +78,7 @@ __global__ void __launch_bounds__(128) probe(const uint16_t* X, const uint16_t* 
         const uint32_t acc = kk > 0 ? 1u : 0u;
         asm volatile(
             "{.reg .pred p; setp.ne.b32 p, %4, 0;\n"
-            "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;}" ::"r"(tmem),
+            "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;}" ::"r"(tmem + (uint32_t(LANE_OFF) << 16)),
             "l"(ad), "l"(bd), "r"(ID), "r"(acc));
       }
     }
@@ -259,12 +259,12 @@ void probe_m64() {
   CK(cudaMemcpy(dX, X.data(), M * K * 2, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(dH, H.data(), M * K * 2, cudaMemcpyHostToDevice));
   CK(cudaMemset(dD, 0, M * 128 * 4));
-  CK(cudaFuncSetAttribute(probe<false, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536 + 1024));
-  probe<false, 64><<<1, 128, 65536 + 1024>>>(dX, dH, dD, 1, dc);
+  CK(cudaFuncSetAttribute(probe<false, 64, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536 + 1024));
+  probe<false, 64, 16><<<1, 128, 65536 + 1024>>>(dX, dH, dD, 1, dc);
   CK(cudaDeviceSynchronize());
   std::vector<float> D(M * 128);
   CK(cudaMemcpy(D.data(), dD, M * 128 * 4, cudaMemcpyDeviceToHost));
-  printf("M=64 lane map (lane: row matched over cols 0..127, or -1):\n");
+  printf("M=64 with D lane offset 16, lane map (lane: row matched over cols 0..127, or -1):\n");
   for (int lane = 0; lane < 128; ++lane) {
     int found = -1, cols = 0;
     for (int row = 0; row < 64 && found < 0; ++row) {
