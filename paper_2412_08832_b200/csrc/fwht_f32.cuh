@@ -646,6 +646,187 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((NT + 1) * 32, 1)
   cluster_sync_all();  // no CTA leaves while its partner may still multicast into it or arrive remotely
 }
 
+// ---------------------------------------------------------------- n = 2^15, one CTA, chunk ring
+// (round 2; VERDICT r1 "fp32 at n = 2^15", third design).  A row (128 KiB) streams into a
+// ring of S chunk slots of CH floats (14 x 16 KiB = 224 KiB), so one row is resident while
+// most of the next one is already in flight.  The bits of the index split by where their
+// butterflies can run:
+//   bits 0..9  lie inside a chunk: consumer group g (GT = CH/32 threads) takes the row's
+//              chunks c = g mod NG as they land -- phase 0 (bits 0..4, 32 contiguous floats
+//              per lane, sign-folded granule butterflies as fwht_f32_fast_kernel) and phase
+//              1 (bits 5..9, 32-float columns at stride 32) -- with only a group barrier;
+//   bits 10..14 span the chunks: after a barrier over all consumers, phase 2 takes
+//              32-float columns at stride 1024 (value t of column col is element
+//              t * 1024 + col, in chunk t * 1024 / CH) straight from the chunk slots,
+//              applies `scale` and writes back in place.
+// Every element makes the same shared-memory trips as in the n <= 2^14 kernel (TMA in,
+// three phases, TMA out).  The producer warp (one thread) loads chunk u (the CTA's u-th,
+// rows in order) into slot u mod S and, once the consumers have signalled a row done
+// (row_done, NT arrivals), stores its chunks -- one bulk group per chunk, so a slot is
+// refilled as soon as ITS store has been read, not the whole row's.  S <= 2 CPR - 1 keeps
+// the row_done parity unambiguous: row k+1 cannot finish before row k's store was issued.
+// Rows are static (row = blockIdx.x + k * gridDim.x), one CTA per SM.
+__device__ __forceinline__ void bulk_wait_read_upto(int pending) {  // wait until <= pending groups read
+  switch (pending < 0 ? 0 : pending) {
+    case 0: bulk_wait_read<0>(); break;
+    case 1: bulk_wait_read<1>(); break;
+    case 2: bulk_wait_read<2>(); break;
+    case 3: bulk_wait_read<3>(); break;
+    case 4: bulk_wait_read<4>(); break;
+    case 5: bulk_wait_read<5>(); break;
+    case 6: bulk_wait_read<6>(); break;
+    default: bulk_wait_read<7>(); break;  // stricter than asked: safe
+  }
+}
+
+template <int CH, int S, int NT>
+__global__ void __launch_bounds__((NT + 1) * 32, 1)
+    fwht_f32_ring_kernel(const float* __restrict__ in, float* __restrict__ out, int64_t m, float scale) {
+  constexpr int N = 32768, CPR = N / CH, CB = CH * 4;
+  constexpr int GT = CH / 32;         // threads of a group: one 32-float item / column each
+  constexpr int NG = NT * 32 / GT;    // consumer groups
+  static_assert(CH >= 1024 && CH % 1024 == 0 && CPR >= 2, "chunks hold whole 1024-float blocks");
+  static_assert(NG * GT == NT * 32 && NG >= 1 && CPR % NG == 0 && NG + 1 < 16, "groups");
+  static_assert(S >= CPR && S <= 2 * CPR - 1, "ring: one row resident, row_done parity unambiguous");
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * CB);
+  uint64_t* row_done = full + S;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t rows = m > int64_t(blockIdx.x) ? (m - 1 - int64_t(blockIdx.x)) / gridDim.x + 1 : 0;
+
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int s = 0; s < S; ++s) mbar_init(&full[s], 1);
+    mbar_init(row_done, NT);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    fence_proxy_async_smem();
+  }
+  __syncthreads();
+  pdl_launch_dependents();
+
+  if (warp == NT) {
+    if (lane == 0) {
+      pdl_wait();
+      const uint64_t pol = policy_evict_first();
+      const int64_t total = rows * CPR;
+      int64_t stored = 0;  // chunks whose store has been issued (in chunk order)
+      auto store_row = [&](int64_t k) {
+        mbar_wait(row_done, uint32_t(k & 1));
+        jitter(8, uint32_t(k));
+        const int64_t r = int64_t(blockIdx.x) + k * gridDim.x;
+#pragma unroll 1
+        for (int c = 0; c < CPR; ++c) {
+          bulk_s2g(out + r * N + c * CH, smem + int((k * CPR + c) % S) * CB, CB);
+          bulk_commit();
+        }
+        stored += CPR;
+      };
+      for (int64_t u = 0; u < total; ++u) {
+        const int s = int(u % S);
+        if (u >= S) {  // slot s held chunk u - S: its row must be done and its store read
+          while (stored <= u - S) store_row(stored / CPR);
+          bulk_wait_read_upto(int(stored - (u - S) - 1));
+          jitter(9, uint32_t(u));
+        }
+        const int64_t r = int64_t(blockIdx.x) + (u / CPR) * gridDim.x;
+        mbar_arrive_expect_tx(&full[s], CB);
+        bulk_g2s(smem + s * CB, in + r * N + (u % CPR) * CH, CB, &full[s], pol);
+      }
+      while (stored < total) store_row(stored / CPR);
+      bulk_wait_all();
+    }
+    return;
+  }
+
+  // ---------------- consumers
+  const int grp = threadIdx.x / GT, gtid = threadIdx.x - grp * GT, tid = threadIdx.x;
+  const uint32_t c = uint32_t(lane) & 7u;
+  float al[3];
+#pragma unroll
+  for (int b = 0; b < 3; ++b) al[b] = ((c >> b) & 1u) ? -1.f : 1.f;
+  for (int64_t k = 0; k < rows; ++k) {
+    // ---- bits 0..9, chunk by chunk as they land
+#pragma unroll 1
+    for (int cc = grp; cc < CPR; cc += NG) {
+      const int64_t u = k * CPR + cc;
+      const int s = int(u % S);
+      mbar_wait(&full[s], uint32_t((u / S) & 1));
+      float* const tb = reinterpret_cast<float*>(smem + s * CB);
+      float v[32];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float4 w = *reinterpret_cast<const float4*>(tb + 4 * (gtid * 8 + int(uint32_t(j) ^ c)));
+        v[4 * j] = w.x;
+        v[4 * j + 1] = w.y;
+        v[4 * j + 2] = w.z;
+        v[4 * j + 3] = w.w;
+      }
+#pragma unroll
+      for (int b = 0; b < 2; ++b)
+#pragma unroll
+        for (int e = 0; e < 32; ++e)
+          if (!(e & (1 << b))) {
+            const float p0 = v[e], p1 = v[e | (1 << b)];
+            v[e] = p0 + p1;
+            v[e | (1 << b)] = p0 - p1;
+          }
+#pragma unroll
+      for (int b = 0; b < 3; ++b)
+#pragma unroll
+        for (int e = 0; e < 32; ++e)
+          if (!(e & (4 << b))) {
+            const float p0 = v[e], p1 = v[e | (4 << b)];
+            v[e] = fmaf(p0, al[b], p1);
+            v[e | (4 << b)] = fmaf(p1, -al[b], p0);
+          }
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        *reinterpret_cast<float4*>(tb + 4 * (gtid * 8 + int(uint32_t(j) ^ c))) =
+            make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+      named_bar_sync(1 + grp, GT);
+      f32_phase<CH, 5, 5, false, GT / 32>(tb, 1, gtid, 1.f);
+    }
+    // ---- bits 10..14 across the row's chunks
+    named_bar_sync(1 + NG, NT * 32);
+    jitter(10, uint32_t(k));
+    uint32_t base[CPR];  // shared address of chunk j's slot
+    {
+      const int s0 = int((k * CPR) % S);
+#pragma unroll
+      for (int j = 0; j < CPR; ++j) base[j] = smem_addr(smem + (s0 + j < S ? s0 + j : s0 + j - S) * CB);
+    }
+#pragma unroll 1
+    for (int col = tid; col < 1024; col += NT * 32) {
+      float v[32];
+#pragma unroll
+      for (int t = 0; t < 32; ++t) {
+        const uint32_t a = base[(t * 1024) / CH] + 4u * uint32_t(((t * 1024) % CH) + col);
+        asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v[t]) : "r"(a) : "memory");
+      }
+#pragma unroll
+      for (int b = 0; b < 5; ++b)
+#pragma unroll
+        for (int e = 0; e < 32; ++e)
+          if (!(e & (1 << b))) {
+            const float p0 = v[e], p1 = v[e | (1 << b)];
+            v[e] = p0 + p1;
+            v[e | (1 << b)] = p0 - p1;
+          }
+#pragma unroll
+      for (int t = 0; t < 32; ++t) {
+        const uint32_t a = base[(t * 1024) / CH] + 4u * uint32_t(((t * 1024) % CH) + col);
+        asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"(v[t] * scale) : "memory");
+      }
+    }
+    fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+      jitter(11, uint32_t(k));
+      mbar_arrive(row_done);
+    }
+  }
+}
+
 // n = 2^15 in fp32, second pass: rows are [a | b] with a, b = H_2^14-transformed halves;
 // out = scale * [a + b | a - b] (the remaining H_2 factor over the top index bit).
 __global__ void f32_half_butterfly_kernel(const float* __restrict__ in, float* __restrict__ out, int64_t m,

@@ -610,7 +610,30 @@ hadacore_status_t launch_f32_fast(const void* in, void* out, int64_t m, float sc
 }
 
 hadacore_status_t launch_f32_32k(const void* in, void* out, int64_t m, float scale, cudaStream_t stream) {
-#ifndef HC_F32_TWO_PASS
+#if !defined(HC_F32_TWO_PASS) && !defined(HC_F32_PAIR) && !defined(HC_F32_MC)
+  // default: one CTA per SM, the row streamed through a ring of chunk slots
+  // (fwht_f32_ring_kernel)
+#ifndef HC_RING_CH
+#define HC_RING_CH 4096
+#endif
+#ifndef HC_RING_NT
+#define HC_RING_NT 16
+#endif
+  constexpr int ch = HC_RING_CH, nt = HC_RING_NT;
+  constexpr int slots = (227 * 1024 - 256) / (ch * 4) < 2 * (32768 / ch) - 1 ? (227 * 1024 - 256) / (ch * 4)
+                                                                              : 2 * (32768 / ch) - 1;
+  constexpr int smem = slots * ch * 4 + (slots + 1) * 8;
+  auto kern = fwht_f32_ring_kernel<ch, slots, nt>;
+  static std::atomic<uint64_t> attr_done{0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return HADACORE_ERR_CUDA;
+  if (!ensure_smem_attr(kern, smem, attr_done, dev)) return HADACORE_ERR_CUDA;
+  const int64_t ctas = m < int64_t(sm_count(dev)) ? m : int64_t(sm_count(dev));
+  if (launch_pdl(kern, int(ctas), (nt + 1) * 32, smem, stream, static_cast<const float*>(in),
+                 static_cast<float*>(out), m, scale) != cudaSuccess)
+    return HADACORE_ERR_CUDA;
+  return cudaPeekAtLastError() == cudaSuccess ? HADACORE_OK : HADACORE_ERR_CUDA;
+#elif !defined(HC_F32_TWO_PASS)
   // one launch of 2-CTA clusters, a row per cluster: fwht_f32_pair_kernel (DSMEM exchange of
   // the transformed halves; default) or fwht_f32_mc_kernel (HC_F32_MC: top bit first,
   // multicast input halves -- measured slower, 3.2-3.6 vs 4.8 TB/s: profiles/r02_f32_mc_ab.txt)
