@@ -666,6 +666,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((NT + 1) * 32, 1)
 // refilled as soon as ITS store has been read, not the whole row's.  S <= 2 CPR - 1 keeps
 // the row_done parity unambiguous: row k+1 cannot finish before row k's store was issued.
 // Rows are static (row = blockIdx.x + k * gridDim.x), one CTA per SM.
+#ifndef HC_RING_STCS
+#define HC_RING_STCS 0
+#endif
 __device__ __forceinline__ void bulk_wait_read_upto(int pending) {  // wait until <= pending groups read
   switch (pending < 0 ? 0 : pending) {
     case 0: bulk_wait_read<0>(); break;
@@ -679,7 +682,7 @@ __device__ __forceinline__ void bulk_wait_read_upto(int pending) {  // wait unti
   }
 }
 
-template <int CH, int S, int NT>
+template <int CH, int S, int NT, bool DIRECT>
 __global__ void __launch_bounds__((NT + 1) * 32, 1)
     fwht_f32_ring_kernel(const float* __restrict__ in, float* __restrict__ out, int64_t m, float scale) {
   constexpr int N = 32768, CPR = N / CH, CB = CH * 4;
@@ -688,6 +691,8 @@ __global__ void __launch_bounds__((NT + 1) * 32, 1)
   static_assert(CH >= 1024 && CH % 1024 == 0 && CPR >= 2, "chunks hold whole 1024-float blocks");
   static_assert(NG * GT == NT * 32 && NG >= 1 && CPR % NG == 0 && NG + 1 < 16, "groups");
   static_assert(S >= CPR && S <= 2 * CPR - 1, "ring: one row resident, row_done parity unambiguous");
+  constexpr int CPT = 1024 / (NT * 32);  // DIRECT: adjacent columns per thread in the cross-chunk phase
+  static_assert(!DIRECT || CPT == 2 || CPT == 4, "DIRECT holds the row in registers: 8 or 16 consumer warps");
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * CB);
   uint64_t* row_done = full + S;
@@ -709,15 +714,17 @@ __global__ void __launch_bounds__((NT + 1) * 32, 1)
       pdl_wait();
       const uint64_t pol = policy_evict_first();
       const int64_t total = rows * CPR;
-      int64_t stored = 0;  // chunks whose store has been issued (in chunk order)
+      int64_t stored = 0;  // chunks whose store has been issued (in chunk order) / released (DIRECT)
       auto store_row = [&](int64_t k) {
         mbar_wait(row_done, uint32_t(k & 1));
         jitter(8, uint32_t(k));
-        const int64_t r = int64_t(blockIdx.x) + k * gridDim.x;
+        if constexpr (!DIRECT) {
+          const int64_t r = int64_t(blockIdx.x) + k * gridDim.x;
 #pragma unroll 1
-        for (int c = 0; c < CPR; ++c) {
-          bulk_s2g(out + r * N + c * CH, smem + int((k * CPR + c) % S) * CB, CB);
-          bulk_commit();
+          for (int c = 0; c < CPR; ++c) {
+            bulk_s2g(out + r * N + c * CH, smem + int((k * CPR + c) % S) * CB, CB);
+            bulk_commit();
+          }
         }
         stored += CPR;
       };
@@ -725,14 +732,16 @@ __global__ void __launch_bounds__((NT + 1) * 32, 1)
         const int s = int(u % S);
         if (u >= S) {  // slot s held chunk u - S: its row must be done and its store read
           while (stored <= u - S) store_row(stored / CPR);
-          bulk_wait_read_upto(int(stored - (u - S) - 1));
+          if constexpr (!DIRECT) bulk_wait_read_upto(int(stored - (u - S) - 1));
           jitter(9, uint32_t(u));
         }
         const int64_t r = int64_t(blockIdx.x) + (u / CPR) * gridDim.x;
         mbar_arrive_expect_tx(&full[s], CB);
         bulk_g2s(smem + s * CB, in + r * N + (u % CPR) * CH, CB, &full[s], pol);
       }
-      while (stored < total) store_row(stored / CPR);
+      if constexpr (!DIRECT) {
+        while (stored < total) store_row(stored / CPR);
+      }
       bulk_wait_all();
     }
     return;
@@ -795,34 +804,82 @@ __global__ void __launch_bounds__((NT + 1) * 32, 1)
 #pragma unroll
       for (int j = 0; j < CPR; ++j) base[j] = smem_addr(smem + (s0 + j < S ? s0 + j : s0 + j - S) * CB);
     }
-#pragma unroll 1
-    for (int col = tid; col < 1024; col += NT * 32) {
-      float v[32];
+    if constexpr (DIRECT) {
+      // the whole row into registers (CPT adjacent columns per thread), release the slots
+      // at once, then butterflies and vector stores straight to global memory
+      float v[32][CPT];
 #pragma unroll
       for (int t = 0; t < 32; ++t) {
-        const uint32_t a = base[(t * 1024) / CH] + 4u * uint32_t(((t * 1024) % CH) + col);
-        asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v[t]) : "r"(a) : "memory");
+        const uint32_t a = base[(t * 1024) / CH] + 4u * uint32_t(((t * 1024) % CH) + CPT * tid);
+        if constexpr (CPT == 4) {
+          asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                       : "=f"(v[t][0]), "=f"(v[t][1]), "=f"(v[t][2]), "=f"(v[t][3])
+                       : "r"(a)
+                       : "memory");
+        } else {
+          asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v[t][0]), "=f"(v[t][1]) : "r"(a) : "memory");
+        }
+      }
+      __syncwarp();
+      if (lane == 0) {
+        jitter(11, uint32_t(k));
+        mbar_arrive(row_done);  // this warp has read the row: the producer may refill its slots
       }
 #pragma unroll
       for (int b = 0; b < 5; ++b)
 #pragma unroll
         for (int e = 0; e < 32; ++e)
-          if (!(e & (1 << b))) {
-            const float p0 = v[e], p1 = v[e | (1 << b)];
-            v[e] = p0 + p1;
-            v[e | (1 << b)] = p0 - p1;
-          }
+          if (!(e & (1 << b)))
+#pragma unroll
+            for (int q = 0; q < CPT; ++q) {
+              const float p0 = v[e][q], p1 = v[e | (1 << b)][q];
+              v[e][q] = p0 + p1;
+              v[e | (1 << b)][q] = p0 - p1;
+            }
+      float* const orow = out + (int64_t(blockIdx.x) + k * gridDim.x) * N + CPT * tid;
 #pragma unroll
       for (int t = 0; t < 32; ++t) {
-        const uint32_t a = base[(t * 1024) / CH] + 4u * uint32_t(((t * 1024) % CH) + col);
-        asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"(v[t] * scale) : "memory");
+        if constexpr (CPT == 4) {
+          *reinterpret_cast<float4*>(orow + t * 1024) =
+              make_float4(v[t][0] * scale, v[t][1] * scale, v[t][2] * scale, v[t][3] * scale);
+        } else {
+#if HC_RING_STCS
+          __stcs(reinterpret_cast<float2*>(orow + t * 1024), make_float2(v[t][0] * scale, v[t][1] * scale));
+#else
+          *reinterpret_cast<float2*>(orow + t * 1024) = make_float2(v[t][0] * scale, v[t][1] * scale);
+#endif
+        }
       }
-    }
-    fence_proxy_async_smem();
-    __syncwarp();
-    if (lane == 0) {
-      jitter(11, uint32_t(k));
-      mbar_arrive(row_done);
+    } else {
+#pragma unroll 1
+      for (int col = tid; col < 1024; col += NT * 32) {
+        float v[32];
+#pragma unroll
+        for (int t = 0; t < 32; ++t) {
+          const uint32_t a = base[(t * 1024) / CH] + 4u * uint32_t(((t * 1024) % CH) + col);
+          asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v[t]) : "r"(a) : "memory");
+        }
+#pragma unroll
+        for (int b = 0; b < 5; ++b)
+#pragma unroll
+          for (int e = 0; e < 32; ++e)
+            if (!(e & (1 << b))) {
+              const float p0 = v[e], p1 = v[e | (1 << b)];
+              v[e] = p0 + p1;
+              v[e | (1 << b)] = p0 - p1;
+            }
+#pragma unroll
+        for (int t = 0; t < 32; ++t) {
+          const uint32_t a = base[(t * 1024) / CH] + 4u * uint32_t(((t * 1024) % CH) + col);
+          asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"(v[t] * scale) : "memory");
+        }
+      }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        jitter(11, uint32_t(k));
+        mbar_arrive(row_done);
+      }
     }
   }
 }

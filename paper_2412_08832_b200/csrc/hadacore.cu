@@ -614,16 +614,19 @@ hadacore_status_t launch_f32_32k(const void* in, void* out, int64_t m, float sca
   // default: one CTA per SM, the row streamed through a ring of chunk slots
   // (fwht_f32_ring_kernel)
 #ifndef HC_RING_CH
-#define HC_RING_CH 4096
+#define HC_RING_CH 2048
 #endif
 #ifndef HC_RING_NT
 #define HC_RING_NT 16
+#endif
+#ifndef HC_RING_DIRECT
+#define HC_RING_DIRECT 1
 #endif
   constexpr int ch = HC_RING_CH, nt = HC_RING_NT;
   constexpr int slots = (227 * 1024 - 256) / (ch * 4) < 2 * (32768 / ch) - 1 ? (227 * 1024 - 256) / (ch * 4)
                                                                               : 2 * (32768 / ch) - 1;
   constexpr int smem = slots * ch * 4 + (slots + 1) * 8;
-  auto kern = fwht_f32_ring_kernel<ch, slots, nt>;
+  auto kern = fwht_f32_ring_kernel<ch, slots, nt, bool(HC_RING_DIRECT)>;
   static std::atomic<uint64_t> attr_done{0};
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return HADACORE_ERR_CUDA;

@@ -2,8 +2,10 @@
 with a targeted stress test"): libhadacore_jitter.so is the product source built with
 -DHC_JITTER, which sleeps for random 0-4 us at a quarter of the synchronization points of
 
-* fwht_f32_pair_kernel (fp32 n = 2^15, 2-CTA clusters: DSMEM exchange with remote
-  mbarrier arrivals `ready` / `consumed`, and the producer's store / refill), and
+* fwht_f32_ring_kernel (fp32 n = 2^15, the default: chunk slots refilled once the row's
+  consumers released them, per-group chunk phases, the cross-chunk phase after an
+  all-consumer barrier; fwht_f32_pair_kernel, the HC_F32_PAIR build, has its own sites:
+  DSMEM exchange with remote mbarrier arrivals `ready` / `consumed`), and
 * fwht_quant_tc_kernel (fused quantization n >= 16384: producer / phase-A / MMA / epilogue
   warp roles, TMEM double buffer, half-stage refills, code-store handoff).
 
@@ -54,7 +56,7 @@ def stream():
 
 
 @pytest.mark.timeout(300)
-def test_f32_pair_kernel_under_jitter(hc, jitter_lib):
+def test_f32_32k_kernel_under_jitter(hc, jitter_lib):
     n = 32768
     m = 3 * 148 + 7  # several rows per cluster, ragged over the clusters
     x = synthetic.generate(m, n, torch.float32, 9191).cuda()

@@ -37,6 +37,9 @@ for n, m in ((2, 5), (64, 9), (2048, 3), (16384, 2), (32768, 3)):
     hc.hadacore_fwht(x)
     hc.fake_quant(x, "int4", per_tensor=True)
     hc.row_sq_error(x, x)
+x = torch.randn(160, 32768, device=dev)  # fp32 ring kernel: some CTAs take 2 rows, so chunk slots are reused
+hc.hadacore_fwht(x)
+hc.hadacore_fwht(x, out=x)
 for dt in (torch.float16, torch.bfloat16):  # the tcgen05 fused quantization: ragged tiles, row grids
     for n, m in ((16384, 5), (32768, 2), (8192, 9)):
         x = torch.randn(m, n, device=dev).to(dt)
