@@ -884,6 +884,142 @@ __global__ void __launch_bounds__((NT + 1) * 32, 1)
   }
 }
 
+// ---------------------------------------------------------------- n = 2^15, one CTA, chunks released early
+// (round 2, after fwht_f32_ring_kernel: there a row's slots stay occupied until its last
+// chunk has landed and been transformed, so only S - CPR slots of loads are in flight at the
+// row boundary).  Here every consumer thread takes part in every chunk: phase 0 and phase 1
+// (bits 0..9) on the chunk with CTA-wide barriers, then each thread reads ITS values of the
+// cross-chunk phase out of the chunk -- columns 2 tid, 2 tid + 1 at every 1024-block the
+// chunk holds -- into registers and the warp releases the slot at once (empty[s], NT
+// arrivals).  After the row's last chunk a thread holds 2 complete columns of 32 values:
+// bits 10..14 as register butterflies, `scale`, 8-byte stores straight to global memory.
+// A slot is thus occupied for one chunk's transform only, and S - 1 chunks of loads stay
+// in flight all the time.
+template <int CH, int S, int NT>
+__global__ void __launch_bounds__((NT + 1) * 32, 1)
+    fwht_f32_stream_kernel(const float* __restrict__ in, float* __restrict__ out, int64_t m, float scale) {
+  constexpr int N = 32768, CPR = N / CH, CB = CH * 4;
+  constexpr int TPC = CH / 1024;  // 1024-blocks (values of a cross-chunk column) per chunk
+  static_assert(NT * 32 == 512, "a thread holds columns 2 tid, 2 tid + 1 of the 1024");
+  static_assert(CH >= 1024 && CH % 1024 == 0 && CPR >= 2 && S >= 2, "chunks");
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * CB);
+  uint64_t* empty = full + S;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t rows = m > int64_t(blockIdx.x) ? (m - 1 - int64_t(blockIdx.x)) / gridDim.x + 1 : 0;
+
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NT);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    fence_proxy_async_smem();
+  }
+  __syncthreads();
+  pdl_launch_dependents();
+
+  if (warp == NT) {
+    if (lane == 0) {
+      pdl_wait();
+      const uint64_t pol = policy_evict_first();
+      const int64_t total = rows * CPR;
+      for (int64_t u = 0; u < total; ++u) {
+        const int s = int(u % S);
+        if (u >= S) mbar_wait(&empty[s], uint32_t(((u / S) - 1) & 1));  // chunk u - S released
+        jitter(12, uint32_t(u));
+        const int64_t r = int64_t(blockIdx.x) + (u / CPR) * gridDim.x;
+        mbar_arrive_expect_tx(&full[s], CB);
+        bulk_g2s(smem + s * CB, in + r * N + (u % CPR) * CH, CB, &full[s], pol);
+      }
+    }
+    return;
+  }
+
+  const int tid = threadIdx.x;
+  const uint32_t c = uint32_t(lane) & 7u;
+  float al[3];
+#pragma unroll
+  for (int b = 0; b < 3; ++b) al[b] = ((c >> b) & 1u) ? -1.f : 1.f;
+  for (int64_t k = 0; k < rows; ++k) {
+    float v[32][2];  // value t of columns 2 tid, 2 tid + 1 (element t * 1024 + col)
+#pragma unroll
+    for (int cc = 0; cc < CPR; ++cc) {
+      const int64_t u = k * CPR + cc;
+      const int s = int(u % S);
+      mbar_wait(&full[s], uint32_t((u / S) & 1));
+      float* const tb = reinterpret_cast<float*>(smem + s * CB);
+      // phase 0: bits 0..4, 32 contiguous floats per item
+#pragma unroll 1
+      for (int item = tid; item < CH / 32; item += NT * 32) {
+        float w[32];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float4 g = *reinterpret_cast<const float4*>(tb + 4 * (item * 8 + int(uint32_t(j) ^ c)));
+          w[4 * j] = g.x;
+          w[4 * j + 1] = g.y;
+          w[4 * j + 2] = g.z;
+          w[4 * j + 3] = g.w;
+        }
+#pragma unroll
+        for (int b = 0; b < 2; ++b)
+#pragma unroll
+          for (int e = 0; e < 32; ++e)
+            if (!(e & (1 << b))) {
+              const float p0 = w[e], p1 = w[e | (1 << b)];
+              w[e] = p0 + p1;
+              w[e | (1 << b)] = p0 - p1;
+            }
+#pragma unroll
+        for (int b = 0; b < 3; ++b)
+#pragma unroll
+          for (int e = 0; e < 32; ++e)
+            if (!(e & (4 << b))) {
+              const float p0 = w[e], p1 = w[e | (4 << b)];
+              w[e] = fmaf(p0, al[b], p1);
+              w[e | (4 << b)] = fmaf(p1, -al[b], p0);
+            }
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          *reinterpret_cast<float4*>(tb + 4 * (item * 8 + int(uint32_t(j) ^ c))) =
+              make_float4(w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
+      }
+      named_bar_sync(1, NT * 32);
+      f32_phase<CH, 5, 5, false, NT>(tb, 1, tid, 1.f);  // phase 1: bits 5..9
+      named_bar_sync(1, NT * 32);
+      // this thread's values of the cross-chunk phase, then release the slot
+#pragma unroll
+      for (int j = 0; j < TPC; ++j) {
+        const float2 g = *reinterpret_cast<const float2*>(tb + j * 1024 + 2 * tid);
+        v[cc * TPC + j][0] = g.x;
+        v[cc * TPC + j][1] = g.y;
+      }
+      __syncwarp();
+      if (lane == 0) {
+        jitter(13, uint32_t(u));
+        mbar_arrive(&empty[s]);
+      }
+    }
+    // bits 10..14 in registers, scale, stores
+#pragma unroll
+    for (int b = 0; b < 5; ++b)
+#pragma unroll
+      for (int e = 0; e < 32; ++e)
+        if (!(e & (1 << b)))
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            const float p0 = v[e][q], p1 = v[e | (1 << b)][q];
+            v[e][q] = p0 + p1;
+            v[e | (1 << b)][q] = p0 - p1;
+          }
+    float* const orow = out + (int64_t(blockIdx.x) + k * gridDim.x) * N + 2 * tid;
+#pragma unroll
+    for (int t = 0; t < 32; ++t)
+      *reinterpret_cast<float2*>(orow + t * 1024) = make_float2(v[t][0] * scale, v[t][1] * scale);
+  }
+}
+
 // n = 2^15 in fp32, second pass: rows are [a | b] with a, b = H_2^14-transformed halves;
 // out = scale * [a + b | a - b] (the remaining H_2 factor over the top index bit).
 __global__ void f32_half_butterfly_kernel(const float* __restrict__ in, float* __restrict__ out, int64_t m,

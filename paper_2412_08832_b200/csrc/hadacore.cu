@@ -622,11 +622,24 @@ hadacore_status_t launch_f32_32k(const void* in, void* out, int64_t m, float sca
 #ifndef HC_RING_DIRECT
 #define HC_RING_DIRECT 1
 #endif
+#ifndef HC_F32_STREAM
+#define HC_F32_STREAM 1  // fwht_f32_stream_kernel (chunks released as soon as read); 0: fwht_f32_ring_kernel
+#endif
+#ifndef HC_STREAM_CH
+#define HC_STREAM_CH 16384
+#endif
+#if HC_F32_STREAM
+  constexpr int ch = HC_STREAM_CH, nt = 16;
+  constexpr int slots = (227 * 1024 - 256) / (ch * 4);
+  constexpr int smem = slots * ch * 4 + 2 * slots * 8;
+  auto kern = fwht_f32_stream_kernel<ch, slots, nt>;
+#else
   constexpr int ch = HC_RING_CH, nt = HC_RING_NT;
   constexpr int slots = (227 * 1024 - 256) / (ch * 4) < 2 * (32768 / ch) - 1 ? (227 * 1024 - 256) / (ch * 4)
                                                                               : 2 * (32768 / ch) - 1;
   constexpr int smem = slots * ch * 4 + (slots + 1) * 8;
   auto kern = fwht_f32_ring_kernel<ch, slots, nt, bool(HC_RING_DIRECT)>;
+#endif
   static std::atomic<uint64_t> attr_done{0};
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return HADACORE_ERR_CUDA;
