@@ -16,10 +16,11 @@
 //             consecutive lanes take consecutive columns, so every LDS.32/STS.32 of
 //             a warp touches 32 consecutive words (conflict-free).
 // A named barrier over the consumer warps separates phases; the last phase applies
-// `scale`.  Rows of n = 2^15 (128 KiB of fp32) do not fit a double-buffered ring in
-// one CTA: fwht_f32_pair_kernel splits each over a 2-CTA cluster (below); the
-// two-pass variant (2^14 halves + f32_half_butterfly_kernel) is the HC_F32_TWO_PASS
-// build, kept for A/B.
+// `scale`.  Rows of n = 2^15 (128 KiB of fp32) do not fit a double-buffered ring of
+// whole rows in one CTA: fwht_f32_stream_kernel (the default, below) streams them in
+// 64 KiB chunks and gathers the cross-chunk phase into registers; fwht_f32_ring_kernel
+// (HC_F32_STREAM=0), fwht_f32_pair_kernel (HC_F32_PAIR, 2-CTA clusters), fwht_f32_mc_kernel
+// (HC_F32_MC) and the two-pass variant (HC_F32_TWO_PASS) are kept for A/B.
 #pragma once
 #include "fwht_small.cuh"
 
