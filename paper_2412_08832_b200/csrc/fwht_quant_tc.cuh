@@ -119,13 +119,26 @@ constexpr bool kTcNegB = false;
 #ifndef HC_QTC_UA
 #define HC_QTC_UA 2
 #endif
+// HC_QTC_CB = 1: each epilogue group stages its tile's codes in a buffer of its own and
+// stores them itself, so a stage is free for the next tile as soon as the MMAs have read
+// it (2 stages); 0: codes staged in the stage's lower half, stored by the producer before
+// it refills that half (3 stages)
+#ifndef HC_QTC_CB
+#define HC_QTC_CB 1
+#endif
+constexpr bool kTcCodeBuf = HC_QTC_CB != 0;
 constexpr int kTcTile = 65536;   // 128 chunks of 256 16-bit elements
 constexpr int kTcHBytes = 32768; // H_128, 16-bit, K-major SW128 (two 64-column atoms)
 constexpr int kTcCols = 512;     // TMEM columns: two tiles x (y_lo 128 + y_hi 128)
 
-template <int STAGES, int NE>
+template <int QT>
+__host__ __device__ constexpr int tc_code_bytes() {  // a tile's codes
+  return QT == QT_INT4 ? kTcTile / 4 : kTcTile / 2;
+}
+template <int STAGES, int NE, int QT, int EG>
 __host__ __device__ constexpr int tc_smem_bytes() {
-  return STAGES * kTcTile + kTcHBytes + int(sizeof(SchedCtl)) + (4 * STAGES + 4) * 8 + 32 + 2 * NE * 2 * 4;
+  return STAGES * kTcTile + (kTcCodeBuf ? EG * tc_code_bytes<QT>() : 0) + kTcHBytes + int(sizeof(SchedCtl)) +
+         (4 * STAGES + 4) * 8 + 32 + 2 * NE * 2 * 4;
 }
 
 // Template parameters: N row length (4096..32768), DT dtype, QT code type, STAGES ring
@@ -148,7 +161,8 @@ __global__ void __launch_bounds__((EG * NE + NA + 2) * 32, 1)
   const int64_t num_tiles = g.num_tiles;
 
   extern __shared__ __align__(1024) uint8_t smem[];
-  uint8_t* const Hs = smem + STAGES * kTcTile;
+  uint8_t* const codebuf = smem + STAGES * kTcTile;  // kTcCodeBuf: EG code buffers (1024-aligned)
+  uint8_t* const Hs = codebuf + (kTcCodeBuf ? EG * tc_code_bytes<QT>() : 0);
   SchedCtl* ctl = reinterpret_cast<SchedCtl*>(Hs + kTcHBytes);
   uint64_t* full = reinterpret_cast<uint64_t*>(ctl + 1);  // TMA -> phase A
   uint64_t* adone = full + STAGES;                         // phase A -> MMA (NA arrivals)
@@ -275,9 +289,11 @@ __global__ void __launch_bounds__((EG * NE + NA + 2) * 32, 1)
             trace(it + STAGES, 0);
             mbar_arrive_expect_tx(&full[s], kTcTile);
             load_half(s, nt, 1);
+            if constexpr (kTcCodeBuf) load_half(s, nt, 0);  // the codes live elsewhere: the whole stage is free
             next_tile(nt);
           }
         }
+        if constexpr (kTcCodeBuf) continue;
         mbar_wait(&cready[s], ph);  // the codes of tile t are staged in the lower half
         jitter(11, it);
         const TileRows tr(g, t);
@@ -420,7 +436,11 @@ __global__ void __launch_bounds__((EG * NE + NA + 2) * 32, 1)
       if (warp == 0 && lane == 0) trace(it, 4);
       tc_fence_after();
       const int tile = buf_tile[b], s = buf_stage[b];
-      if (tile < 0) break;
+      const bool elect = ew == 0 && lane == 0;  // issues this group's code stores (kTcCodeBuf)
+      if (tile < 0) {
+        if (kTcCodeBuf && elect) bulk_wait_all();
+        break;
+      }
       if (HC_TC_DIAG & 2) {
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[b]);
@@ -448,6 +468,7 @@ __global__ void __launch_bounds__((EG * NE + NA + 2) * 32, 1)
       for (int o = 8; o >= 1; o >>= 1) au = max(au, __shfl_xor_sync(0xffffffffu, au, o));
       if ((lane & 15) == 0) red[b * NE * 2 + ew * 2 + (lane >> 4)] = __uint_as_float(au);
       jitter(14, it);
+      if (kTcCodeBuf && elect) bulk_wait_read<0>();  // this group's previous code store has read its buffer
       named_bar_sync(1 + eg, NE * 32);
       if (warp == 0 && lane == 0) trace(it, 5);
       float am = 0.f;
@@ -477,7 +498,7 @@ __global__ void __launch_bounds__((EG * NE + NA + 2) * 32, 1)
       // pass 2: codes, staged in the tile's (consumed) stage as the 128-byte-swizzled image of
       // its contiguous code block: 128-byte lines L (E4M3 / INT8: L = 2 m + h, the half-chunk
       // h of chunk row m; INT4: L = m), 16-byte granule q at (q ^ (L & 7))
-      uint8_t* const qs = smem + s * kTcTile;
+      uint8_t* const qs = kTcCodeBuf ? codebuf + eg * tc_code_bytes<QT>() : smem + s * kTcTile;
 #pragma unroll 1
       for (int j = j0; j < j0 + ((HC_TC_DIAG & 16) ? 0 : NJ); ++j) {
         float P[32], Rr[32];
@@ -530,7 +551,15 @@ __global__ void __launch_bounds__((EG * NE + NA + 2) * 32, 1)
       __syncwarp();
       if (lane == 0) {
         mbar_arrive(&tempty[b]);
-        mbar_arrive(&cready[s]);
+        if constexpr (!kTcCodeBuf) mbar_arrive(&cready[s]);
+      }
+      if constexpr (kTcCodeBuf) {  // the group's codes are staged: one TMA tensor store of them
+        named_bar_sync(1 + eg, NE * 32);
+        if (elect) {
+          const TileRows tr(g, tile);
+          tma_store_4d(&tm_q, 0, 0, int(tr.j0), int(tr.i0), qs);
+          bulk_commit();
+        }
       }
       if (warp == 0 && lane == 0) trace(it, 6);
     }

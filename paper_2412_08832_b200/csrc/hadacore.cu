@@ -296,7 +296,10 @@ bool ensure_smem_attr(Kern kern, int smem, std::atomic<uint64_t>& done, int dev)
 #define HC_QTC_NE 4
 #endif
 #ifndef HC_QTC_ST
-#define HC_QTC_ST 3
+#define HC_QTC_ST 3  // stages when the codes are staged in them (HC_QTC_CB = 0)
+#endif
+#ifndef HC_QTC_ST_CB
+#define HC_QTC_ST_CB 2  // stages with separate code buffers (HC_QTC_CB = 1, the default)
 #endif
 #ifndef HC_QTC_EG
 #define HC_QTC_EG 2  // epilogue groups on alternate tiles (INT4 +4.5 %: profiles/r02_quant_tc_eg.txt)
@@ -337,8 +340,8 @@ bool encode_tc_qmap(CUtensorMap* map, void* q, const Layout& L, int code_bytes, 
 template <int N, int DT, int QT>
 hadacore_status_t launch_qtc(const void* in, uint8_t* out_q, float* row_scale, const Layout& L, float scale,
                              cudaStream_t stream) {
-  constexpr int NA = HC_QTC_NA, NE = HC_QTC_NE, ST = HC_QTC_ST, EG = HC_QTC_EG;
-  constexpr int smem = tc_smem_bytes<ST, NE>();
+  constexpr int NA = HC_QTC_NA, NE = HC_QTC_NE, ST = kTcCodeBuf ? HC_QTC_ST_CB : HC_QTC_ST, EG = HC_QTC_EG;
+  constexpr int smem = tc_smem_bytes<ST, NE, QT, EG>();
   static_assert(smem <= 227 * 1024, "shared memory");
   static std::atomic<uint64_t> attr_done{0};
   int dev = 0;
