@@ -127,6 +127,13 @@ constexpr bool kTcNegB = false;
 #define HC_QTC_CB 1
 #endif
 constexpr bool kTcCodeBuf = HC_QTC_CB != 0;
+// HC_QTC_SPLIT = 1 (with HC_QTC_CB): the two half-tile boxes complete on their own mbarriers
+// (lower half first) and phase A takes the items of the lower half first, so it starts
+// while the upper half is still in flight
+#ifndef HC_QTC_SPLIT
+#define HC_QTC_SPLIT 0  // measured slower: E4M3 -4 %, INT4 -5..-13 % (profiles/r02_quant_tc_cb_ab.txt)
+#endif
+constexpr bool kTcSplit = kTcCodeBuf && HC_QTC_SPLIT != 0;
 constexpr int kTcTile = 65536;   // 128 chunks of 256 16-bit elements
 constexpr int kTcHBytes = 32768; // H_128, 16-bit, K-major SW128 (two 64-column atoms)
 constexpr int kTcCols = 512;     // TMEM columns: two tiles x (y_lo 128 + y_hi 128)
@@ -138,7 +145,7 @@ __host__ __device__ constexpr int tc_code_bytes() {  // a tile's codes
 template <int STAGES, int NE, int QT, int EG>
 __host__ __device__ constexpr int tc_smem_bytes() {
   return STAGES * kTcTile + (kTcCodeBuf ? EG * tc_code_bytes<QT>() : 0) + kTcHBytes + int(sizeof(SchedCtl)) +
-         (4 * STAGES + 4) * 8 + 32 + 2 * NE * 2 * 4;
+         (5 * STAGES + 4) * 8 + 32 + 2 * NE * 2 * 4;
 }
 
 // Template parameters: N row length (4096..32768), DT dtype, QT code type, STAGES ring
@@ -170,7 +177,8 @@ __global__ void __launch_bounds__((EG * NE + NA + 2) * 32, 1)
   uint64_t* ufree = cready + STAGES;                       // MMA commit -> producer: stage read
   uint64_t* tfull = ufree + STAGES;                        // [2] MMA -> epilogue (commit + arrive)
   uint64_t* tempty = tfull + 2;                            // [2] epilogue -> MMA (NE arrivals)
-  int* buf_tile = reinterpret_cast<int*>(tempty + 2);      // [2] tile id of each TMEM buffer
+  uint64_t* full_hi = tempty + 2;                          // kTcSplit: TMA -> phase A, upper half
+  int* buf_tile = reinterpret_cast<int*>(full_hi + STAGES); // [2] tile id of each TMEM buffer
   int* buf_stage = buf_tile + 2;                           // [2] ... and the stage it came from
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(buf_stage + 2);
   float* red = reinterpret_cast<float*>(tmem_slot + 2);    // [2][NE * 2] row-max partials
@@ -186,6 +194,7 @@ __global__ void __launch_bounds__((EG * NE + NA + 2) * 32, 1)
       mbar_init(&adone[s], NA);
       mbar_init(&cready[s], NE);
       mbar_init(&ufree[s], 1);
+      mbar_init(&full_hi[s], 1);
     }
 #pragma unroll
     for (int b = 0; b < 2; ++b) {
@@ -247,10 +256,10 @@ __global__ void __launch_bounds__((EG * NE + NA + 2) * 32, 1)
           tile = t + gridDim.x;
         }
       };
-      auto load_half = [&](int st, int64_t t, int half) {
+      auto load_half = [&](int st, int64_t t, int half, uint64_t* bar = nullptr) {
         const TileRows tr(g, t);
         tma_load_5d(smem + st * kTcTile + half * (kTcTile / 2), &tm_in, 0, 0, int(tr.j0), int(tr.i0), 2 * half,
-                    &full[st], pol);
+                    bar ? bar : &full[st], pol);
       };
       bool ended = false;
       for (int k = 0; k < STAGES; ++k) {  // fill the ring
@@ -264,9 +273,16 @@ __global__ void __launch_bounds__((EG * NE + NA + 2) * 32, 1)
         ctl->stage_tile[k] = int(t);
         if constexpr (kClc) clc_request(ctl);
         trace(k, 0);
-        mbar_arrive_expect_tx(&full[k], kTcTile);
-        load_half(k, t, 1);
-        load_half(k, t, 0);
+        if constexpr (kTcSplit) {
+          mbar_arrive_expect_tx(&full[k], kTcTile / 2);
+          load_half(k, t, 0);
+          mbar_arrive_expect_tx(&full_hi[k], kTcTile / 2);
+          load_half(k, t, 1, &full_hi[k]);
+        } else {
+          mbar_arrive_expect_tx(&full[k], kTcTile);
+          load_half(k, t, 1);
+          load_half(k, t, 0);
+        }
         next_tile(t);
       }
       for (int it = 0;; ++it) {
@@ -287,9 +303,16 @@ __global__ void __launch_bounds__((EG * NE + NA + 2) * 32, 1)
             ctl->stage_tile[s] = int(nt);
             if constexpr (kClc) clc_request(ctl);
             trace(it + STAGES, 0);
-            mbar_arrive_expect_tx(&full[s], kTcTile);
-            load_half(s, nt, 1);
-            if constexpr (kTcCodeBuf) load_half(s, nt, 0);  // the codes live elsewhere: the whole stage is free
+            if constexpr (kTcSplit) {  // the codes live elsewhere: the whole stage is free
+              mbar_arrive_expect_tx(&full[s], kTcTile / 2);
+              load_half(s, nt, 0);
+              mbar_arrive_expect_tx(&full_hi[s], kTcTile / 2);
+              load_half(s, nt, 1, &full_hi[s]);
+            } else {
+              mbar_arrive_expect_tx(&full[s], kTcTile);
+              load_half(s, nt, 1);
+              if constexpr (kTcCodeBuf) load_half(s, nt, 0);  // the codes live elsewhere: the whole stage is free
+            }
             next_tile(nt);
           }
         }
@@ -378,7 +401,17 @@ __global__ void __launch_bounds__((EG * NE + NA + 2) * 32, 1)
 #pragma unroll
           for (int u = 0; u < UA; ++u) {
             const int item = item0 + u * NA < ITEMS ? item0 + u * NA : item0;  // (tail: redo item0)
-            const uint32_t r = uint32_t(item / NLOOP), lp = uint32_t(item % NLOOP);
+            uint32_t r, lp;
+            if constexpr (kTcSplit) {  // lower-half items (top loop bit clear = segments 0-1) first
+              constexpr int HALF = ITEMS / 2, HL = NLOOP / 2;
+              const int hi = item >= HALF, rest = item - hi * HALF;
+              r = uint32_t(rest / HL);
+              lp = uint32_t(hi * HL + rest % HL);
+              if (hi) mbar_wait(&full_hi[s], uint32_t((it / STAGES) & 1));
+            } else {
+              r = uint32_t(item / NLOOP);
+              lp = uint32_t(item % NLOOP);
+            }
             const uint32_t gg = g_l | (lp << LOOP_SHIFT);
 #pragma unroll
             for (int xi = 0; xi < F; ++xi) {
