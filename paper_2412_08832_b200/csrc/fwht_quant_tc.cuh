@@ -21,10 +21,11 @@
 //     issues the MMAs;
 //   epilogue (NE warps): TMEM -> registers twice -- once for the row maximum of |y|
 //     (FADD2/FSUB2 butterflies, FMNMX3), once for the codes (FFMA2 + cvt, the quant4_fast epilogues of
-//     fwht_kernel.cuh).  The codes are staged, 128-byte swizzled, in the tile's own stage
-//     (consumed by then) and the producer writes them with one TMA tensor store per tile
-//     before it refills the stage (a thread's 32 contiguous codes sit 256 B from its
-//     neighbours': direct 16-byte stores touched 32 lines per instruction and cost 35 %).
+//     fwht_kernel.cuh).  The codes are staged, 128-byte swizzled, in the epilogue group's own
+//     code buffer and one elected thread of the group writes them with one TMA tensor store
+//     per tile (a thread's 32 contiguous codes sit 256 B from its neighbours': direct 16-byte
+//     stores touched 32 lines per instruction and cost 35 %); HC_QTC_CB=0 stages them in the
+//     tile's own (consumed) stage instead, stored by the producer before it refills it.
 //
 // Nothing is held in registers across the row-maximum barrier (the fp32 results live in
 // tensor memory: 2 x 256 columns, two tiles in flight), so the phase-A warps, the MMA
@@ -36,9 +37,9 @@
 // so the 128 chunk lines of one 64-element segment are consecutive 128-byte lines -- an MMA
 // operand with rows m = r * C + c at 128-byte pitch, 8-row groups 1024 B apart (SBO), and
 // the SWIZZLE_128B granule XOR (line & 7) that both the TMA unit and the tensor core apply.
-// Shared memory: 3 stages x 64 KiB + H_128 32 KiB.  The upper half of a stage (segments
-// 2-3) is refilled as soon as the MMAs have read it; the lower half first receives the
-// tile's codes (32 / 16 KiB), which the producer stores with one TMA tensor copy.
+// Shared memory: 2 stages x 64 KiB, refilled as soon as the MMAs have read them, + EG code
+// buffers (32 / 16 KiB) + H_128 32 KiB.  (HC_QTC_CB=0: 3 stages; the upper half of a stage is
+// refilled once the MMAs have read it, the lower half first receives the tile's codes.)
 #pragma once
 
 namespace hadacore {
