@@ -2,7 +2,7 @@
 dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --csv` launch list (one
 launch per (dtype, n), in the order tools/ncu_quant.py / ncu_one.py issue them).
 
-    python tools/traffic_json.py launches.csv out.json "<source note>" [alg_bytes_per_el] [ns]
+    python tools/traffic_json.py launches.csv out.json "<source note>" [alg_bytes_per_el] [ns] [dtypes: fp16,bf16]
 """
 import csv
 import io
@@ -21,12 +21,13 @@ def main():
     for r in csv.DictReader(io.StringIO(body)):
         per.setdefault(int(r["ID"]), {"kernel": r["Kernel Name"]})[r["Metric Name"]] = float(r["Metric Value"])
     launches = [per[k] for k in sorted(per)]
-    order = [(dt, n) for dt in ("fp16", "bf16") for n in ns]
+    dts = sys.argv[6].split(",") if len(sys.argv) > 6 else ["fp16", "bf16"]
+    order = [(dt, n) for dt in dts for n in ns]
     rows = []
     for (dt, n), l in zip(order, launches):
         rd, wr = l.get("dram__bytes_read.sum", 0.0), l.get("dram__bytes_write.sum", 0.0)
         dur = l.get("gpu__time_duration.sum", 0.0)
-        alg = bpe * (1 << 28) + 4.0 * ((1 << 28) // n)
+        alg = bpe * (1 << 28) + (4.0 * ((1 << 28) // n) if bpe < 4.0 else 0.0)  # + row scales when quantizing
         m = re.match(r"void (?:hadacore::)?(\w+)", l["kernel"])
         rows.append({"n": n, "dtype": dt, "kernel": m.group(1) if m else l["kernel"][:40], "dram_bytes": rd + wr,
                      "read_bytes": rd, "write_bytes": wr, "duration_us": dur / 1e3 if dur > 1e4 else dur,
