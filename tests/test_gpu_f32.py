@@ -104,10 +104,11 @@ def test_f32_full_size_sampled(hc, n):
     assert rel_l2_rows(widen(y[rows]), oracle.fwht(widen(x[rows]))).max() <= TOL
 
 
-def test_f32_pair_kernel_repeatability_stress(hc):
-    """The 2-CTA cluster kernel (fp32 n = 2^15) synchronizes the DSMEM exchange with remote
-    mbarriers only (which racecheck cannot model): 40 back-to-back launches over more rows
-    than co-resident clusters must all give the same bits, in place and out of place."""
+def test_f32_32k_kernel_repeatability_stress(hc):
+    """The fp32 n = 2^15 kernel (fwht_f32_stream_kernel: chunk slots refilled as soon as every
+    consumer warp has gathered its columns, results stored from registers; the HC_F32_PAIR build's
+    2-CTA cluster kernel synchronizes through remote mbarriers): 40 back-to-back launches over
+    more rows than SMs must all give the same bits, in place and out of place."""
     n, m = 32768, 300
     x = synthetic.generate(m, n, torch.float32, 13, device="cuda")
     ref = hc.hadacore_fwht(x)
