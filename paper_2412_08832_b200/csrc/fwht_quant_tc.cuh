@@ -158,7 +158,8 @@ __global__ void __launch_bounds__((EG * NE + NA + 2) * 32, 1)
     fwht_quant_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ CUtensorMap tm_q,
                          float* __restrict__ row_scale, const RowGrid g, float s_res) {
   constexpr int C = N / 256, R = 128 / C, Q = log2_n<N>() - 8;
-  static_assert(C >= 16 && C <= 128, "n = 4096 .. 32768");
+  static_assert(C >= 2 && C <= 128, "n = 512 .. 32768");
+  static_assert(C >= 16 || NE == 4, "rows of < 16 chunks: a thread holds its whole chunk (row max in-warp)");
   static_assert(NE == 4 || NE == 8, "epilogue warps");
   using PL = PlanL<Q>;
   constexpr int NLOOP = 1 << PL::nloop_bits;
@@ -383,7 +384,10 @@ __global__ void __launch_bounds__((EG * NE + NA + 2) * 32, 1)
     make_const_b<DT>(PL::mask_a, 1, Bc1);
     const uint32_t r0 = lane & 1, r1 = (lane >> 1) & 1, r2 = (lane >> 2) & 1, j0 = (lane >> 3) & 1,
                    j1 = (lane >> 4) & 1;
-    uint32_t c_l = 0, g_l = 0;
+    uint32_t c_l = 0, g_l = 0;  // chunk / granule bits supplied by the lane (as fwht_rows_kernel)
+    if constexpr (Q == 1) { c_l = r0; g_l = j0 | (r1 << 1) | (r2 << 2) | (j1 << 3); }
+    if constexpr (Q == 2) { c_l = r0 | (r1 << 1); g_l = j0 | (j1 << 1) | (r2 << 2); }
+    if constexpr (Q == 3) { c_l = r0 | (r1 << 1) | (r2 << 2); g_l = j0 | (j1 << 1); }
     if constexpr (Q == 4) { c_l = r0 | (r1 << 1) | (r2 << 2) | (j1 << 3); g_l = j0; }
     if constexpr (Q >= 5) { c_l = r0 | (r1 << 1) | (r2 << 2) | (j1 << 3) | (j0 << 4); g_l = 0; }
     constexpr int LOOP_SHIFT = 5 - PL::nloop_bits;
@@ -496,17 +500,18 @@ __global__ void __launch_bounds__((EG * NE + NA + 2) * 32, 1)
           a = absmax3(a, Rr[e], Rr[e + 1]);
         }
       }
-      // the row's maximum: 16-lane groups (C >= 16 chunks per row), then across warps
+      // the row's maximum: 16-lane groups (C >= 16 chunks per row), then across warps; rows of
+      // C < 16 chunks are C consecutive lanes of one warp
       uint32_t au = __float_as_uint(a);
 #pragma unroll
-      for (int o = 8; o >= 1; o >>= 1) au = max(au, __shfl_xor_sync(0xffffffffu, au, o));
-      if ((lane & 15) == 0) red[b * NE * 2 + ew * 2 + (lane >> 4)] = __uint_as_float(au);
+      for (int o = (C < 16 ? C : 16) / 2; o >= 1; o >>= 1) au = max(au, __shfl_xor_sync(0xffffffffu, au, o));
+      if (C >= 16 && (lane & 15) == 0) red[b * NE * 2 + ew * 2 + (lane >> 4)] = __uint_as_float(au);
       jitter(14, it);
       if (kTcCodeBuf && elect) bulk_wait_read<0>();  // this group's previous code store has read its buffer
       named_bar_sync(1 + eg, NE * 32);
       if (warp == 0 && lane == 0) trace(it, 5);
-      float am = 0.f;
-      {
+      float am = C < 16 ? __uint_as_float(au) : 0.f;
+      if constexpr (C >= 16) {
         constexpr int G = C / 16;  // 16-lane groups per row
 #pragma unroll
         for (int gi = 0; gi < G; ++gi) {
