@@ -137,6 +137,26 @@ constexpr bool kTcCodeBuf = HC_QTC_CB != 0;
 constexpr bool kTcSplit = kTcCodeBuf && HC_QTC_SPLIT != 0;
 constexpr int kTcTile = 65536;   // 128 chunks of 256 16-bit elements
 constexpr int kTcHBytes = 32768; // H_128, 16-bit, K-major SW128 (two 64-column atoms)
+// HC_QTC_H64 (INT4 with code buffers): B = H_64 only (8 KiB) and N = 64 MMAs, H_128 = H_2 (x) H_64
+// being [[H_64, H_64], [H_64, -H_64]]: output columns 0..63 of a half-chunk accumulate the two
+// K-halves against H_64, columns 64..127 the second K-half with the negate-B bit.  Twice the
+// A-operand reads, but 24 KiB of shared memory freed: 3 stages + one code buffer shared by the
+// two epilogue groups (each waits for the other's store to have read it).
+#ifndef HC_QTC_H64
+#define HC_QTC_H64 0  // measured 7-9 % slower for INT4 (profiles/r02_quant_tc_small_c_ab.txt): off
+#endif
+template <int QT>
+__host__ __device__ constexpr bool tc_h64() {
+  return HC_QTC_H64 != 0 && kTcCodeBuf && QT == QT_INT4;
+}
+template <int QT>
+__host__ __device__ constexpr int tc_hbytes() {
+  return tc_h64<QT>() ? 8192 : kTcHBytes;
+}
+template <int QT, int EG>
+__host__ __device__ constexpr int tc_ncb() {  // code buffers
+  return kTcCodeBuf ? (tc_h64<QT>() ? 1 : EG) : 0;
+}
 constexpr int kTcCols = 512;     // TMEM columns: two tiles x (y_lo 128 + y_hi 128)
 
 template <int QT>
@@ -145,8 +165,8 @@ __host__ __device__ constexpr int tc_code_bytes() {  // a tile's codes
 }
 template <int STAGES, int NE, int QT, int EG>
 __host__ __device__ constexpr int tc_smem_bytes() {
-  return STAGES * kTcTile + (kTcCodeBuf ? EG * tc_code_bytes<QT>() : 0) + kTcHBytes + int(sizeof(SchedCtl)) +
-         (5 * STAGES + 4) * 8 + 32 + 2 * NE * 2 * 4;
+  return STAGES * kTcTile + tc_ncb<QT, EG>() * tc_code_bytes<QT>() + tc_hbytes<QT>() + int(sizeof(SchedCtl)) +
+         (5 * STAGES + 5) * 8 + 32 + 2 * NE * 2 * 4;
 }
 
 // Template parameters: N row length (4096..32768), DT dtype, QT code type, STAGES ring
@@ -167,12 +187,16 @@ __global__ void __launch_bounds__((EG * NE + NA + 2) * 32, 1)
   constexpr int UA = (HC_QTC_UA >> PL::nx) > 0 ? (HC_QTC_UA >> PL::nx) : 1;  // phase-A items in flight per warp
   constexpr uint32_t IDESC = umma_idesc<DT>(128, 128);
   constexpr uint32_t IDESC_NEG = IDESC | (1u << 14);  // B negated: the -H_128 blocks of H_256
+  constexpr bool H64 = tc_h64<QT>();
+  constexpr int NCB = tc_ncb<QT, EG>();
+  constexpr uint32_t IDESC64 = umma_idesc<DT>(128, 64);
+  constexpr uint32_t IDESC64_NEG = IDESC64 | (1u << 14);
   const int64_t num_tiles = g.num_tiles;
 
   extern __shared__ __align__(1024) uint8_t smem[];
-  uint8_t* const codebuf = smem + STAGES * kTcTile;  // kTcCodeBuf: EG code buffers (1024-aligned)
-  uint8_t* const Hs = codebuf + (kTcCodeBuf ? EG * tc_code_bytes<QT>() : 0);
-  SchedCtl* ctl = reinterpret_cast<SchedCtl*>(Hs + kTcHBytes);
+  uint8_t* const codebuf = smem + STAGES * kTcTile;  // kTcCodeBuf: NCB code buffers (1024-aligned)
+  uint8_t* const Hs = codebuf + NCB * tc_code_bytes<QT>();
+  SchedCtl* ctl = reinterpret_cast<SchedCtl*>(Hs + tc_hbytes<QT>());
   uint64_t* full = reinterpret_cast<uint64_t*>(ctl + 1);  // TMA -> phase A
   uint64_t* adone = full + STAGES;                         // phase A -> MMA (NA arrivals)
   uint64_t* cready = adone + STAGES;                       // epilogue -> producer: codes staged (NE)
@@ -180,7 +204,8 @@ __global__ void __launch_bounds__((EG * NE + NA + 2) * 32, 1)
   uint64_t* tfull = ufree + STAGES;                        // [2] MMA -> epilogue (commit + arrive)
   uint64_t* tempty = tfull + 2;                            // [2] epilogue -> MMA (NE arrivals)
   uint64_t* full_hi = tempty + 2;                          // kTcSplit: TMA -> phase A, upper half
-  int* buf_tile = reinterpret_cast<int*>(full_hi + STAGES); // [2] tile id of each TMEM buffer
+  uint64_t* cbuf_free = full_hi + STAGES;                  // NCB == 1: the shared code buffer was read
+  int* buf_tile = reinterpret_cast<int*>(cbuf_free + 1);   // [2] tile id of each TMEM buffer
   int* buf_stage = buf_tile + 2;                           // [2] ... and the stage it came from
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(buf_stage + 2);
   float* red = reinterpret_cast<float*>(tmem_slot + 2);    // [2][NE * 2] row-max partials
@@ -203,12 +228,14 @@ __global__ void __launch_bounds__((EG * NE + NA + 2) * 32, 1)
       mbar_init(&tfull[b], 2);
       mbar_init(&tempty[b], NE);
     }
+    mbar_init(cbuf_free, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   // B operand: H_128 (unnormalized +-1, Sylvester order), row n (output element),
   // column k (input element), K-major SW128: atom k >> 6, line n, granule (k & 63) >> 3
-  for (int i = threadIdx.x; i < 128 * 16; i += blockDim.x) {
-    const int nrow = i >> 4, g = i & 15;
+  // (H64: H_64 only, one atom of 64 lines)
+  for (int i = threadIdx.x; i < (H64 ? 64 * 8 : 128 * 16); i += blockDim.x) {
+    const int nrow = H64 ? (i >> 3) : (i >> 4), g = H64 ? (i & 7) : (i & 15);
     uint32_t w[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
@@ -355,7 +382,20 @@ __global__ void __launch_bounds__((EG * NE + NA + 2) * 32, 1)
           break;
         }
         tc_fence_after();
-        if (!(HC_TC_DIAG & 4))
+        if (H64 && !(HC_TC_DIAG & 4)) {
+          // D_h = H_128 x_h as two 64-column halves: q = 0: x_h,lo H_64 + x_h,hi H_64; q = 1: x_h,lo H_64 - x_h,hi H_64
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int q = 0; q < 2; ++q)
+#pragma unroll
+              for (int kk = 0; kk < 8; ++kk) {
+                const uint32_t a = sm0 + s * kTcTile + (2 * h + (kk >> 2)) * 16384 + (kk & 3) * 32;
+                const uint32_t bh = hs0 + (kk & 3) * 32;
+                umma_f16(tmem + b * 256 + h * 128 + q * 64, umma_desc_sw128(a), umma_desc_sw128(bh),
+                         (q == 1 && kk >= 4) ? IDESC64_NEG : IDESC64, kk > 0 ? 1u : 0u);
+              }
+        } else if (!(HC_TC_DIAG & 4))
 #pragma unroll
         for (int h = 0; h < 2; ++h)
 #pragma unroll
@@ -508,6 +548,7 @@ __global__ void __launch_bounds__((EG * NE + NA + 2) * 32, 1)
       if (C >= 16 && (lane & 15) == 0) red[b * NE * 2 + ew * 2 + (lane >> 4)] = __uint_as_float(au);
       jitter(14, it);
       if (kTcCodeBuf && elect) bulk_wait_read<0>();  // this group's previous code store has read its buffer
+      if (NCB == 1 && elect && it > 0) mbar_wait(cbuf_free, uint32_t((it - 1) & 1));  // ... and the other group's
       named_bar_sync(1 + eg, NE * 32);
       if (warp == 0 && lane == 0) trace(it, 5);
       float am = C < 16 ? __uint_as_float(au) : 0.f;
@@ -537,7 +578,7 @@ __global__ void __launch_bounds__((EG * NE + NA + 2) * 32, 1)
       // pass 2: codes, staged in the tile's (consumed) stage as the 128-byte-swizzled image of
       // its contiguous code block: 128-byte lines L (E4M3 / INT8: L = 2 m + h, the half-chunk
       // h of chunk row m; INT4: L = m), 16-byte granule q at (q ^ (L & 7))
-      uint8_t* const qs = kTcCodeBuf ? codebuf + eg * tc_code_bytes<QT>() : smem + s * kTcTile;
+      uint8_t* const qs = kTcCodeBuf ? codebuf + (NCB == 1 ? 0 : eg) * tc_code_bytes<QT>() : smem + s * kTcTile;
 #pragma unroll 1
       for (int j = j0; j < j0 + ((HC_TC_DIAG & 16) ? 0 : NJ); ++j) {
         float P[32], Rr[32];
@@ -598,6 +639,10 @@ __global__ void __launch_bounds__((EG * NE + NA + 2) * 32, 1)
           const TileRows tr(g, tile);
           tma_store_4d(&tm_q, 0, 0, int(tr.j0), int(tr.i0), qs);
           bulk_commit();
+          if constexpr (NCB == 1) {  // the next tile (the other group) may write the buffer once this store read it
+            bulk_wait_read<0>();
+            mbar_arrive(cbuf_free);
+          }
         }
       }
       if (warp == 0 && lane == 0) trace(it, 6);

@@ -340,7 +340,8 @@ bool encode_tc_qmap(CUtensorMap* map, void* q, const Layout& L, int code_bytes, 
 template <int N, int DT, int QT>
 hadacore_status_t launch_qtc(const void* in, uint8_t* out_q, float* row_scale, const Layout& L, float scale,
                              cudaStream_t stream) {
-  constexpr int NA = HC_QTC_NA, NE = HC_QTC_NE, ST = kTcCodeBuf ? HC_QTC_ST_CB : HC_QTC_ST, EG = HC_QTC_EG;
+  constexpr int NA = HC_QTC_NA, NE = HC_QTC_NE, EG = HC_QTC_EG;
+  constexpr int ST = kTcCodeBuf ? (tc_h64<QT>() ? 3 : HC_QTC_ST_CB) : HC_QTC_ST;  // H64 frees room for a third stage
   constexpr int smem = tc_smem_bytes<ST, NE, QT, EG>();
   static_assert(smem <= 227 * 1024, "shared memory");
   static std::atomic<uint64_t> attr_done{0};
