@@ -32,6 +32,20 @@
 
 namespace hadacore {
 
+#ifndef HC_SMALL_PACKED
+#define HC_SMALL_PACKED 0  // 1: packed f32x2 butterflies in fwht_small_kernel -- measured mixed (quant n = 32, 64 -2..-6 %, Q/K quant n = 8..64 +3 %), off
+#endif
+constexpr bool kSmallPacked = HC_SMALL_PACKED != 0;
+// packed butterfly with the second operand times s: (a0, a1) <- b * s + a, (b0, b1) <- b * ns + a (ns = -s)
+// (fma.rn.f32x2, SASS FFMA2: IEEE-identical to the two scalar fmaf of each half)
+__device__ __forceinline__ void bfly2_sgn(float& a0, float& a1, float& b0, float& b1, float s, float ns) {
+  asm("{.reg .b64 a, b, p, q, r, t;\n mov.b64 a, {%0,%1};\n mov.b64 b, {%2,%3};\n mov.b64 p, {%4,%4};\n"
+      " mov.b64 q, {%5,%5};\n fma.rn.f32x2 r, b, p, a;\n fma.rn.f32x2 t, b, q, a;\n"
+      " mov.b64 {%0,%1}, r;\n mov.b64 {%2,%3}, t;}"
+      : "+f"(a0), "+f"(a1), "+f"(b0), "+f"(b1)
+      : "f"(s), "f"(ns));
+}
+
 __device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
 #if HC_STORE_HINT  // evict-first in L2, as the TMA tensor stores (fwht_kernel.cuh)
   asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(dst),
@@ -278,14 +292,20 @@ __global__ void __launch_bounds__((NT + 1) * 32, 1)
       for (int u = 0; u < U; ++u) {
         // element bits (inside a granule; for n <= 8 each row of n elements is
         // contiguous in the granule, so bits 0..k-1 never cross rows): P:50-64 butterflies
+        // (bits >= 1 as packed FADD2 / FFMA2 pairs of elements e, e + 1: the same IEEE
+        // operations as the scalar form, half the issue slots; bit 0 pairs e with e + 1 itself)
 #pragma unroll
         for (int b = 0; b < KE; ++b)
 #pragma unroll
           for (int e = 0; e < 8 * G; ++e)
             if (!(e & (1 << b))) {
-              const float p0 = v[u][e], p1 = v[u][e | (1 << b)];
-              v[u][e] = p0 + p1;
-              v[u][e | (1 << b)] = p0 - p1;
+              if (b == 0 || !kSmallPacked) {
+                const float p0 = v[u][e], p1 = v[u][e | (1 << b)];
+                v[u][e] = p0 + p1;
+                v[u][e | (1 << b)] = p0 - p1;
+              } else if (!(e & 1)) {
+                bfly2(v[u][e], v[u][e + 1], v[u][e | (1 << b)], v[u][(e | (1 << b)) + 1]);
+              }
             }
         // granule bits: butterflies with the second operand times sg[b] (= the plain
         // butterfly followed by a swap across bit b when c has bit b set)
@@ -294,9 +314,13 @@ __global__ void __launch_bounds__((NT + 1) * 32, 1)
 #pragma unroll
           for (int e = 0; e < 8 * G; ++e)
             if (!(e & (8 << b))) {
-              const float p0 = v[u][e], p1 = v[u][e | (8 << b)];
-              v[u][e] = fmaf(p1, sg[b], p0);
-              v[u][e | (8 << b)] = fmaf(p1, -sg[b], p0);
+              if (!kSmallPacked) {
+                const float p0 = v[u][e], p1 = v[u][e | (8 << b)];
+                v[u][e] = fmaf(p1, sg[b], p0);
+                v[u][e | (8 << b)] = fmaf(p1, -sg[b], p0);
+              } else if (!(e & 1)) {
+                bfly2_sgn(v[u][e], v[u][e + 1], v[u][e | (8 << b)], v[u][(e | (8 << b)) + 1], sg[b], -sg[b]);
+              }
             }
       }
       if constexpr (QT >= 0) {
