@@ -35,6 +35,9 @@ namespace hadacore {
 #ifndef HC_SMALL_PACKED
 #define HC_SMALL_PACKED 0  // 1: packed f32x2 butterflies in fwht_small_kernel -- measured mixed (quant n = 32, 64 -2..-6 %, Q/K quant n = 8..64 +3 %), off
 #endif
+#ifndef HC_SMALL_PACKED_GRID
+#define HC_SMALL_PACKED_GRID 1  // ... but on for the row-grid (Q/K head) instantiations: Q/K quant n = 8..64 +3 %
+#endif
 constexpr bool kSmallPacked = HC_SMALL_PACKED != 0;
 // packed butterfly with the second operand times s: (a0, a1) <- b * s + a, (b0, b1) <- b * ns + a (ns = -s)
 // (fma.rn.f32x2, SASS FFMA2: IEEE-identical to the two scalar fmaf of each half)
@@ -107,6 +110,7 @@ __global__ void __launch_bounds__((NT + 1) * 32, 1)
   static_assert(!GRID || N >= 8, "row grids: n >= 8 (16-byte TMA rows)");
 
   constexpr int CODE_STAGE = small_code_stage_bytes<N, QT, GRID, TILE_BYTES>();
+  constexpr bool PACKED = kSmallPacked || (GRID && HC_SMALL_PACKED_GRID != 0);  // f32x2 butterflies
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* const codes = smem + STAGES * TILE_BYTES;  // CODE_STAGE bytes per stage (may be 0)
   SchedCtl* ctl = reinterpret_cast<SchedCtl*>(smem + STAGES * (TILE_BYTES + CODE_STAGE));
@@ -299,7 +303,7 @@ __global__ void __launch_bounds__((NT + 1) * 32, 1)
 #pragma unroll
           for (int e = 0; e < 8 * G; ++e)
             if (!(e & (1 << b))) {
-              if (b == 0 || !kSmallPacked) {
+              if (b == 0 || !PACKED) {
                 const float p0 = v[u][e], p1 = v[u][e | (1 << b)];
                 v[u][e] = p0 + p1;
                 v[u][e | (1 << b)] = p0 - p1;
@@ -314,7 +318,7 @@ __global__ void __launch_bounds__((NT + 1) * 32, 1)
 #pragma unroll
           for (int e = 0; e < 8 * G; ++e)
             if (!(e & (8 << b))) {
-              if (!kSmallPacked) {
+              if (!PACKED) {
                 const float p0 = v[u][e], p1 = v[u][e | (8 << b)];
                 v[u][e] = fmaf(p1, sg[b], p0);
                 v[u][e | (8 << b)] = fmaf(p1, -sg[b], p0);
