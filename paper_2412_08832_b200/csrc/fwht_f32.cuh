@@ -896,6 +896,10 @@ __global__ void __launch_bounds__((NT + 1) * 32, 1)
 // bits 10..14 as register butterflies, `scale`, 8-byte stores straight to global memory.
 // A slot is thus occupied for one chunk's transform only, and S - 1 chunks of loads stay
 // in flight all the time.
+#ifndef HC_F32_STREAM_CLC
+#define HC_F32_STREAM_CLC 1  // 0: static round-robin rows over a persistent grid (A/B)
+#endif
+constexpr bool kStreamClc = kClc && HC_F32_STREAM_CLC != 0;
 template <int CH, int S, int NT>
 __global__ void __launch_bounds__((NT + 1) * 32, 1)
     fwht_f32_stream_kernel(const float* __restrict__ in, float* __restrict__ out, int64_t m, float scale) {
@@ -904,12 +908,14 @@ __global__ void __launch_bounds__((NT + 1) * 32, 1)
   static_assert(NT * 32 == 512, "a thread holds columns 2 tid, 2 tid + 1 of the 1024");
   static_assert(CH >= 1024 && CH % 1024 == 0 && CPR >= 2 && S >= 2, "chunks");
   extern __shared__ __align__(1024) uint8_t smem[];
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * CB);
+  SchedCtl* ctl = reinterpret_cast<SchedCtl*>(smem + S * CB);  // stage_tile[s] = the row of slot s (-1: end)
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * CB + sizeof(SchedCtl));
   uint64_t* empty = full + S;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t rows = m > int64_t(blockIdx.x) ? (m - 1 - int64_t(blockIdx.x)) / gridDim.x + 1 : 0;
+  static_assert(S <= 16, "SchedCtl::stage_tile");
 
   if (threadIdx.x == 0) {
+    mbar_init(&ctl->clc_bar, 1);
 #pragma unroll
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
@@ -922,17 +928,39 @@ __global__ void __launch_bounds__((NT + 1) * 32, 1)
   pdl_launch_dependents();
 
   if (warp == NT) {
+    // rows: this CTA's own (blockIdx.x), then rows of not-yet-launched CTAs taken over with
+    // cluster launch control (kClc; as fwht_f32_fast_kernel), or static round-robin
     if (lane == 0) {
       pdl_wait();
       const uint64_t pol = policy_evict_first();
-      const int64_t total = rows * CPR;
-      for (int64_t u = 0; u < total; ++u) {
-        const int s = int(u % S);
-        if (u >= S) mbar_wait(&empty[s], uint32_t(((u / S) - 1) & 1));  // chunk u - S released
-        jitter(12, uint32_t(u));
-        const int64_t r = int64_t(blockIdx.x) + (u / CPR) * gridDim.x;
-        mbar_arrive_expect_tx(&full[s], CB);
-        bulk_g2s(smem + s * CB, in + r * N + (u % CPR) * CH, CB, &full[s], pol);
+      uint32_t clc_phase = 0;
+      int64_t u = 0;  // chunk sequence number of this CTA
+      auto slot = [&](int64_t uu) {
+        const int s = int(uu % S);
+        if (uu >= S) mbar_wait(&empty[s], uint32_t(((uu / S) - 1) & 1));  // chunk uu - S released
+        jitter(12, uint32_t(uu));
+        return s;
+      };
+      for (int64_t row = blockIdx.x;;) {
+        if (row < 0 || row >= m) {  // end: the consumers stop at the next slot
+          const int s = slot(u);
+          ctl->stage_tile[s] = -1;
+          mbar_arrive(&full[s]);
+          break;
+        }
+        if constexpr (kStreamClc) clc_request(ctl);
+#pragma unroll 1
+        for (int c = 0; c < CPR; ++c, ++u) {
+          const int s = slot(u);
+          ctl->stage_tile[s] = int(row);
+          mbar_arrive_expect_tx(&full[s], CB);
+          bulk_g2s(smem + s * CB, in + row * N + c * CH, CB, &full[s], pol);
+        }
+        if constexpr (kStreamClc) {
+          row = clc_result(ctl, clc_phase);
+        } else {
+          row += gridDim.x;
+        }
       }
     }
     return;
@@ -943,13 +971,19 @@ __global__ void __launch_bounds__((NT + 1) * 32, 1)
   float al[3];
 #pragma unroll
   for (int b = 0; b < 3; ++b) al[b] = ((c >> b) & 1u) ? -1.f : 1.f;
-  for (int64_t k = 0; k < rows; ++k) {
+  for (int k = 0;; ++k) {  // (32-bit chunk counters: at most 2 m chunks per CTA)
+    {
+      const int u0 = k * CPR;
+      mbar_wait(&full[u0 % S], uint32_t((u0 / S) & 1));
+    }
+    const int row = ctl->stage_tile[(k * CPR) % S];
+    if (row < 0) break;
     float v[32][2];  // value t of columns 2 tid, 2 tid + 1 (element t * 1024 + col)
 #pragma unroll
     for (int cc = 0; cc < CPR; ++cc) {
-      const int64_t u = k * CPR + cc;
-      const int s = int(u % S);
-      mbar_wait(&full[s], uint32_t((u / S) & 1));
+      const int u = k * CPR + cc;
+      const int s = u % S;
+      if (cc > 0) mbar_wait(&full[s], uint32_t((u / S) & 1));
       float* const tb = reinterpret_cast<float*>(smem + s * CB);
       // phase 0: bits 0..4, 32 contiguous floats per item
 #pragma unroll 1
@@ -1014,7 +1048,7 @@ __global__ void __launch_bounds__((NT + 1) * 32, 1)
             v[e][q] = p0 + p1;
             v[e | (1 << b)][q] = p0 - p1;
           }
-    float* const orow = out + (int64_t(blockIdx.x) + k * gridDim.x) * N + 2 * tid;
+    float* const orow = out + int64_t(row) * N + 2 * tid;
 #pragma unroll
     for (int t = 0; t < 32; ++t)
       *reinterpret_cast<float2*>(orow + t * 1024) = make_float2(v[t][0] * scale, v[t][1] * scale);

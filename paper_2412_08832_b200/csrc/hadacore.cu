@@ -635,7 +635,7 @@ hadacore_status_t launch_f32_32k(const void* in, void* out, int64_t m, float sca
 #if HC_F32_STREAM
   constexpr int ch = HC_STREAM_CH, nt = 16;
   constexpr int slots = (227 * 1024 - 256) / (ch * 4);
-  constexpr int smem = slots * ch * 4 + 2 * slots * 8;
+  constexpr int smem = slots * ch * 4 + int(sizeof(SchedCtl)) + 2 * slots * 8;
   auto kern = fwht_f32_stream_kernel<ch, slots, nt>;
 #else
   constexpr int ch = HC_RING_CH, nt = HC_RING_NT;
@@ -648,7 +648,10 @@ hadacore_status_t launch_f32_32k(const void* in, void* out, int64_t m, float sca
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return HADACORE_ERR_CUDA;
   if (!ensure_smem_attr(kern, smem, attr_done, dev)) return HADACORE_ERR_CUDA;
-  const int64_t ctas = m < int64_t(sm_count(dev)) ? m : int64_t(sm_count(dev));
+  // fwht_f32_stream_kernel: one CTA per row under CLC (resident CTAs take over the rest);
+  // fwht_f32_ring_kernel: a persistent grid with static rows
+  const int64_t cap = (HC_F32_STREAM && kStreamClc) ? int64_t(INT32_MAX) : int64_t(sm_count(dev));
+  const int64_t ctas = m < cap ? m : cap;
   if (launch_pdl(kern, int(ctas), (nt + 1) * 32, smem, stream, static_cast<const float*>(in),
                  static_cast<float*>(out), m, scale) != cudaSuccess)
     return HADACORE_ERR_CUDA;
