@@ -905,7 +905,8 @@ __global__ void __launch_bounds__((NT + 1) * 32, 1)
     fwht_f32_stream_kernel(const float* __restrict__ in, float* __restrict__ out, int64_t m, float scale) {
   constexpr int N = 32768, CPR = N / CH, CB = CH * 4;
   constexpr int TPC = CH / 1024;  // 1024-blocks (values of a cross-chunk column) per chunk
-  static_assert(NT * 32 == 512, "a thread holds columns 2 tid, 2 tid + 1 of the 1024");
+  constexpr int CPT = 1024 / (NT * 32);  // adjacent columns of the cross-chunk phase per thread
+  static_assert(CPT == 2 || CPT == 4, "8 or 16 consumer warps");
   static_assert(CH >= 1024 && CH % 1024 == 0 && CPR >= 2 && S >= 2, "chunks");
   extern __shared__ __align__(1024) uint8_t smem[];
   SchedCtl* ctl = reinterpret_cast<SchedCtl*>(smem + S * CB);  // stage_tile[s] = the row of slot s (-1: end)
@@ -978,7 +979,7 @@ __global__ void __launch_bounds__((NT + 1) * 32, 1)
     }
     const int row = ctl->stage_tile[(k * CPR) % S];
     if (row < 0) break;
-    float v[32][2];  // value t of columns 2 tid, 2 tid + 1 (element t * 1024 + col)
+    float v[32][CPT];  // value t of columns CPT tid .. CPT tid + CPT - 1 (element t * 1024 + col)
 #pragma unroll
     for (int cc = 0; cc < CPR; ++cc) {
       const int u = k * CPR + cc;
@@ -1026,9 +1027,17 @@ __global__ void __launch_bounds__((NT + 1) * 32, 1)
       // this thread's values of the cross-chunk phase, then release the slot
 #pragma unroll
       for (int j = 0; j < TPC; ++j) {
-        const float2 g = *reinterpret_cast<const float2*>(tb + j * 1024 + 2 * tid);
-        v[cc * TPC + j][0] = g.x;
-        v[cc * TPC + j][1] = g.y;
+        if constexpr (CPT == 4) {
+          const float4 g = *reinterpret_cast<const float4*>(tb + j * 1024 + 4 * tid);
+          v[cc * TPC + j][0] = g.x;
+          v[cc * TPC + j][1] = g.y;
+          v[cc * TPC + j][2] = g.z;
+          v[cc * TPC + j][3] = g.w;
+        } else {
+          const float2 g = *reinterpret_cast<const float2*>(tb + j * 1024 + 2 * tid);
+          v[cc * TPC + j][0] = g.x;
+          v[cc * TPC + j][1] = g.y;
+        }
       }
       __syncwarp();
       if (lane == 0) {
@@ -1043,15 +1052,20 @@ __global__ void __launch_bounds__((NT + 1) * 32, 1)
       for (int e = 0; e < 32; ++e)
         if (!(e & (1 << b)))
 #pragma unroll
-          for (int q = 0; q < 2; ++q) {
+          for (int q = 0; q < CPT; ++q) {
             const float p0 = v[e][q], p1 = v[e | (1 << b)][q];
             v[e][q] = p0 + p1;
             v[e | (1 << b)][q] = p0 - p1;
           }
-    float* const orow = out + int64_t(row) * N + 2 * tid;
+    float* const orow = out + int64_t(row) * N + CPT * tid;
 #pragma unroll
     for (int t = 0; t < 32; ++t)
-      *reinterpret_cast<float2*>(orow + t * 1024) = make_float2(v[t][0] * scale, v[t][1] * scale);
+      if constexpr (CPT == 4) {
+        *reinterpret_cast<float4*>(orow + t * 1024) =
+            make_float4(v[t][0] * scale, v[t][1] * scale, v[t][2] * scale, v[t][3] * scale);
+      } else {
+        *reinterpret_cast<float2*>(orow + t * 1024) = make_float2(v[t][0] * scale, v[t][1] * scale);
+      }
   }
 }
 

@@ -633,7 +633,10 @@ hadacore_status_t launch_f32_32k(const void* in, void* out, int64_t m, float sca
 #define HC_STREAM_CH 16384
 #endif
 #if HC_F32_STREAM
-  constexpr int ch = HC_STREAM_CH, nt = 16;
+#ifndef HC_STREAM_NT
+#define HC_STREAM_NT 16
+#endif
+  constexpr int ch = HC_STREAM_CH, nt = HC_STREAM_NT;
   constexpr int slots = (227 * 1024 - 256) / (ch * 4);
   constexpr int smem = slots * ch * 4 + int(sizeof(SchedCtl)) + 2 * slots * 8;
   auto kern = fwht_f32_stream_kernel<ch, slots, nt>;
