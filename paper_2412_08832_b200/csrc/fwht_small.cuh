@@ -32,6 +32,9 @@
 
 namespace hadacore {
 
+#ifndef HC_SMALL_SPLIT
+#define HC_SMALL_SPLIT 0  // bit 0: n = 32, bit 1: n = 64 fused quantization with half rows per lane (SPLIT): measured 15-25 % slower, off
+#endif
 #ifndef HC_SMALL_PACKED
 #define HC_SMALL_PACKED 0  // 1: packed f32x2 butterflies in fwht_small_kernel -- measured mixed (quant n = 32, 64 -2..-6 %, Q/K quant n = 8..64 +3 %), off
 #endif
@@ -102,9 +105,13 @@ __global__ void __launch_bounds__((NT + 1) * 32, 1)
                       float* __restrict__ row_scale = nullptr, const __grid_constant__ CUtensorMap tm_in = {},
                       const __grid_constant__ CUtensorMap tm_out = {}, const RowGrid g = {}) {
   constexpr int K = log2_n<N>();
-  constexpr int G = N >= 8 ? N / 8 : 1;            // granules per item
+  // SPLIT (fused quantization of contiguous rows, n = 32, 64): an item is HALF a row, held by
+  // lanes 2r, 2r + 1; the top index bit is a butterfly across the lane pair (shuffles), the
+  // row maximum one more shuffle -- half the registers of a whole row per lane
+  constexpr bool SPLIT = QT >= 0 && !GRID && (N == 64 || N == 32) && (HC_SMALL_SPLIT & (N / 32)) != 0;
+  constexpr int G = N >= 8 ? N / 8 / (SPLIT ? 2 : 1) : 1;  // granules per item
   constexpr int ITEM_BYTES = 16 * G;
-  constexpr int KG = N >= 16 ? K - 3 : 0;          // granule bits of an item
+  constexpr int KG = N >= 16 ? K - 3 - (SPLIT ? 1 : 0) : 0;  // granule bits of an item
   constexpr int KE = K < 3 ? K : 3;                // element bits inside a granule
   static_assert(TILE_BYTES % ITEM_BYTES == 0 && STAGES <= 16, "tile layout");
   static_assert(!GRID || N >= 8, "row grids: n >= 8 (16-byte TMA rows)");
@@ -327,6 +334,20 @@ __global__ void __launch_bounds__((NT + 1) * 32, 1)
               }
             }
       }
+      if constexpr (SPLIT) {
+        // the top index bit across the lane pair (same slot -> granule map and slot signs in
+        // both lanes: c depends on lane >> 1): lane 2r keeps a + b, lane 2r + 1 a - b, the
+        // P:50-64 butterfly in the same order and fp32 rounding as the in-lane version
+        const unsigned pair = __activemask();  // partners are active together (whole rows)
+        const bool hi = lane & 1;
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+          for (int e = 0; e < 8 * G; ++e) {
+            const float p = __shfl_xor_sync(pair, v[u][e], 1);
+            v[u][e] = hi ? p - v[u][e] : v[u][e] + p;
+          }
+      }
       if constexpr (QT >= 0) {
         // ---- fused quantization: rows are in-lane (n >= 16: the item; n <= 8: 8/n rows of
         // the granule, contiguous in v); y = v * sc[j], so |y| = |v| |scale|
@@ -349,6 +370,7 @@ __global__ void __launch_bounds__((NT + 1) * 32, 1)
             float a = 0.f;
 #pragma unroll
             for (int e = 0; e < (N >= 8 ? 8 * G : N); ++e) a = absmax_nan(a, v[u][rr * N + e]);
+            if constexpr (SPLIT) a = absmax_nan(a, __shfl_xor_sync(__activemask(), a, 1));  // |.| of a max is itself
             if (quant_fast_range(a, 0x1p100f)) {
               scr[rr] = a * q_ss;                 // max |y| / Q
               mul[rr] = q_qs * rcp_ftz(a);        // Q / max |v|, times sign(scale)
@@ -369,7 +391,7 @@ __global__ void __launch_bounds__((NT + 1) * 32, 1)
           } else if constexpr (RI == 2) {
             if (whole) *reinterpret_cast<float2*>(row_scale + row0) = make_float2(scr[0], scr[1]);
           } else {
-            row_scale[row0] = scr[0];
+            if (!SPLIT || !(lane & 1)) row_scale[row0] = scr[0];
           }
           if (!whole)  // partial granule (n <= 4): the valid rows only
             for (int rr = 0; rr < RI; ++rr)
@@ -397,7 +419,7 @@ __global__ void __launch_bounds__((NT + 1) * 32, 1)
               const uint32_t cw[2] = {QT == QT_INT4 ? __byte_perm(c0, c1, 0x5410) : c0, c1};
               for (int bq = 0; bq < valid; ++bq) out_q[cbyte + bq] = uint8_t(cw[bq >> 2] >> (8 * (bq & 3)));
             } else if (STAGE_ALWAYS || (CODE_STAGE > 0 && stage_q)) {  // into the stage's code buffer (row `item`)
-              uint8_t* dst = codes + s * CODE_STAGE + ((int64_t(item) * N + 8 * int64_t(uint32_t(j) ^ c)) * CB2) / 2;
+              uint8_t* dst = codes + s * CODE_STAGE + ((int64_t(item) * (8 * G) + 8 * int64_t(uint32_t(j) ^ c)) * CB2) / 2;
               if constexpr (QT == QT_INT4) {
                 asm volatile("st.shared.u32 [%0], %1;" ::"r"(smem_addr(dst)), "r"(__byte_perm(c0, c1, 0x5410)) : "memory");
               } else {
