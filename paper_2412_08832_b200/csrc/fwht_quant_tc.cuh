@@ -636,6 +636,7 @@ __global__ void __launch_bounds__((EG * NE + NA + 2) * 32, 1)
       if constexpr (kTcCodeBuf) {  // the group's codes are staged: one TMA tensor store of them
         named_bar_sync(1 + eg, NE * 32);
         if (elect) {
+          jitter(16, it);
           const TileRows tr(g, tile);
           tma_store_4d(&tm_q, 0, 0, int(tr.j0), int(tr.i0), qs);
           bulk_commit();
