@@ -76,8 +76,8 @@ template <int N> struct Tuned : Tuned0<N> {};
 // and the CTA count to the register file (paired sweeps, profiles/r01_quant_tune_v3.txt).  HC_QTUNE = "nt,tkb,st,ctas"
 // overrides n = 512..8192 (A/B builds).
 template <int N> struct TunedQ0     { static constexpr int nt = 8, tkb = 16, st = 3, u = 1, ctas = 3; };
-template <> struct TunedQ0<128>     { static constexpr int nt = 8, tkb = 32, st = 2, u = 1, ctas = 3; };
-template <> struct TunedQ0<256>     { static constexpr int nt = 8, tkb = 32, st = 2, u = 1, ctas = 3; };
+template <> struct TunedQ0<128>     { static constexpr int nt = 8, tkb = 32, st = 2, u = 4, ctas = 3; };  // u = 4 (was 1): INT4 +16 %, Q/K quant (profiles/r02_quant_n128_ab.txt)
+template <> struct TunedQ0<256>     { static constexpr int nt = 8, tkb = 32, st = 2, u = 2, ctas = 3; };  // u = 2 (was 1): INT4 +2..5 %
 template <> struct TunedQ0<8192>    { static constexpr int nt = 8, tkb = 32, st = 3, u = 2, ctas = 2; };
 template <> struct TunedQ0<16384>   { static constexpr int nt = 8, tkb = 32, st = 3, u = 1, ctas = 2; };
 template <> struct TunedQ0<32768>   { static constexpr int nt = 16, tkb = 64, st = 3, u = 1, ctas = 1; };
