@@ -75,10 +75,13 @@ template <int N> struct Tuned : Tuned0<N> {};
 // per lane) in registers across the row-max barrier, so tiles are sized to IW = 4..8
 // and the CTA count to the register file (paired sweeps, profiles/r01_quant_tune_v3.txt).  HC_QTUNE = "nt,tkb,st,ctas"
 // overrides n = 512..8192 (A/B builds).
-template <int N> struct TunedQ0     { static constexpr int nt = 8, tkb = 16, st = 3, u = 1, ctas = 3; };
+// round 2: 4 items in flight per warp (u = 4; E4M3/INT8 n = 512..8192 sweep 6.17 -> 6.48 TB/s), 4 warps x 4 CTAs
+// at n = 2048 and 8192 (+2..5 % there; profiles/r02_quant_u_ab.txt)
+template <int N> struct TunedQ0     { static constexpr int nt = 8, tkb = 16, st = 3, u = 4, ctas = 3; };
+template <> struct TunedQ0<2048>    { static constexpr int nt = 4, tkb = 16, st = 3, u = 4, ctas = 4; };
 template <> struct TunedQ0<128>     { static constexpr int nt = 8, tkb = 32, st = 2, u = 4, ctas = 3; };  // u = 4 (was 1): INT4 +16 %, Q/K quant (profiles/r02_quant_n128_ab.txt)
 template <> struct TunedQ0<256>     { static constexpr int nt = 8, tkb = 32, st = 2, u = 2, ctas = 3; };  // u = 2 (was 1): INT4 +2..5 %
-template <> struct TunedQ0<8192>    { static constexpr int nt = 8, tkb = 32, st = 3, u = 2, ctas = 2; };
+template <> struct TunedQ0<8192>    { static constexpr int nt = 4, tkb = 16, st = 3, u = 4, ctas = 4; };
 template <> struct TunedQ0<16384>   { static constexpr int nt = 8, tkb = 32, st = 3, u = 1, ctas = 2; };
 template <> struct TunedQ0<32768>   { static constexpr int nt = 16, tkb = 64, st = 3, u = 1, ctas = 1; };
 #ifdef HC_QTUNE  // A/B builds: HC_QTUNE_N = the n to override (0: every n in 512..8192)
