@@ -290,7 +290,12 @@ bool ensure_smem_attr(Kern kern, int smem, std::atomic<uint64_t>& done, int dev)
 #define HC_QTC_MINN 16384  // E4M3 / INT8; per-(qtype, n) A/B: profiles/r02_quant_tc_ab.txt
 #endif
 #ifndef HC_QTC_MINN4
-#define HC_QTC_MINN4 512  // INT4 (half the code bytes: the register epilogue is issue-bound there; n = 512..2048 +4..13 %, profiles/r02_quant_tc_small_c_ab.txt)
+#define HC_QTC_MINN4 16384  // INT4 from this n, plus n = HC_QTC_INT4_N below (after the register epilogue's u = 4
+                           // retune it leads at n = 1024..8192 by 1..10 %, the tcgen05 kernel at 512 by 6..11 %:
+                           // profiles/r02_quant_u_ab.txt; before it, tcgen05 led from 512: r02_quant_tc_small_c_ab.txt)
+#endif
+#ifndef HC_QTC_INT4_N
+#define HC_QTC_INT4_N 512
 #endif
 #ifndef HC_QTC_NA
 #define HC_QTC_NA 8
@@ -368,7 +373,8 @@ hadacore_status_t launch_qtc(const void* in, uint8_t* out_q, float* row_scale, c
 template <int N, int DT, int QT>
 hadacore_status_t launch(const void* in, void* out, uint8_t* out_q, float* row_scale, const Layout& L, float scale,
                          cudaStream_t stream) {
-  if constexpr (QT >= 0 && N >= 512 && HC_QTC_MINN > 0 && N >= (QT == QT_INT4 ? HC_QTC_MINN4 : HC_QTC_MINN)) {
+  if constexpr (QT >= 0 && N >= 512 && HC_QTC_MINN > 0 &&
+                (N >= (QT == QT_INT4 ? HC_QTC_MINN4 : HC_QTC_MINN) || (QT == QT_INT4 && N == HC_QTC_INT4_N))) {
     return launch_qtc<N, DT, QT>(in, out_q, row_scale, L, scale, stream);
   }
 #ifndef HC_TUNE
