@@ -143,7 +143,10 @@ constexpr int QT_SMALLM = -2;  // kernels treat every QT < 0 as the plain transf
 template <int N> struct TunedMidM0 { static constexpr int nt = 8, tkb = 8, st = 4, u = 1, ctas = 2; };
 #ifdef HC_MIDM_NT
 template <int N> struct TunedMidM {
-  static constexpr int nt = HC_MIDM_NT, tkb = HC_MIDM_TKB, st = HC_MIDM_ST, u = 1, ctas = HC_MIDM_CTAS;
+#ifndef HC_MIDM_U
+#define HC_MIDM_U 1
+#endif
+  static constexpr int nt = HC_MIDM_NT, tkb = HC_MIDM_TKB, st = HC_MIDM_ST, u = HC_MIDM_U, ctas = HC_MIDM_CTAS;
 };
 #else
 template <int N> struct TunedMidM : TunedMidM0<N> {};
