@@ -68,3 +68,35 @@ def test_fuzz_strided_and_quant(hc, case):
     assert torch.equal(q.view(torch.uint8), q2.view(torch.uint8)) and torch.equal(s, s2), (n, heads, tokens, qt)
     ref = oracle.fwht(view.contiguous().reshape(-1, n).cpu().double().numpy())
     assert rel_err(y.reshape(-1, n).cpu().double().numpy(), ref) <= TOL[dt]
+
+
+@pytest.mark.parametrize("case", range(24))
+def test_fuzz_quant_sampled_rows(hc, case):
+    """Fused quantization over random (n, m, dtype, qtype, scale) with up to 2^22 elements -- several
+    tiles per CTA and a ragged last tile for every kernel family and launch-table entry -- checked on
+    sampled rows (first, last, random) against the fp64 oracle: row scales within the transform
+    tolerance and the dequantized rows within the quantization bound of test_gpu_quant.py."""
+    from test_gpu_quant import gpu_codes, code_values
+    rng = np.random.default_rng(3000 + case)
+    n = 1 << int(rng.integers(1, 16))
+    m = int(rng.integers(1, max(2, (1 << 22) // n)))
+    dt = [torch.float16, torch.bfloat16][int(rng.integers(0, 2))]
+    qt = ["e4m3", "int8", "int4"][int(rng.integers(0, 3))]
+    scale = float(rng.choice([1.0 / math.sqrt(n), 1.0, 0.37]))
+    x = synthetic.generate(m, n, dt, 700 + case, dist="D1" if case % 2 else "D0").cuda()
+    q, s = hc.hadacore_fwht_quant(x, qtype=qt, scale=scale)
+    rows = sorted(set([0, m - 1] + rng.integers(0, m, 62).tolist()))
+    codes = gpu_codes(q[rows], qt)
+    s_gpu = s[rows].cpu().double().numpy()
+    y = oracle.fwht(x[rows].cpu().double().numpy(), scale=scale)
+    _, s_ref = oracle.quantize_rows(y, qt)
+    tol = TOL[dt]
+    assert np.all(np.abs(s_gpu - s_ref) <= tol * s_ref), (n, m, dt, qt, scale)
+    deq = code_values(codes, qt) * s_gpu[:, None]
+    err = np.linalg.norm(deq - y, axis=1)
+    ny = np.linalg.norm(y, axis=1)
+    if qt != "e4m3":
+        bound = s_gpu / 2 * math.sqrt(n) + tol * ny
+    else:
+        bound = (2.0 ** -4 + tol) * ny + 2.0 ** -10 * s_gpu * math.sqrt(n)
+    assert np.all(err <= bound * 1.0001), (n, m, dt, qt, scale, float(np.max(err / bound)))
