@@ -896,6 +896,9 @@ __global__ void __launch_bounds__((NT + 1) * 32, 1)
 // bits 10..14 as register butterflies, `scale`, 8-byte stores straight to global memory.
 // A slot is thus occupied for one chunk's transform only, and S - 1 chunks of loads stay
 // in flight all the time.
+#ifndef HC_STREAM_ST128
+#define HC_STREAM_ST128 0  // 1: lane-pair swap + 16-byte stores of the results -- measured 6.43 -> 5.90 TB/s, off
+#endif
 #ifndef HC_F32_STREAM_CLC
 #define HC_F32_STREAM_CLC 1  // 0: static round-robin rows over a persistent grid (A/B)
 #endif
@@ -1058,6 +1061,21 @@ __global__ void __launch_bounds__((NT + 1) * 32, 1)
             v[e | (1 << b)][q] = p0 - p1;
           }
     float* const orow = out + int64_t(row) * N + CPT * tid;
+    if constexpr (CPT == 2 && HC_STREAM_ST128) {
+      // lane pairs swap halves so that each lane stores 4 adjacent columns of every other
+      // block: 16 STG.128 per lane instead of 32 STG.64 (fewer entries in the store queue)
+      const bool odd = lane & 1;
+      float* const orow4 = out + int64_t(row) * N + 4 * (tid >> 1);
+#pragma unroll
+      for (int t2 = 0; t2 < 16; ++t2) {
+        const float s0 = odd ? v[2 * t2][0] : v[2 * t2 + 1][0], s1 = odd ? v[2 * t2][1] : v[2 * t2 + 1][1];
+        const float m0 = odd ? v[2 * t2 + 1][0] : v[2 * t2][0], m1 = odd ? v[2 * t2 + 1][1] : v[2 * t2][1];
+        const float r0 = __shfl_xor_sync(0xffffffffu, s0, 1), r1 = __shfl_xor_sync(0xffffffffu, s1, 1);
+        const float4 o = odd ? make_float4(r0 * scale, r1 * scale, m0 * scale, m1 * scale)
+                             : make_float4(m0 * scale, m1 * scale, r0 * scale, r1 * scale);
+        *reinterpret_cast<float4*>(orow4 + (2 * t2 + (odd ? 1 : 0)) * 1024) = o;
+      }
+    } else
 #pragma unroll
     for (int t = 0; t < 32; ++t)
       if constexpr (CPT == 4) {
